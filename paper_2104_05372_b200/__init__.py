@@ -1,0 +1,324 @@
+"""B200 execution backend for the data-parallel core of dexlet (arXiv 2104.05372).
+
+Thin ctypes binding over the C-ABI of ``libdexlet_cuda.so`` (include/dexlet_cuda.h).
+The product path is C++/CUDA: the reference front end (parse, typecheck,
+simplify, linearize/transpose, optimize) compiled unmodified, then device
+lowering of every ``for``/``runAccum`` nest into NVRTC-compiled sm_100a kernels
+built on the hand-written device runtime ``csrc/dx_device.cuh``.
+
+There is no CPU fallback: if the shared library is missing this module raises
+at import, and on a machine without a GPU only compile-only programs
+(``Program(..., ctx=None)``) can be created.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdexlet_cuda.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C paper_2104_05372_b200/csrc` "
+        "(or __graft_entry__.build()); the backend has no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# status codes (include/dexlet_cuda.h)
+DXC_OK = 0
+DXC_E_PARSE = 1
+DXC_E_TYPE = 4
+DXC_E_SIZE = 11
+DXC_E_BOUNDS = 12
+DXC_E_REF = 13
+DXC_E_PARALLEL = 14
+DXC_E_INTERNAL = 15
+DXC_E_CUDA = 100
+DXC_E_ARG = 101
+
+LEAF_FLOAT, LEAF_INT, LEAF_INDEX = 0, 1, 2
+DXC_F32, DXC_F64, DXC_I32, DXC_I64, DXC_U32 = 0, 1, 2, 3, 4
+
+F_NO_FUSION = 1
+F_NO_ROWSCATTER = 2
+F_DUMP = 4
+
+_ERRNAMES = {
+    DXC_E_PARSE: "E-parse", DXC_E_TYPE: "E-type", DXC_E_SIZE: "E-size",
+    DXC_E_BOUNDS: "E-bounds", DXC_E_REF: "E-ref", DXC_E_PARALLEL: "E-parallel",
+    DXC_E_INTERNAL: "E-internal", DXC_E_CUDA: "E-cuda", DXC_E_ARG: "E-arg",
+}
+
+
+class DexError(RuntimeError):
+    """Mirror of dexlet::DexError (reference include/dexlet/errors.hpp:62-99)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[{_ERRNAMES.get(code, code)}] {message}")
+        self.code = code
+        self.message = message
+
+
+class DxlOptions(ctypes.Structure):
+    _fields_ = [("float64", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("threads", ctypes.c_int), ("flags", ctypes.c_int)]
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_vp = ctypes.c_void_p
+_ip = ctypes.POINTER(ctypes.c_int)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_sig("dxc_last_error", ctypes.c_char_p)
+_sig("dxc_init", ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp))
+_sig("dxc_destroy", ctypes.c_int, _vp)
+_sig("dxc_device_count", ctypes.c_int, _ip)
+_sig("dxc_sm_count", ctypes.c_int, _vp, _ip)
+_sig("dxc_stream", _vp, _vp)
+_sig("dxc_sync", ctypes.c_int, _vp)
+_sig("dxc_host_alloc", ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(_vp))
+_sig("dxc_host_free", ctypes.c_int, _vp)
+_sig("dxc_event_record", ctypes.c_int, _vp, ctypes.POINTER(_vp))
+_sig("dxc_event_elapsed_ms", ctypes.c_int, _vp, _vp, ctypes.POINTER(ctypes.c_float))
+_sig("dxc_event_destroy", ctypes.c_int, _vp)
+_sig("dxc_nccl_unique_id", ctypes.c_int, _vp)
+_sig("dxc_comm_init", ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int)
+_sig("dxc_allreduce_sum", ctypes.c_int, _vp, _vp, ctypes.c_size_t, ctypes.c_int)
+_sig("dxc_desc_size", ctypes.c_int, ctypes.c_char_p, _i64p)
+_sig("dxc_desc_reverse", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64, _i64p)
+_sig("dxc_chunk_range", ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _i64p, _i64p)
+_sig("dxl_program_create", ctypes.c_int, _vp, ctypes.c_char_p, ctypes.c_char_p,
+     ctypes.POINTER(DxlOptions), ctypes.POINTER(_vp))
+_sig("dxl_program_destroy", ctypes.c_int, _vp)
+_sig("dxl_program_num_inputs", ctypes.c_int, _vp, _ip)
+_sig("dxl_program_input_num_leaves", ctypes.c_int, _vp, ctypes.c_int, _ip)
+_sig("dxl_program_input_leaf", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _ip, _i64p)
+_sig("dxl_program_output_num_leaves", ctypes.c_int, _vp, _ip)
+_sig("dxl_program_output_leaf", ctypes.c_int, _vp, ctypes.c_int, _ip, _i64p)
+_sig("dxl_program_set_input", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int)
+_sig("dxl_program_bind_input_device", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp)
+_sig("dxl_program_input_device_ptr", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp))
+_sig("dxl_program_run", ctypes.c_int, _vp)
+_sig("dxl_program_get_output", ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int)
+_sig("dxl_program_output_device_ptr", ctypes.c_int, _vp, ctypes.c_int, ctypes.POINTER(_vp))
+_sig("dxl_program_source", ctypes.c_char_p, _vp)
+_sig("dxl_program_plan", ctypes.c_char_p, _vp)
+_sig("dxl_program_num_launches", ctypes.c_int, _vp, _ip)
+
+#: every symbol declared in include/dexlet_cuda.h
+ABI_SYMBOLS = [
+    "dxc_last_error", "dxc_init", "dxc_destroy", "dxc_device_count", "dxc_sm_count", "dxc_stream",
+    "dxc_sync", "dxc_buf_alloc", "dxc_buf_free", "dxc_buf_ptr", "dxc_buf_upload", "dxc_buf_download",
+    "dxc_buf_zero", "dxc_host_alloc", "dxc_host_free", "dxc_module_compile", "dxc_module_cubin",
+    "dxc_launch", "dxc_event_record", "dxc_event_elapsed_ms", "dxc_event_destroy",
+    "dxc_nccl_unique_id", "dxc_comm_init", "dxc_allreduce_sum", "dxl_program_create",
+    "dxl_program_destroy", "dxl_program_num_inputs", "dxl_program_input_num_leaves",
+    "dxl_program_input_leaf", "dxl_program_output_num_leaves", "dxl_program_output_leaf",
+    "dxl_program_set_input", "dxl_program_bind_input_device", "dxl_program_input_device_ptr",
+    "dxl_program_run", "dxl_program_get_output", "dxl_program_output_device_ptr",
+    "dxl_program_source", "dxl_program_plan", "dxl_program_num_launches", "dxc_desc_size",
+    "dxc_desc_reverse", "dxc_chunk_range",
+]
+
+
+def _check(rc: int):
+    if rc != DXC_OK:
+        raise DexError(rc, _lib.dxc_last_error().decode(errors="replace"))
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def chunk_range(total: int, parts: int, c: int) -> Tuple[int, int]:
+    """Contiguous chunk `c` of `parts` (reference eval.cpp:323-330)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.dxc_chunk_range(total, parts, c, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def device_count() -> int:
+    n = ctypes.c_int()
+    rc = _lib.dxc_device_count(ctypes.byref(n))
+    return n.value if rc == DXC_OK else 0
+
+
+class Context:
+    """One GPU: primary CUDA context + a stream (replaces the chunk threads)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(_lib.dxc_init(device, ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        return _lib.dxc_stream(self.handle)
+
+    def sm_count(self) -> int:
+        n = ctypes.c_int()
+        _check(_lib.dxc_sm_count(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def sync(self):
+        _check(_lib.dxc_sync(self.handle))
+
+    def event(self):
+        e = _vp()
+        _check(_lib.dxc_event_record(self.handle, ctypes.byref(e)))
+        return e
+
+    @staticmethod
+    def elapsed_ms(e0, e1) -> float:
+        ms = ctypes.c_float()
+        _check(_lib.dxc_event_elapsed_ms(e0, e1, ctypes.byref(ms)))
+        return ms.value
+
+    @staticmethod
+    def destroy_event(e):
+        _lib.dxc_event_destroy(e)
+
+    def init_comm(self, unique_id: bytes, nranks: int, rank: int):
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        _check(_lib.dxc_comm_init(self.handle, buf, nranks, rank))
+
+    def close(self):
+        if self.handle:
+            _lib.dxc_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.dxc_nccl_unique_id(buf))
+    return buf.raw
+
+
+_NP_DT = {DXC_F32: np.float32, DXC_F64: np.float64, DXC_I32: np.int32, DXC_I64: np.int64,
+          DXC_U32: np.uint32}
+_DT_OF = {np.dtype(np.float32): DXC_F32, np.dtype(np.float64): DXC_F64, np.dtype(np.int32): DXC_I32,
+          np.dtype(np.int64): DXC_I64, np.dtype(np.uint32): DXC_U32}
+
+
+class Program:
+    """A dexlet program lowered for the device.
+
+    ``source`` defines ``entry = \\x1:T1. ... \\xk:Tk. body``; inputs are the
+    lambda parameters, flattened to SoA leaves (a table of pairs is a pair of
+    tables), row-major by index-set ordinal.  Index leaves are ordinals.
+    """
+
+    def __init__(self, source: str, entry: str = "main", ctx: Optional[Context] = None,
+                 float64: bool = False, rank: int = 0, world: int = 1, threads: int = 0,
+                 flags: int = 0):
+        opts = DxlOptions(1 if float64 else 0, rank, world, threads, flags)
+        h = _vp()
+        _check(_lib.dxl_program_create(ctx.handle if ctx else None, source.encode(), entry.encode(),
+                                       ctypes.byref(opts), ctypes.byref(h)))
+        self.handle = h
+        self.ctx = ctx
+        self.float64 = float64
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _lib.dxl_program_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    @property
+    def source(self) -> str:
+        return _lib.dxl_program_source(self.handle).decode()
+
+    @property
+    def plan(self) -> str:
+        return _lib.dxl_program_plan(self.handle).decode()
+
+    def num_launches(self) -> int:
+        n = ctypes.c_int()
+        _check(_lib.dxl_program_num_launches(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def input_leaves(self) -> List[List[Tuple[int, int]]]:
+        n = ctypes.c_int()
+        _check(_lib.dxl_program_num_inputs(self.handle, ctypes.byref(n)))
+        out = []
+        for i in range(n.value):
+            m = ctypes.c_int()
+            _check(_lib.dxl_program_input_num_leaves(self.handle, i, ctypes.byref(m)))
+            leaves = []
+            for l in range(m.value):
+                k, c = ctypes.c_int(), ctypes.c_int64()
+                _check(_lib.dxl_program_input_leaf(self.handle, i, l, ctypes.byref(k), ctypes.byref(c)))
+                leaves.append((k.value, c.value))
+            out.append(leaves)
+        return out
+
+    def output_leaves(self) -> List[Tuple[int, int]]:
+        n = ctypes.c_int()
+        _check(_lib.dxl_program_output_num_leaves(self.handle, ctypes.byref(n)))
+        out = []
+        for l in range(n.value):
+            k, c = ctypes.c_int(), ctypes.c_int64()
+            _check(_lib.dxl_program_output_leaf(self.handle, l, ctypes.byref(k), ctypes.byref(c)))
+            out.append((k.value, c.value))
+        return out
+
+    def set_input(self, i: int, leaf: int, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr)
+        dt = _DT_OF[arr.dtype]
+        _check(_lib.dxl_program_set_input(self.handle, i, leaf, arr.ctypes.data_as(_vp), dt))
+
+    def set_input_ptr(self, i: int, leaf: int, host_ptr: int, dtype: int):
+        _check(_lib.dxl_program_set_input(self.handle, i, leaf, _vp(host_ptr), dtype))
+
+    def bind_input_device(self, i: int, leaf: int, devptr: int):
+        _check(_lib.dxl_program_bind_input_device(self.handle, i, leaf, _vp(devptr)))
+
+    def input_device_ptr(self, i: int, leaf: int) -> int:
+        p = _vp()
+        _check(_lib.dxl_program_input_device_ptr(self.handle, i, leaf, ctypes.byref(p)))
+        return p.value or 0
+
+    def output_device_ptr(self, leaf: int) -> int:
+        p = _vp()
+        _check(_lib.dxl_program_output_device_ptr(self.handle, leaf, ctypes.byref(p)))
+        return p.value or 0
+
+    def run(self):
+        _check(_lib.dxl_program_run(self.handle))
+
+    def get_output(self, leaf: int, dtype: int = DXC_F64) -> np.ndarray:
+        kinds = self.output_leaves()
+        k, c = kinds[leaf]
+        out = np.empty(c, dtype=_NP_DT[dtype])
+        _check(_lib.dxl_program_get_output(self.handle, leaf, out.ctypes.data_as(_vp), dtype))
+        return out
+
+    def get_output_ptr(self, leaf: int, host_ptr: int, dtype: int):
+        _check(_lib.dxl_program_get_output(self.handle, leaf, _vp(host_ptr), dtype))
+
+    def __call__(self, *inputs: Sequence[np.ndarray]) -> List[np.ndarray]:
+        """Run with one list of leaf arrays per input; returns output leaves
+        (floats as f64, ints/indices as i64)."""
+        for i, leaves in enumerate(inputs):
+            if isinstance(leaves, np.ndarray):
+                leaves = [leaves]
+            for l, a in enumerate(leaves):
+                self.set_input(i, l, a)
+        self.run()
+        res = []
+        for l, (k, c) in enumerate(self.output_leaves()):
+            res.append(self.get_output(l, DXC_F64 if k == LEAF_FLOAT else DXC_I64))
+        return res

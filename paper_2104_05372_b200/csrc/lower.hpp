@@ -1,0 +1,128 @@
+// Device lowering of first-order dexlet IR (the output of the reference's
+// optimize(), proj/src/simplify.cpp:1107-1111) into a plan of sm_100a kernels.
+//
+// This is the B200 replacement of Interp (proj/src/eval.cpp:93-546): instead
+// of walking the boxed RtVal tree per iteration, every host-level `for` /
+// `runAccum` nest becomes one generated CUDA kernel (built on the hand-written
+// primitives of dx_device.cuh) over flat SoA buffers.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dexlet/index_set.hpp"
+#include "dexlet/ir.hpp"
+
+namespace dexlet {
+namespace dev {
+
+// Storage kinds of plan buffers.
+enum class SK { F, I, X, U32 };  // Float (f32|f64), Int (i64), Index (i32), counters
+
+// Resolved device type of a value (index-set sizes concrete).
+struct DType;
+using DTy = std::shared_ptr<const DType>;
+struct DType {
+  enum K { Float, Int, Unit, Idx, Pair, Table, Ref, Sum } k;  // Sum: data Either (a | b)
+  DescPtr desc;  // Idx: its index set; Table: its domain
+  DTy a, b;      // Pair/Sum: components; Table: a = element; Ref: a = payload
+};
+
+struct LeafInfo {
+  SK kind;
+  long long count;  // scalars of this leaf per value
+  DescPtr desc;     // Idx leaves: the index set of the member
+};
+void leavesOf(const DTy& t, std::vector<LeafInfo>& out, long long mult = 1);
+std::string showType(const DTy& t);
+
+struct BufDecl {
+  enum Role { Input, Cell, Output, Partial, Const, Temp, Flag } role;
+  SK kind;
+  long long elems;
+  int input = -1, leaf = -1;
+  std::vector<double> initF;     // Const / host-known cell values (Float)
+  std::vector<long long> initI;  // Const (Int / Index)
+  long long partialWidth = 0;    // Partial: elements per block (sized at prepare)
+  int partialKernel = -1;        // Partial: the step index of its kernel
+};
+
+struct KArg {
+  enum K { Buf, I64 } k;
+  int buf = -1;
+  long long off = 0;   // Buf: element offset
+  long long i = 0;     // I64 value
+  int special = 0;     // 1: range lo, 2: range hi
+};
+
+struct Step {
+  enum K { Zero, Upload, Kernel, Finalize, Allreduce, AddBuf, CopyBuf } k;
+  int buf = -1, buf2 = -1;
+  long long off = 0, off2 = 0, elems = 0;
+  // Kernel
+  std::string name;
+  std::vector<KArg> args;
+  long long total = 0;  // iterations of the outer loop (1 for serial)
+  bool serial = false;
+  bool sharded = false;
+  int threads = 256;
+  int smem = 0;           // dynamic shared memory bytes
+  int minGrid = 0;        // informational
+  // Finalize: partial buf -> cell (buf, off, elems = width)
+  enum FinK { Seq, Tree, Count } fin = Seq;
+  int kernelStep = -1;
+  double scale = 1.0;
+  std::string note;
+};
+
+struct OutLeaf {
+  SK kind;
+  long long count;
+  DescPtr desc;           // index leaves
+  bool host = false;      // value known on the host
+  std::vector<double> hostF;
+  std::vector<long long> hostI;
+  int buf = -1;
+  long long off = 0;
+};
+
+struct InLeaf {
+  SK kind;
+  long long count;
+  DescPtr desc;
+  int buf;
+};
+
+struct Plan {
+  bool f64 = false;
+  int rank = 0, world = 1;
+  std::vector<BufDecl> bufs;
+  std::vector<Step> steps;
+  std::string source;           // generated kernels (device runtime prepended at compile)
+  std::vector<std::vector<InLeaf>> inputs;
+  std::vector<DTy> inputTypes;
+  std::vector<Name> inputNames;
+  std::vector<OutLeaf> outputs;
+  DTy outputType;
+  int errFlagBuf = -1;          // E-bounds flag raised by fused index checks
+  int numKernels = 0;
+  std::string summary() const;
+};
+
+struct LowerOptions {
+  bool f64 = false;
+  int rank = 0, world = 1;
+  int threads = 256;
+  bool noFusion = false;
+  bool noRowScatter = false;
+};
+
+// Lowers `e` (first-order, post-optimize) whose free variables are the
+// given inputs.  Throws DexError(Internal, ...) when a construct is not
+// lowerable: there is no CPU fallback.
+Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>& inputs,
+                  const LowerOptions& opts);
+
+}  // namespace dev
+}  // namespace dexlet

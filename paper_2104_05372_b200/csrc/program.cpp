@@ -1,0 +1,675 @@
+// Program-level C-ABI (dxl_*): the device counterpart of the reference's
+// harness path  evalExpr(env, optimize(simplify(compile(src))))
+// (reference tests/acceptance.cpp:63-71, tools/dexlet_main.cpp:177-207).
+//
+// The reference front end (parser, typechecker, simplifier, autodiff) is
+// compiled unmodified from /root/reference/proj/src into this library; its
+// evaluator (eval.cpp) is NOT linked: every loop runs on the GPU.
+
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "dexlet/errors.hpp"
+#include "dexlet/parser.hpp"
+#include "dexlet/printer.hpp"
+#include "dexlet/simplify.hpp"
+#include "dexlet/typecheck.hpp"
+#include "dexlet_cuda.h"
+#include "lower.hpp"
+#include "program_impl.hpp"
+#include "runtime.hpp"
+
+using namespace dexlet;
+using namespace dexlet::dev;
+using dxrt::setError;
+
+namespace dexlet {
+namespace dev {
+
+static int errCodeToStatus(ErrCode c) {
+  switch (c) {
+    case ErrCode::Parse: return DXC_E_PARSE;
+    case ErrCode::UnresolvedSize: return DXC_E_SIZE;
+    case ErrCode::OutOfBounds: return DXC_E_BOUNDS;
+    case ErrCode::EscapedRef: return DXC_E_REF;
+    case ErrCode::StateInParallel: return DXC_E_PARALLEL;
+    case ErrCode::Internal: return DXC_E_INTERNAL;
+    default: return DXC_E_TYPE;
+  }
+}
+
+size_t storageBytes(SK k, bool f64) {
+  switch (k) {
+    case SK::F: return f64 ? 8 : 4;
+    case SK::I: return 8;
+    case SK::X: return 4;
+    case SK::U32: return 4;
+  }
+  return 4;
+}
+
+// Builds `let decls in let a1 = entry x1 in ... in ak` with fresh input
+// names, exactly as the survey harness does.
+ExprPtr buildEntryApplication(const std::string& src, const std::string& entry,
+                              std::vector<std::pair<Name, ValuePtr>>& params, ExprPtr* optimized) {
+  NameSupply::reset(1000000);
+  ElabProgram p = parseProgram(src, "program.dexlet");
+  const ElabDecl* m = p.find(entry);
+  if (!m) fail(ErrCode::UnboundVariable, "entry '" + entry + "' is not defined");
+  ExprPtr b = m->bound;
+  while (true) {
+    const ERet* r = as<ERet>(b);
+    if (!r) break;
+    const VLam* l = as<VLam>(r->value);
+    if (!l) break;
+    params.push_back({NameSupply::fresh(l->binder.text), l->annot});
+    b = l->body;
+  }
+  TypeEnv env;
+  for (auto& [n, t] : params) env.bind(n, t);
+  Name last = m->binder;
+  std::vector<std::pair<Name, ExprPtr>> apps;
+  for (auto& [n, t] : params) {
+    Name a = NameSupply::fresh("ap");
+    apps.push_back({a, eApp(vVar(last), vVar(n))});
+    last = a;
+  }
+  ExprPtr e = eRet(vVar(last));
+  for (auto it = apps.rbegin(); it != apps.rend(); ++it) e = eLet(it->first, nullptr, it->second, e);
+  for (auto it = p.decls.rbegin(); it != p.decls.rend(); ++it) e = eLet(it->binder, nullptr, it->bound, e);
+  checkExpr(Capability::pure(), env, e);
+  SimplResult r = simplify(env, e);
+  ExprPtr o = optimize(contextFill(r.ctx, eRet(r.residual)));
+  if (!isFirstOrder(o)) fail(ErrCode::Internal, "simplified program is not first-order");
+  *optimized = o;
+  return e;
+}
+
+int Program::prepare() {
+  bool f64 = plan.f64;
+  // module
+  if (!ctx) {
+    std::string cubin;
+    return dxrt::compileCubin(plan.source, cubin);
+  }
+  int rc = ctx->loadModule(plan.source, &mod);
+  if (rc) return rc;
+  ctx->makeCurrent();
+  // kernels: functions + grids
+  grids.assign(plan.steps.size(), 0);
+  funcs.assign(plan.steps.size(), nullptr);
+  ranges.assign(plan.steps.size(), {0, 0});
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    Step& s = plan.steps[i];
+    if (s.k != Step::Kernel) continue;
+    CUfunction f;
+    if ((rc = dxrt::check(cuModuleGetFunction(&f, mod, s.name.c_str()), "cuModuleGetFunction"))) return rc;
+    funcs[i] = f;
+    if (s.smem > 48 * 1024) {
+      if ((rc = dxrt::check(cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, s.smem),
+                            "cuFuncSetAttribute")))
+        return rc;
+    }
+    long long lo = 0, hi = s.total;
+    if (s.sharded) {
+      int64_t a, b;
+      dxc_chunk_range(s.total, plan.world, plan.rank, &a, &b);
+      lo = a;
+      hi = b;
+    }
+    ranges[i] = {lo, hi};
+    if (s.serial) {
+      grids[i] = 1;
+      continue;
+    }
+    int nb = 1;
+    if ((rc = dxrt::check(cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, s.threads, s.smem), "occupancy")))
+      return rc;
+    if (nb < 1) nb = 1;
+    long long U = s.minGrid > 0 ? s.minGrid : 1;  // ordinals per thread
+    long long need = ((hi - lo + U - 1) / U + s.threads - 1) / s.threads;
+    long long cap = (long long)ctx->smCount * nb;
+    long long grid = std::max(1LL, std::min(need, cap));
+    grids[i] = (int)grid;
+  }
+  // buffers
+  devptr.assign(plan.bufs.size(), 0);
+  for (size_t b = 0; b < plan.bufs.size(); ++b) {
+    BufDecl& d = plan.bufs[b];
+    long long elems = d.elems;
+    if (d.role == BufDecl::Partial) elems = (long long)grids[d.partialKernel] * d.partialWidth;
+    size_t bytes = (size_t)std::max(1LL, elems) * storageBytes(d.kind, f64);
+    if (d.role == BufDecl::Input && boundInputs.count((int)b)) continue;  // bound later
+    if (d.elems < 0) continue;                                              // dead
+    if ((rc = dxrt::check(cuMemAlloc(&devptr[b], bytes), "cuMemAlloc"))) return rc;
+    owned.push_back(devptr[b]);
+    if (d.role == BufDecl::Const) {
+      std::vector<char> host = convertInit(d);
+      if ((rc = dxrt::check(cuMemcpyHtoD(devptr[b], host.data(), host.size()), "upload const"))) return rc;
+    }
+  }
+  // host-known cell values live in their Const buffer (uploaded once, here);
+  // each run copies them device-to-device, so the whole run is capturable
+  // in a CUDA graph.  Under sharding only rank 0 contributes them.
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    Step& s = plan.steps[i];
+    if (s.k == Step::Upload && s.buf != s.buf2) {
+      BufDecl tmp = plan.bufs[s.buf2];
+      tmp.kind = plan.bufs[s.buf].kind;
+      std::vector<char> host = convertInit(tmp);
+      if (plan.world > 1 && plan.rank != 0) std::fill(host.begin(), host.end(), 0);
+      if ((rc = dxrt::check(cuMemcpyHtoD(devptr[s.buf2], host.data(), host.size()), "upload cell init"))) return rc;
+    }
+  }
+  if (std::getenv("DEXLET_NO_GRAPH") || plan.world > 1) useGraph = false;
+  // finalize functions
+  const char* fz[4] = {"dx_fin_f32", "dx_fin_f64", "dx_fin_count_f32", "dx_fin_count_f64"};
+  for (int k = 0; k < 4; ++k)
+    if ((rc = dxrt::check(cuModuleGetFunction(&finFn[k], mod, fz[k]), "finalize fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&addFn[0], mod, "dx_add_f32"), "add fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&addFn[1], mod, "dx_add_f64"), "add fn"))) return rc;
+  prepared = true;
+  return DXC_OK;
+}
+
+std::vector<char> Program::convertInit(const BufDecl& d) const {
+  size_t es = storageBytes(d.kind, plan.f64);
+  long long n = d.kind == SK::F ? (long long)d.initF.size() : (long long)d.initI.size();
+  std::vector<char> out((size_t)std::max(1LL, n) * es, 0);
+  for (long long i = 0; i < n; ++i) {
+    char* p = out.data() + i * es;
+    switch (d.kind) {
+      case SK::F:
+        if (plan.f64) { double v = d.initF[i]; std::memcpy(p, &v, 8); }
+        else { float v = (float)d.initF[i]; std::memcpy(p, &v, 4); }
+        break;
+      case SK::I: { long long v = d.initI[i]; std::memcpy(p, &v, 8); break; }
+      case SK::X:
+      case SK::U32: { int v = (int)d.initI[i]; std::memcpy(p, &v, 4); break; }
+    }
+  }
+  return out;
+}
+
+int Program::launch(CUfunction f, unsigned grid, unsigned block, unsigned smem, void** args) {
+  return dxrt::check(cuLaunchKernel(f, grid, 1, 1, block, 1, 1, smem, ctx->stream, args, nullptr),
+                     "cuLaunchKernel");
+}
+
+int Program::run() {
+  if (!ctx) { setError("program has no device context"); return DXC_E_ARG; }
+  int rc;
+  if (!prepared && (rc = prepare())) return rc;
+  ctx->makeCurrent();
+  if (!useGraph) return issue();
+  if (!graphExec) {
+    // capture the whole plan once; replay it with a single launch per run
+    if ((rc = dxrt::check(cuStreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture"))) return rc;
+    int irc = issue();
+    CUgraph graph = nullptr;
+    CUresult er = cuStreamEndCapture(ctx->stream, &graph);
+    if (irc) { if (graph) cuGraphDestroy(graph); return irc; }
+    if ((rc = dxrt::check(er, "end capture"))) return rc;
+    rc = dxrt::check(cuGraphInstantiate(&graphExec, graph, 0), "graph instantiate");
+    cuGraphDestroy(graph);
+    if (rc) return rc;
+  }
+  return dxrt::check(cuGraphLaunch(graphExec, ctx->stream), "graph launch");
+}
+
+int Program::issue() {
+  int rc;
+  bool f64 = plan.f64;
+  CUstream st = ctx->stream;
+  launches = 0;
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    Step& s = plan.steps[i];
+    switch (s.k) {
+      case Step::Zero: {
+        size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
+        long long n = s.elems > 0 ? s.elems : plan.bufs[s.buf].elems;
+        if ((rc = dxrt::check(cuMemsetD8Async(devptr[s.buf] + s.off * es, 0, (size_t)n * es, st), "memset"))) return rc;
+        break;
+      }
+      case Step::Upload: {
+        if (s.buf == s.buf2) break;  // immutable constant, uploaded at prepare
+        size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
+        if ((rc = dxrt::check(cuMemcpyDtoDAsync(devptr[s.buf], devptr[s.buf2], (size_t)s.elems * es, st), "cell init")))
+          return rc;
+        break;
+      }
+      case Step::CopyBuf: {
+        size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
+        if ((rc = dxrt::check(cuMemcpyDtoDAsync(devptr[s.buf] + s.off * es, devptr[s.buf2] + s.off2 * es,
+                                                (size_t)s.elems * es, st), "copy")))
+          return rc;
+        break;
+      }
+      case Step::Kernel: {
+        std::vector<CUdeviceptr> ptrs(s.args.size());
+        std::vector<long long> ints(s.args.size());
+        std::vector<void*> argv(s.args.size());
+        for (size_t a = 0; a < s.args.size(); ++a) {
+          const KArg& ka = s.args[a];
+          if (ka.k == KArg::Buf) {
+            ptrs[a] = devptr[ka.buf] + ka.off * storageBytes(plan.bufs[ka.buf].kind, f64);
+            argv[a] = &ptrs[a];
+          } else {
+            ints[a] = ka.special == 1 ? ranges[i].first : ka.special == 2 ? ranges[i].second : ka.i;
+            argv[a] = &ints[a];
+          }
+        }
+        if ((rc = launch(funcs[i], grids[i], s.threads, s.smem, argv.data()))) return rc;
+        ++launches;
+        break;
+      }
+      case Step::Finalize: {
+        CUdeviceptr part = devptr[s.buf2], cell = devptr[s.buf];
+        int nblk = grids[s.kernelStep];
+        long long w = s.elems;
+        unsigned g = (unsigned)((w + 31) / 32);
+        if (s.fin == Step::Count) {
+          float sf = (float)s.scale;
+          double sd = s.scale;
+          void* args[5] = {&part, &nblk, &w, f64 ? (void*)&sd : (void*)&sf, &cell};
+          if ((rc = launch(finFn[f64 ? 3 : 2], g, 1024, 0, args))) return rc;
+        } else {
+          void* args[4] = {&part, &nblk, &w, &cell};
+          if ((rc = launch(finFn[f64 ? 1 : 0], g, 1024, 0, args))) return rc;
+        }
+        ++launches;
+        break;
+      }
+      case Step::Allreduce: {
+        size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
+        SK k = plan.bufs[s.buf].kind;
+        int dt = k == SK::F ? (f64 ? DXC_F64 : DXC_F32) : k == SK::I ? DXC_I64 : DXC_I32;
+        if ((rc = ctx->allreduceSum(devptr[s.buf] + s.off * es, (size_t)s.elems, dt))) return rc;
+        break;
+      }
+      case Step::AddBuf: {
+        CUdeviceptr c = devptr[s.buf], src = devptr[s.buf2];
+        long long n = s.elems;
+        void* args[3] = {&c, &src, &n};
+        if ((rc = launch(addFn[f64 ? 1 : 0], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args)))
+          return rc;
+        ++launches;
+        break;
+      }
+    }
+  }
+  return DXC_OK;
+}
+
+Program::~Program() {
+  if (ctx) {
+    ctx->makeCurrent();
+    if (graphExec) cuGraphExecDestroy(graphExec);
+    for (CUdeviceptr p : owned) cuMemFree(p);
+  }
+}
+
+}  // namespace dev
+}  // namespace dexlet
+
+// ===========================================================================
+
+struct dxl_program : dexlet::dev::Program {};
+
+#define GUARD_BEGIN try {
+#define GUARD_END                                                   \
+  }                                                                 \
+  catch (const DexError& e) {                                       \
+    setError(std::string(errCodeName(e.code())) + ": " + e.message()); \
+    return errCodeToStatus(e.code());                               \
+  }                                                                 \
+  catch (const std::exception& e) {                                 \
+    setError(std::string("E-internal: ") + e.what());               \
+    return DXC_E_INTERNAL;                                          \
+  }
+
+extern "C" {
+
+int dxl_program_create(dxc_ctx* ctx, const char* source, const char* entry, const dxl_options* opts,
+                       dxl_program** out) {
+  GUARD_BEGIN
+  auto* p = new dxl_program();
+  p->ctx = reinterpret_cast<dxrt::Ctx*>(ctx);
+  LowerOptions lo;
+  if (opts) {
+    lo.f64 = opts->float64 != 0;
+    lo.rank = opts->rank;
+    lo.world = opts->world < 1 ? 1 : opts->world;
+    lo.threads = opts->threads > 0 ? opts->threads : 256;
+    lo.noFusion = (opts->flags & DXL_F_NO_FUSION) != 0;
+    lo.noRowScatter = (opts->flags & DXL_F_NO_ROWSCATTER) != 0;
+  }
+  std::vector<std::pair<Name, ValuePtr>> params;
+  ExprPtr optimized;
+  try {
+    buildEntryApplication(source, entry ? entry : "main", params, &optimized);
+    p->optimizedIR = printExpr(optimized);
+    p->plan = lowerProgram(optimized, params, lo);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  p->plan.source = std::string(lo.f64 ? "typedef double dx_f;\n" : "typedef float dx_f;\n") + p->plan.source;
+  p->planText = p->plan.summary();
+  if (opts && (opts->flags & DXL_F_DUMP)) {
+    if (const char* d = std::getenv("DEXLET_DUMP_DIR")) {
+      std::ofstream(std::string(d) + "/" + (entry ? entry : "main") + ".cu") << p->plan.source;
+      std::ofstream(std::string(d) + "/" + (entry ? entry : "main") + ".plan") << p->planText << "\n"
+                                                                                << p->optimizedIR;
+    }
+  }
+  int rc = p->prepare();
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return DXC_OK;
+  GUARD_END
+}
+
+int dxl_program_destroy(dxl_program* p) {
+  delete p;
+  return DXC_OK;
+}
+
+int dxl_program_num_inputs(dxl_program* p, int* out) {
+  *out = (int)p->plan.inputs.size();
+  return DXC_OK;
+}
+
+int dxl_program_input_num_leaves(dxl_program* p, int input, int* out) {
+  if (input < 0 || input >= (int)p->plan.inputs.size()) { setError("bad input"); return DXC_E_ARG; }
+  *out = (int)p->plan.inputs[input].size();
+  return DXC_OK;
+}
+
+static int leafKind(SK k) { return k == SK::F ? DXC_LEAF_FLOAT : k == SK::I ? DXC_LEAF_INT : DXC_LEAF_INDEX; }
+
+int dxl_program_input_leaf(dxl_program* p, int input, int leaf, int* kind, int64_t* count) {
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  const InLeaf& l = p->plan.inputs[input][leaf];
+  *kind = leafKind(l.kind);
+  *count = l.count;
+  return DXC_OK;
+}
+
+int dxl_program_output_num_leaves(dxl_program* p, int* out) {
+  *out = (int)p->plan.outputs.size();
+  return DXC_OK;
+}
+
+int dxl_program_output_leaf(dxl_program* p, int leaf, int* kind, int64_t* count) {
+  if (leaf < 0 || leaf >= (int)p->plan.outputs.size()) { setError("bad output leaf"); return DXC_E_ARG; }
+  *kind = leafKind(p->plan.outputs[leaf].kind);
+  *count = p->plan.outputs[leaf].count;
+  return DXC_OK;
+}
+
+// Converts host data of `dtype` into the leaf's storage type.
+static std::vector<char> convertIn(const void* host, int dtype, SK kind, bool f64, long long n, int* rc,
+                                   long long idxSize) {
+  size_t es = storageBytes(kind, f64);
+  std::vector<char> out((size_t)n * es);
+  *rc = DXC_OK;
+  for (long long i = 0; i < n; ++i) {
+    double dv = 0;
+    long long iv = 0;
+    switch (dtype) {
+      case DXC_F32: dv = ((const float*)host)[i]; iv = (long long)dv; break;
+      case DXC_F64: dv = ((const double*)host)[i]; iv = (long long)dv; break;
+      case DXC_I32: iv = ((const int32_t*)host)[i]; dv = (double)iv; break;
+      case DXC_I64: iv = ((const int64_t*)host)[i]; dv = (double)iv; break;
+      case DXC_U32: iv = ((const uint32_t*)host)[i]; dv = (double)iv; break;
+      default: *rc = DXC_E_ARG; return out;
+    }
+    char* p = out.data() + i * es;
+    switch (kind) {
+      case SK::F:
+        if (f64) std::memcpy(p, &dv, 8);
+        else { float f = (float)dv; std::memcpy(p, &f, 4); }
+        break;
+      case SK::I: std::memcpy(p, &iv, 8); break;
+      case SK::X: {
+        if (iv < 0 || iv >= idxSize) {
+          *rc = DXC_E_BOUNDS;
+          setError("E-bounds: input ordinal " + std::to_string(iv) + " is outside an index set of size " +
+                   std::to_string(idxSize));
+          return out;
+        }
+        int32_t v = (int32_t)iv;
+        std::memcpy(p, &v, 4);
+        break;
+      }
+      case SK::U32: { uint32_t v = (uint32_t)iv; std::memcpy(p, &v, 4); break; }
+    }
+  }
+  return out;
+}
+
+int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host, int dtype) {
+  GUARD_BEGIN
+  if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  const InLeaf& l = p->plan.inputs[input][leaf];
+  bool f64 = p->plan.f64;
+  size_t es = storageBytes(l.kind, f64);
+  p->ctx->makeCurrent();
+  CUdeviceptr dst = p->devptr[l.buf];
+  if (p->boundInputs.count(l.buf)) { setError("input is bound to device memory"); return DXC_E_ARG; }
+  bool direct = (l.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) ||
+                (l.kind == SK::X && dtype == DXC_I32) || (l.kind == SK::I && dtype == DXC_I64);
+  if (direct) {
+    // index leaves are range-checked on the device where they are read
+    // (dx_chk_idx in every kernel that loads them)
+    return dxrt::check(cuMemcpyHtoDAsync(dst, host, (size_t)l.count * es, p->ctx->stream), "input upload");
+  }
+  int rc;
+  long long isz = l.desc ? size(l.desc) : 0;
+  std::vector<char> buf = convertIn(host, dtype, l.kind, f64, l.count, &rc, isz);
+  if (rc) return rc;
+  rc = dxrt::check(cuMemcpyHtoD(dst, buf.data(), buf.size()), "input upload");
+  return rc;
+  GUARD_END
+}
+
+int dxl_program_bind_input_device(dxl_program* p, int input, int leaf, void* devptr) {
+  if (((uintptr_t)devptr & 15) != 0) {
+    setError("device input pointers must be 16-byte aligned");
+    return DXC_E_ARG;
+  }
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  const InLeaf& l = p->plan.inputs[input][leaf];
+  p->boundInputs.insert(l.buf);
+  p->devptr[l.buf] = (CUdeviceptr)devptr;
+  if (p->graphExec) {  // kernel arguments are baked into the graph
+    cuGraphExecDestroy(p->graphExec);
+    p->graphExec = nullptr;
+  }
+  return DXC_OK;
+}
+
+int dxl_program_input_device_ptr(dxl_program* p, int input, int leaf, void** out) {
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  *out = (void*)p->devptr[p->plan.inputs[input][leaf].buf];
+  return DXC_OK;
+}
+
+int dxl_program_run(dxl_program* p) {
+  GUARD_BEGIN
+  return p->run();
+  GUARD_END
+}
+
+int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype) {
+  GUARD_BEGIN
+  if (leaf < 0 || leaf >= (int)p->plan.outputs.size()) { setError("bad output leaf"); return DXC_E_ARG; }
+  const OutLeaf& o = p->plan.outputs[leaf];
+  bool f64 = p->plan.f64;
+  std::vector<char> raw;
+  size_t es = storageBytes(o.kind, f64);
+  if (o.host) {
+    raw.resize(es);
+    if (o.kind == SK::F) {
+      if (f64) std::memcpy(raw.data(), &o.hostF[0], 8);
+      else { float f = (float)o.hostF[0]; std::memcpy(raw.data(), &f, 4); }
+    } else if (o.kind == SK::I) {
+      std::memcpy(raw.data(), &o.hostI[0], 8);
+    } else {
+      int v = (int)o.hostI[0];
+      std::memcpy(raw.data(), &v, 4);
+    }
+  } else {
+    if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+    p->ctx->makeCurrent();
+    bool direct = (o.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) ||
+                  (o.kind == SK::X && dtype == DXC_I32) || (o.kind == SK::I && dtype == DXC_I64);
+    int rc;
+    int flag = 0;
+    if (p->plan.errFlagBuf >= 0 && p->checkFlag) {
+      if ((rc = dxrt::check(cuMemcpyDtoHAsync(&flag, p->devptr[p->plan.errFlagBuf], 4, p->ctx->stream), "flag")))
+        return rc;
+    }
+    CUdeviceptr src = p->devptr[o.buf] + o.off * es;
+    if (direct) {
+      rc = dxrt::check(cuMemcpyDtoHAsync(host, src, (size_t)o.count * es, p->ctx->stream), "output download");
+      if (rc) return rc;
+      if ((rc = dxrt::check(cuStreamSynchronize(p->ctx->stream), "sync"))) return rc;
+      if (flag) { setError("E-bounds: an input ordinal is outside its index set"); return DXC_E_BOUNDS; }
+      return DXC_OK;
+    }
+    raw.resize((size_t)o.count * es);
+    rc = dxrt::check(cuMemcpyDtoHAsync(raw.data(), src, raw.size(), p->ctx->stream), "output download");
+    if (rc) return rc;
+    if ((rc = dxrt::check(cuStreamSynchronize(p->ctx->stream), "sync"))) return rc;
+    if (flag) { setError("E-bounds: an input ordinal is outside its index set"); return DXC_E_BOUNDS; }
+  }
+  long long n = o.host ? 1 : o.count;
+  for (long long i = 0; i < n; ++i) {
+    double dv = 0;
+    long long iv = 0;
+    const char* s = raw.data() + i * es;
+    switch (o.kind) {
+      case SK::F:
+        if (f64) std::memcpy(&dv, s, 8);
+        else { float f; std::memcpy(&f, s, 4); dv = f; }
+        iv = (long long)dv;
+        break;
+      case SK::I: std::memcpy(&iv, s, 8); dv = (double)iv; break;
+      case SK::X:
+      case SK::U32: { int32_t v; std::memcpy(&v, s, 4); iv = v; dv = v; break; }
+    }
+    switch (dtype) {
+      case DXC_F32: ((float*)host)[i] = (float)dv; break;
+      case DXC_F64: ((double*)host)[i] = dv; break;
+      case DXC_I32: ((int32_t*)host)[i] = (int32_t)iv; break;
+      case DXC_I64: ((int64_t*)host)[i] = iv; break;
+      case DXC_U32: ((uint32_t*)host)[i] = (uint32_t)iv; break;
+      default: setError("bad dtype"); return DXC_E_ARG;
+    }
+  }
+  return DXC_OK;
+  GUARD_END
+}
+
+int dxl_program_output_device_ptr(dxl_program* p, int leaf, void** out) {
+  if (leaf < 0 || leaf >= (int)p->plan.outputs.size()) { setError("bad output leaf"); return DXC_E_ARG; }
+  const OutLeaf& o = p->plan.outputs[leaf];
+  if (o.host) { *out = nullptr; return DXC_OK; }
+  *out = (void*)(p->devptr[o.buf] + o.off * storageBytes(o.kind, p->plan.f64));
+  return DXC_OK;
+}
+
+const char* dxl_program_source(dxl_program* p) { return p->plan.source.c_str(); }
+const char* dxl_program_plan(dxl_program* p) {
+  p->planDump = p->planText + "\n--- optimized IR ---\n" + p->optimizedIR;
+  return p->planDump.c_str();
+}
+
+int dxl_program_num_launches(dxl_program* p, int* out) {
+  int n = 0;
+  for (auto& s : p->plan.steps)
+    if (s.k == Step::Kernel || s.k == Step::Finalize || s.k == Step::AddBuf) ++n;
+  *out = n;
+  return DXC_OK;
+}
+
+// ---- index-set helpers -----------------------------------------------------
+
+static DescPtr parseDesc(const char*& s) {
+  switch (*s) {
+    case 'U': ++s; return descUnit();
+    case 'F': {
+      ++s;
+      char* end;
+      long long n = std::strtoll(s, &end, 10);
+      s = end;
+      return descFin(n);
+    }
+    case 'P': { ++s; DescPtr a = parseDesc(s); DescPtr b = parseDesc(s); return descPair(a, b); }
+    case 'E': { ++s; DescPtr a = parseDesc(s); DescPtr b = parseDesc(s); return descEither(a, b); }
+  }
+  fail(ErrCode::Internal, "bad descriptor string");
+}
+
+int dxc_desc_size(const char* desc, int64_t* out) {
+  GUARD_BEGIN
+  const char* s = desc;
+  *out = size(parseDesc(s));
+  return DXC_OK;
+  GUARD_END
+}
+
+int dxc_desc_reverse(const char* desc, int64_t ordinal, int64_t* out) {
+  GUARD_BEGIN
+  const char* s = desc;
+  long long n = size(parseDesc(s));
+  if (ordinal < 0 || ordinal >= n) {
+    setError("E-bounds: ordinal outside the index set");
+    return DXC_E_BOUNDS;
+  }
+  *out = n - 1 - ordinal;
+  return DXC_OK;
+  GUARD_END
+}
+
+int dxc_chunk_range(int64_t total, int parts, int c, int64_t* lo, int64_t* hi) {
+  if (parts < 1 || c < 0 || c >= parts) { setError("bad chunk"); return DXC_E_ARG; }
+  if (parts > total && total > 0) parts = (int)total;
+  if (c >= parts) { *lo = *hi = total; return DXC_OK; }
+  long long base = total / parts, rem = total % parts;
+  long long start = 0;
+  for (int i = 0; i < c; ++i) start += base + (i < rem ? 1 : 0);
+  *lo = start;
+  *hi = start + base + (c < rem ? 1 : 0);
+  return DXC_OK;
+}
+
+}  // extern "C"

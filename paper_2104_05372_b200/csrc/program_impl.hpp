@@ -1,0 +1,53 @@
+// Internal: a lowered program bound to a device context.
+#pragma once
+
+#include <cuda.h>
+
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "lower.hpp"
+#include "runtime.hpp"
+
+namespace dexlet {
+namespace dev {
+
+size_t storageBytes(SK k, bool f64);
+
+ExprPtr buildEntryApplication(const std::string& src, const std::string& entry,
+                              std::vector<std::pair<Name, ValuePtr>>& params, ExprPtr* optimized);
+
+struct Program {
+  dxrt::Ctx* ctx = nullptr;
+  Plan plan;
+  std::string optimizedIR;
+  std::string planText;
+  std::string planDump;
+  CUmodule mod = nullptr;
+  bool prepared = false;
+  bool checkFlag = true;
+  std::vector<CUdeviceptr> devptr;
+  std::vector<CUdeviceptr> owned;
+  std::set<int> boundInputs;
+  std::vector<int> grids;
+  std::vector<CUfunction> funcs;
+  std::vector<std::pair<long long, long long>> ranges;
+  std::vector<std::vector<char>> staging;
+  CUfunction finFn[4] = {};
+  CUfunction addFn[2] = {};
+  int launches = 0;
+  CUgraphExec graphExec = nullptr;
+  bool useGraph = true;
+
+  int prepare();
+  int run();
+  int issue();  // enqueue every plan step on the context stream
+  int launch(CUfunction f, unsigned grid, unsigned block, unsigned smem, void** args);
+  std::vector<char> convertInit(const BufDecl& d) const;
+  ~Program();
+};
+
+}  // namespace dev
+}  // namespace dexlet
