@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""Benchmark: k-means cost + gradient (BASELINE.json configs[1]) on B200.
+
+Workload: ``paper_2104_05372_b200.programs.kmeans_cost_grad`` -- the reference
+language's k-means objective at fixed assignments, value and gradient w.r.t.
+the centroids through the reference's own linearize/transpose, lowered by this
+backend into one fused sm_100a kernel (+ fixed-order finalize of the Accum
+partials).  n = 1,000,000 points per GPU, d = 16, K = 64, fp32.  One step =
+one forward+gradient evaluation over every point.
+
+Timing (rules of the task): W >= 3 warm-up steps; the 126 MB L2 is flushed
+(256 MB scratch write on our stream, outside the timed events) before every
+timed step; each step is bracketed by CUDA events on the stream the kernels
+run on; the max over ranks is reported; nvidia-smi clocks are sampled during
+the timed region.  `e2e` repeats the metric through the C-ABI with pinned
+host buffers: H2D of every input, the run, and D2H of the outputs inside the
+events.  `--impl reference` times the unmodified reference evaluator
+(oracle/_ref, compiled from /root/reference sources) on the host cores.
+
+Multi-GPU (torchrun): weak scaling, n = 1M x world points; every rank runs the
+same program sharded by (rank, world) -- contiguous point ranges, the
+reference's chunk rule -- and the Accum cells (cost, dC) are combined with an
+NCCL all-reduce.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_PER_GPU, D, K = 1_000_000, 16, 64
+METRIC = "kmeans fwd+grad evals/s (1M points/GPU, d=16, K=64)"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=10_000,
+                    help="points per reference step (bounded CPU sample)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def kmeans_inputs_fast(n, d, k, seed=20211):
+    """Synthetic k-means data: N(0,1) points, centroids sampled from the
+    points, assignments = nearest centroid (f32 GEMM distances)."""
+    rng = np.random.default_rng(seed)
+    pts = rng.standard_normal((n, d), dtype=np.float32)
+    cs = pts[rng.choice(n, size=k, replace=False)].copy()
+    asg = np.empty(n, dtype=np.int32)
+    c2 = (cs.astype(np.float32) ** 2).sum(1)
+    bs = 1 << 20
+    for s in range(0, n, bs):
+        p = pts[s:s + bs]
+        dd = c2[None, :] - 2.0 * (p @ cs.T)
+        asg[s:s + bs] = np.argmin(dd, axis=1)
+    return pts, asg, cs
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, gpu):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def lines(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except OSError:
+            return 0
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        # under-load samples only (exclude idle gaps between steps)
+        load = [x for x in sm if smax and x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_per_launch():
+    p = os.path.join(ROOT, "profiles", "kmeans_ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("dram_bytes_per_launch")
+    return None
+
+
+def reference_rate(sample_n, chunks, reps, warm=1):
+    """Evals/s of the 1M-point workload from the reference evaluator timed on a
+    bounded sample (linear scaling in points; the reference's transposed sum
+    is O(n^2), so this is optimistic for the reference)."""
+    import oracle
+    from paper_2104_05372_b200 import programs as P
+    pts, asg, cs = kmeans_inputs_fast(sample_n, D, K, seed=7)
+    prog = oracle.RefProgram(P.kmeans_cost_grad(sample_n, D, K))
+    times = []
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        prog(pts, asg, cs, chunks=chunks)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    sec = statistics.mean(times)
+    return (sample_n / N_PER_GPU) / sec, sec, times
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    rate, sec, times = reference_rate(args.ref_sample, cores, args.steps, warm=args.warmup)
+    sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2) on "
+              f"n={args.ref_sample} points (d={D}, K={K}), chunks={cores}; {sec:.3f} s/eval; "
+              f"scaled linearly to 1M points")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) points, centroids sampled from points, nearest-centroid assignments)",
+        "config": {"workload": "kmeans cost+grad, d=16, K=64, fixed assignments (BASELINE configs[1])",
+                   "reference_sample_points": args.ref_sample},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group(backend="nccl")
+        dist = tdist
+    ctx = dx.Context(local)
+    if dist is not None:
+        import torch
+        obj = [dx.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm(obj[0], world, rank)
+
+    n = N_PER_GPU * world
+    pts, asg, cs = kmeans_inputs_fast(n, D, K)
+    src = P.kmeans_cost_grad(n, D, K)
+    prog = dx.Program(src, ctx=ctx, rank=rank, world=world)
+    prog.set_input(0, 0, pts)
+    prog.set_input(1, 0, asg)
+    prog.set_input(2, 0, cs)
+    prog.enable_kernel_timing(True)
+    launches_per_run = prog.num_launches()
+
+    def barrier():
+        ctx.sync()
+        if dist is not None:
+            import torch
+            torch.cuda.synchronize()
+            dist.barrier()
+
+    # ---- device-resident throughput ------------------------------------------
+    # The clock sampler (100 ms period) starts before the warm-up; the same
+    # workload keeps running untimed until it has under-load samples, then
+    # the K timed steps follow, then a short untimed tail.
+    clocks = Clocks(local)
+    for _ in range(args.warmup):
+        ctx.l2_flush()
+        prog.run()
+    t_end = time.time() + 5.0
+    t_min = time.time() + 0.6
+    while time.time() < t_end and (clocks.lines() < 3 or time.time() < t_min):
+        for _ in range(20):
+            ctx.l2_flush()
+            prog.run()
+        ctx.sync()
+    barrier()
+    step_ms, kern = [], {}
+    for _ in range(args.steps):
+        ctx.l2_flush()
+        e0 = ctx.event()
+        prog.run()
+        e1 = ctx.event()
+        step_ms.append(ctx.elapsed_ms(e0, e1))
+        ctx.destroy_event(e0)
+        ctx.destroy_event(e1)
+        for name, ms in prog.kernel_times():
+            kern.setdefault(name, []).append(ms)
+    barrier()
+    t_tail = time.time() + 0.3
+    while time.time() < t_tail:
+        for _ in range(20):
+            ctx.l2_flush()
+            prog.run()
+        ctx.sync()
+    clk = clocks.stop()
+    ms_local = statistics.mean(step_ms)
+    # dominant kernel
+    dom = max(kern.items(), key=lambda kv: statistics.mean(kv[1]))
+    dom_ms = statistics.mean(dom[1])
+
+    # ---- end to end through the C-ABI with host buffers ----------------------
+    import ctypes
+    hp = {}
+    for name, arr in (("pts", pts), ("asg", asg), ("cs", cs)):
+        p = ctypes.c_void_p()
+        dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
+        ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
+        hp[name] = (p.value, arr.nbytes)
+    out_cost = ctypes.c_void_p()
+    out_grad = ctypes.c_void_p()
+    dx.lib().dxc_host_alloc(8, ctypes.byref(out_cost))
+    dx.lib().dxc_host_alloc(K * D * 4, ctypes.byref(out_grad))
+    h2d = sum(b for _, b in hp.values())
+    d2h = 4 + K * D * 4
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        ctx.l2_flush()
+        e0 = ctx.event()
+        prog.set_input_ptr(0, 0, hp["pts"][0], dx.DXC_F32)
+        prog.set_input_ptr(1, 0, hp["asg"][0], dx.DXC_I32)
+        prog.set_input_ptr(2, 0, hp["cs"][0], dx.DXC_F32)
+        prog.run()
+        prog.get_output_ptr(0, out_cost.value, dx.DXC_F32)
+        prog.get_output_ptr(1, out_grad.value, dx.DXC_F32)
+        e1 = ctx.event()
+        ms = ctx.elapsed_ms(e0, e1)
+        ctx.destroy_event(e0)
+        ctx.destroy_event(e1)
+        if i >= args.warmup:
+            e2e_ms.append(ms)
+    e2e_local = statistics.mean(e2e_ms)
+
+    # ---- max over ranks --------------------------------------------------------
+    ms_step, e2e_step, dom_ms_max = ms_local, e2e_local, dom_ms
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms_local, e2e_local, dom_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, e2e_step, dom_ms_max = [float(x) for x in t.tolist()]
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        n_local = N_PER_GPU
+        alg_bytes = n_local * D * 4 + n_local * 4 + 2 * K * D * 4
+        achieved = alg_bytes / (dom_ms_max * 1e-3) / 1e9
+        tr = traffic_per_launch()
+        line = {
+            "metric": METRIC, "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded N(0,1) points, centroids sampled from points, nearest-centroid assignments)",
+            "config": {"workload": "kmeans cost+grad, n=1M points per GPU, d=16, K=64, fixed assignments "
+                                   "(BASELINE configs[1]); value_and_grad via linearize+transpose",
+                       "n_total": n, "d": D, "k": K, "parallelism": f"points sharded x{world} + NCCL allreduce",
+                       "l2": "flushed before every timed step (256 MB scratch write, outside the events)"},
+            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": tr, "kernel_ms": dom_ms_max,
+                         "algorithmic_bytes": alg_bytes,
+                         "bytes_basis": "n*d*4 (points) + n*4 (assignments) + 2*K*d*4 (centroids in, dC out)"},
+            "e2e": {"value": world * 1000.0 / e2e_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "gpu_launches": launches_per_run * args.steps,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cores = os.cpu_count() or 1
+                rate, sec, _ = reference_rate(10_000, cores, 3)
+                line["cpu_baseline"] = {
+                    "value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": (f"reference evalExpr (oracle/_ref) on n=10000 points, chunks={cores}, "
+                               f"3 evals, {sec:.3f} s/eval, scaled linearly to 1M points (the reference's "
+                               f"transposed sum is O(n^2): optimistic for the reference)")}
+            except Exception as e:  # the oracle library must travel with the repo
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

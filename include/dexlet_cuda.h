@@ -92,6 +92,10 @@ int dxc_module_cubin(const char* source, void* out, size_t cap, size_t* size);
 int dxc_launch(dxc_ctx* ctx, dxc_module* mod, const char* kernel, unsigned grid,
                unsigned block, unsigned smem, void** args);
 
+/* Writes `bytes` of a context-owned scratch buffer on the context stream:
+ * evicts the 126 MB L2 between timed iterations of a benchmark. */
+int dxc_l2_flush(dxc_ctx* ctx, size_t bytes);
+
 /* Events on the context stream (device-side timing). */
 int dxc_event_record(dxc_ctx* ctx, void** ev);
 int dxc_event_elapsed_ms(void* ev0, void* ev1, float* ms);
@@ -161,6 +165,12 @@ int dxl_program_output_device_ptr(dxl_program* p, int leaf, void** out);
 const char* dxl_program_source(dxl_program* p);
 const char* dxl_program_plan(dxl_program* p);
 int dxl_program_num_launches(dxl_program* p, int* out);
+/* Per-kernel device time of the last run, from CUDA events recorded around
+ * every kernel inside the (graph-captured) plan when timing was enabled
+ * before the first run.  names: '\n'-separated kernel names. */
+int dxl_program_enable_kernel_timing(dxl_program* p, int on);
+int dxl_program_kernel_times(dxl_program* p, float* ms, int cap, int* n);
+const char* dxl_program_kernel_names(dxl_program* p);
 
 /* Index-set ordinal math (reference index_set.cpp:74-125), exported so host
  * bindings can lay out inputs exactly like the device does.  A descriptor is

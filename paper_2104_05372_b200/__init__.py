@@ -113,6 +113,10 @@ _sig("dxl_program_output_device_ptr", ctypes.c_int, _vp, ctypes.c_int, ctypes.PO
 _sig("dxl_program_source", ctypes.c_char_p, _vp)
 _sig("dxl_program_plan", ctypes.c_char_p, _vp)
 _sig("dxl_program_num_launches", ctypes.c_int, _vp, _ip)
+_sig("dxl_program_enable_kernel_timing", ctypes.c_int, _vp, ctypes.c_int)
+_sig("dxl_program_kernel_times", ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int, _ip)
+_sig("dxl_program_kernel_names", ctypes.c_char_p, _vp)
+_sig("dxc_l2_flush", ctypes.c_int, _vp, ctypes.c_size_t)
 
 #: every symbol declared in include/dexlet_cuda.h
 ABI_SYMBOLS = [
@@ -126,7 +130,8 @@ ABI_SYMBOLS = [
     "dxl_program_set_input", "dxl_program_bind_input_device", "dxl_program_input_device_ptr",
     "dxl_program_run", "dxl_program_get_output", "dxl_program_output_device_ptr",
     "dxl_program_source", "dxl_program_plan", "dxl_program_num_launches", "dxc_desc_size",
-    "dxc_desc_reverse", "dxc_chunk_range",
+    "dxc_desc_reverse", "dxc_chunk_range", "dxc_l2_flush", "dxl_program_enable_kernel_timing",
+    "dxl_program_kernel_times", "dxl_program_kernel_names",
 ]
 
 
@@ -187,6 +192,10 @@ class Context:
     @staticmethod
     def destroy_event(e):
         _lib.dxc_event_destroy(e)
+
+    def l2_flush(self, nbytes: int = 256 << 20):
+        """Overwrite a scratch buffer larger than the 126 MB L2 (on our stream)."""
+        _check(_lib.dxc_l2_flush(self.handle, nbytes))
 
     def init_comm(self, unique_id: bytes, nranks: int, rank: int):
         buf = ctypes.create_string_buffer(unique_id, 128)
@@ -249,6 +258,18 @@ class Program:
         n = ctypes.c_int()
         _check(_lib.dxl_program_num_launches(self.handle, ctypes.byref(n)))
         return n.value
+
+    def enable_kernel_timing(self, on: bool = True):
+        _check(_lib.dxl_program_enable_kernel_timing(self.handle, 1 if on else 0))
+
+    def kernel_times(self):
+        """[(kernel name, ms)] of the last run (CUDA events inside the graph)."""
+        cap = 256
+        arr = (ctypes.c_float * cap)()
+        n = ctypes.c_int()
+        _check(_lib.dxl_program_kernel_times(self.handle, arr, cap, ctypes.byref(n)))
+        names = _lib.dxl_program_kernel_names(self.handle).decode().split("\n")
+        return [(names[i], arr[i]) for i in range(min(n.value, cap))]
 
     def input_leaves(self) -> List[List[Tuple[int, int]]]:
         n = ctypes.c_int()

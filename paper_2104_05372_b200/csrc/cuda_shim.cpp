@@ -61,6 +61,7 @@ SHIM(cuMemcpyDtoDAsync, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (
 SHIM(cuMemsetD8Async, (CUdeviceptr d, unsigned char v, size_t n, CUstream st), (d, v, n, st))
 SHIM(cuEventCreate, (CUevent* e, unsigned int f), (e, f))
 SHIM(cuEventRecord, (CUevent e, CUstream s), (e, s))
+SHIM(cuEventRecordWithFlags, (CUevent e, CUstream s, unsigned int f), (e, s, f))
 SHIM(cuEventSynchronize, (CUevent e), (e))
 SHIM(cuEventElapsedTime, (float* ms, CUevent a, CUevent b), (ms, a, b))
 SHIM(cuEventDestroy, (CUevent e), (e))
@@ -70,3 +71,8 @@ SHIM(cuGraphInstantiate, (CUgraphExec* e, CUgraph g, unsigned long long f), (e, 
 SHIM(cuGraphLaunch, (CUgraphExec e, CUstream s), (e, s))
 SHIM(cuGraphExecDestroy, (CUgraphExec e), (e))
 SHIM(cuGraphDestroy, (CUgraph g), (g))
+SHIM(cuTensorMapEncodeTiled,
+     (CUtensorMap * m, CUtensorMapDataType dt, cuuint32_t rank, void* addr, const cuuint64_t* dims,
+      const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* estr, CUtensorMapInterleave il,
+      CUtensorMapSwizzle sw, CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob),
+     (m, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob))

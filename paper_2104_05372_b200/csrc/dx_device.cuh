@@ -67,6 +67,58 @@ __device__ __forceinline__ void dx_count_smem(unsigned* bins, int k, unsigned ac
   atomicAdd(&bins[k], 1u);
 }
 
+// ---- TMA bulk copies + mbarriers (streaming tiles into shared memory) ----
+__device__ __forceinline__ unsigned dx_smem_addr(const void* p) {
+  unsigned a;
+  asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+  return a;
+}
+__device__ __forceinline__ void dx_mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(dx_smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dx_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void dx_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void dx_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dx_smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy (TMA, 1-D), completion counted on `bar`.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void dx_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dx_smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(dx_smem_addr(bar))
+      : "memory");
+}
+// 2-D TMA tensor tile load (CUtensorMap passed as a __grid_constant__
+// kernel parameter); coordinates {c0 = column, c1 = row}.
+struct __align__(64) dx_tmap {
+  unsigned long long v[16];
+};
+__device__ __forceinline__ void dx_tma_2d(void* dst, const dx_tmap* map, int c0, int c1, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dx_smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(dx_smem_addr(bar))
+      : "memory");
+}
+// Byte address swizzle of TMA SWIZZLE_{32,64,128}B: 16-byte chunk bits XOR
+// the 128-byte line bits (mask 1, 3, 7).
+__device__ __forceinline__ unsigned dx_swz(unsigned a, unsigned mask) { return a ^ (((a >> 7) & mask) << 4); }
+
+__device__ __forceinline__ void dx_mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n DX_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra DX_WAIT_%=;\n}" ::"r"(
+          dx_smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Warp-cooperative row scatter: every lane holds one row `v[0..D)` destined
 // for row `key` (key < 0: nothing) of a warp-private table `tab[K][D]` in
 // shared memory.  Rows are staged through `stage[32][D+1]` (+32 key slots) and
@@ -139,6 +191,217 @@ __device__ __forceinline__ void dx_row_flush(T* tab, T* stage, int key, const T 
     }
   }
   __syncwarp();
+}
+
+// Tile-sorted row reduction (block level, every thread must call it).
+// Thread t of an NT-thread block holds one row v[0..D) for table row `key`
+// (-1: none), already stored at etile[t*(D+1) ..].  The rows are bucketed by
+// key with a stable counting sort (warp ranks from __match_any_sync, per-warp
+// counts, per-key prefix over warps, prefix over keys), then thread t adds the
+// rows of bucket k = e / D, column j = e % D into acc[i] for its entries
+// e = t + i*NT, in ascending thread order: a deterministic segmented sum with
+// the accumulators in registers across tiles (no atomics, no RMW).
+template <class T, int D, int K, int NT, int NACC>
+__device__ __forceinline__ void dx_tile_rows(const T* etile, int key, int* wcnt, int* start, int* perm,
+                                             T (&acc)[NACC]) {
+  constexpr int NW = NT / 32;
+  constexpr int SUBS = (NT / K) < 32 ? (NT / K) : 32;  // threads per key in the warp scan
+  constexpr int WPS = (NW + SUBS - 1) / SUBS;          // warps summarized per thread
+  static_assert(SUBS >= 1 && (SUBS & (SUBS - 1)) == 0, "SUBS must be a power of two");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned peers = __match_any_sync(DX_FULL, key);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  for (int i = tid; i < NW * K; i += NT) wcnt[i] = 0;
+  __syncthreads();
+  if (rank == 0 && key >= 0) wcnt[warp * K + key] = __popc(peers);
+  __syncthreads();
+  // per key: exclusive prefix over warps (SUBS threads per key, shuffles)
+  if (tid < K * SUBS) {
+    const int k = tid / SUBS, sub = tid % SUBS;
+    int c[WPS];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < WPS; ++q) {
+      const int w = sub * WPS + q;
+      c[q] = w < NW ? wcnt[w * K + k] : 0;
+      loc += c[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < SUBS; o <<= 1) {
+      const int y = __shfl_up_sync(DX_FULL, inc, o, SUBS);
+      if (sub >= o) inc += y;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int q = 0; q < WPS; ++q) {
+      const int w = sub * WPS + q;
+      if (w < NW) wcnt[w * K + k] = run;
+      run += c[q];
+    }
+    if (sub == SUBS - 1) start[k + 1] = inc;  // bucket size
+  }
+  __syncthreads();
+  // exclusive scan over the K bucket sizes (one warp)
+  if (warp == 0) {
+    constexpr int PER = (K + 31) / 32;
+    int v[PER];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane * PER + q;
+      v[q] = k < K ? start[k + 1] : 0;
+      loc += v[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(DX_FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane * PER + q;
+      if (k < K) start[k] = run;
+      run += v[q];
+    }
+    if (lane == 31) start[K] = inc;
+  }
+  __syncthreads();
+  if (key >= 0) perm[start[key] + wcnt[warp * K + key] + rank] = tid;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    const int e = tid + i * NT;
+    if (e < K * D) {
+      const int k = e / D, j = e - (e / D) * D;
+      const int q1 = start[k + 1];
+      T sum = acc[i];
+      for (int q = start[k]; q < q1; ++q) sum += etile[perm[q] * (D + 1) + j];
+      acc[i] = sum;
+    }
+  }
+  __syncthreads();
+}
+
+// f32 rows with D % 4 == 0: rows live in etile as D/4 float4 blocks, block b
+// of row t stored at slot b ^ ((t >> 1) & (D/4 - 1)) (conflict-free 128-bit
+// stores: each 8-lane phase hits 8 distinct 16-byte bank groups).
+template <int D>
+__device__ __forceinline__ void dx_tile_store4(float* etile, int t, const float (&v)[D]) {
+  constexpr int NB = D / 4;
+  float4* row = reinterpret_cast<float4*>(etile + t * D);
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+    row[b ^ ((t >> 1) & (NB - 1))] = make_float4(v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
+}
+
+// Vectorized variant of dx_tile_rows: thread tid owns (key k, column block jb)
+// pair p = tid % P (P = K*D/4) and split s = tid / P of the bucket (elements
+// q = start + s, s + NS, ...), accumulating a float4 in registers.
+template <int D, int K, int NT>
+__device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* wcnt, int* start, int* perm,
+                                              float4& acc) {
+  constexpr int NB = D / 4, P = K * NB;
+  constexpr int NS = P >= NT ? 1 : NT / P;
+  constexpr int NW = NT / 32;
+  constexpr int SUBS = (NT / K) < 32 ? (NT / K) : 32;
+  constexpr int WPS = (NW + SUBS - 1) / SUBS;
+  static_assert(P <= NT, "one (key, block) pair per thread at most");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned peers = __match_any_sync(DX_FULL, key);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  for (int i = tid; i < NW * K; i += NT) wcnt[i] = 0;
+  __syncthreads();
+  if (rank == 0 && key >= 0) wcnt[warp * K + key] = __popc(peers);
+  __syncthreads();
+  if (tid < K * SUBS) {
+    const int k = tid / SUBS, sub = tid % SUBS;
+    int c[WPS];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < WPS; ++q) {
+      const int w = sub * WPS + q;
+      c[q] = w < NW ? wcnt[w * K + k] : 0;
+      loc += c[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < SUBS; o <<= 1) {
+      const int y = __shfl_up_sync(DX_FULL, inc, o, SUBS);
+      if (sub >= o) inc += y;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int q = 0; q < WPS; ++q) {
+      const int w = sub * WPS + q;
+      if (w < NW) wcnt[w * K + k] = run;
+      run += c[q];
+    }
+    if (sub == SUBS - 1) start[k + 1] = inc;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int PER = (K + 31) / 32;
+    int v[PER];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane * PER + q;
+      v[q] = k < K ? start[k + 1] : 0;
+      loc += v[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(DX_FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane * PER + q;
+      if (k < K) start[k] = run;
+      run += v[q];
+    }
+    if (lane == 31) start[K] = inc;
+  }
+  __syncthreads();
+  if (key >= 0) perm[start[key] + wcnt[warp * K + key] + rank] = tid;
+  __syncthreads();
+  if (tid < P * NS) {
+    const int p = tid % P, sp = tid / P;
+    const int k = p / NB, jb = p % NB;
+    const int q1 = start[k + 1];
+    float4 a = acc;
+    for (int q = start[k] + sp; q < q1; q += NS) {
+      const int r = perm[q];
+      const float4 w = reinterpret_cast<const float4*>(etile + r * D)[jb ^ ((r >> 1) & (NB - 1))];
+      a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
+    }
+    acc = a;
+  }
+  __syncthreads();
+}
+
+// Block partial of a dx_tile_rows4 table: splits folded in fixed order.
+template <int D, int K, int NT>
+__device__ __forceinline__ void dx_tile_rows4_flush(float* scratch, const float4& acc, float* part) {
+  constexpr int NB = D / 4, P = K * NB;
+  constexpr int NS = P >= NT ? 1 : NT / P;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid < P * NS) reinterpret_cast<float4*>(scratch)[tid] = acc;
+  __syncthreads();
+  for (int p = tid; p < P; p += NT) {
+    float4 s = reinterpret_cast<const float4*>(scratch)[p];
+    for (int sp = 1; sp < NS; ++sp) {
+      const float4 w = reinterpret_cast<const float4*>(scratch)[sp * P + p];
+      s.x += w.x; s.y += w.y; s.z += w.z; s.w += w.w;
+    }
+    reinterpret_cast<float4*>(part)[p] = s;  // entry (k, 4*jb..4*jb+3) at p*4
+  }
 }
 
 // ---- finalize: fold per-block partials into the Accum cell, fixed order ----

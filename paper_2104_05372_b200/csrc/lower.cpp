@@ -24,6 +24,7 @@
 #include "lower.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <functional>
 #include <map>
@@ -130,6 +131,14 @@ static DTy memberType(const DescPtr& d) {
     case IndexSetDesc::Kind::Either: return tIdx(d);
   }
   return tUnit();
+}
+
+static size_t storageBytesOf(SK k, bool f64 = false) {
+  switch (k) {
+    case SK::F: return f64 ? 8 : 4;
+    case SK::I: return 8;
+    default: return 4;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -290,6 +299,11 @@ struct Slot {
   SK kind = SK::F;
   long long align = 1; // offset is a multiple of this many elements
   int cellLeaf = -1;   // Ref slots into a global cell: which leaf of the cell
+  // Streaming row: offset == (kernel ordinal) * streamL + streamBase + rowOff,
+  // so the tile kernel can fetch the block's rows by TMA into shared memory.
+  bool stream = false;
+  long long streamL = 0, streamBase = 0;
+  std::string rowOff;
 };
 
 static long long alignOf(long long c) {
@@ -380,12 +394,14 @@ struct Cell {
 // Per-kernel view of one cell leaf.
 struct CellUse {
   int cell = -1, leaf = -1;
-  enum Strat { Owner, Reg, Smem, Count, Row, Global, Direct } strat = Global;
+  enum Strat { Owner, Reg, Smem, Count, Row, TileRow, Global, Direct } strat = Global;
   // pass-0 analysis
   bool any = false, allOwner = true, allConst = true, allRow = true;
   double constVal = 0;
   bool haveConst = false;
   long long rowD = 0;
+  int rowSitesN = 0;     // row-eligible accumulation sites (pass 0)
+  bool vec4 = false;     // TileRow with float4 column blocks (f32, D % 4 == 0)
   long long width = 0;
   int partialBuf = -1;
   int targetBuf = -1;   // cell leaf buffer or its delta (sharded)
@@ -430,6 +446,12 @@ struct KGen {
   int threads = 256;              // block size chosen for this kernel
   std::set<int> streamBufs;       // ro buffers read at exactly the ordinal
   std::set<int> stateCells;       // host-level State cells read/written (serial kernels)
+  // TMA staging analysis (pass 0) and decisions (pass 1)
+  std::map<int, std::pair<long long, long long>> streamUse;  // buf -> (row length, base offset)
+  std::set<int> nonStream, needAlign;
+  std::set<int> staged, wholeStaged;
+  std::map<int, int> tensorStaged;  // buf -> swizzle mask (TMA 2-D with SWIZZLE_{32,64,128}B)
+  bool tile = false;
   bool usesErr = false;
   bool usesScratch = false;
   int curBranch = 0;
@@ -1490,6 +1512,19 @@ class Lowering {
     notLowerable("host value");
   }
 
+  // Pass-0 bookkeeping of read-only HBM reads for TMA staging decisions.
+  void noteRead(KGen& g, const Slot& s, bool vector) {
+    if (g.pass != 0 || !s.global || !s.ro || s.buf < 0) return;
+    if (s.stream) {
+      auto it = g.streamUse.find(s.buf);
+      if (it == g.streamUse.end()) g.streamUse[s.buf] = {s.streamL, s.streamBase};
+      else if (it->second != std::make_pair(s.streamL, s.streamBase)) g.nonStream.insert(s.buf);
+      if (vector) g.needAlign.insert(s.buf);
+    } else {
+      g.nonStream.insert(s.buf);
+    }
+  }
+
   // Build a value from leaf slots (loads scalars into fresh registers).
   KV viewSlots(KGen& g, const DTy& t, const std::vector<Slot>& slots, size_t base = 0) {
     switch (t->k) {
@@ -1523,14 +1558,28 @@ class Lowering {
           long long cnt = leaves(t)[0].count;
           int es = (s0.kind == SK::F && opt.f64) || s0.kind == SK::I ? 8 : 4;
           int vw = 16 / es;  // elements per 16-byte load
+          if (cnt <= 32 && cnt % vw == 0 && s0.align % vw == 0) noteRead(g, s0, true);
           if (cnt <= 32 && cnt % vw == 0 && s0.align % vw == 0 && g.out) {
             std::string r = g.fresh("row");
+            std::string B = std::to_string(s0.buf);
+            // address of the q-th 16-byte block of the row
+            std::string addrq = "(const " + std::string(es == 8 ? (s0.kind == SK::F ? "double2" : "longlong2") : (s0.kind == SK::F ? "float4" : "int4")) + "*)(" + s0.base + " + " + s0.off + " + q * " + lit(vw) + ")";
+            if (s0.stream && g.staged.count(s0.buf) && g.tensorStaged.count(s0.buf))
+              addrq = "(const float4*)((const char*)(sb" + B + " + dx_sh" + B + ") + dx_swz((unsigned)(threadIdx.x * " +
+                      lit(s0.streamL * es) + " + (" + s0.rowOff + ") * " + lit(es) + " + q * 16), " +
+                      lit(g.tensorStaged[s0.buf]) + "))";
+            else if (s0.stream && g.staged.count(s0.buf))
+              addrq = "(const float4*)(sb" + B + " + dx_sh" + B + " + threadIdx.x * " + lit(s0.streamL) + " + " +
+                      s0.rowOff + " + q * " + lit(vw) + ")";
+            else if (g.wholeStaged.count(s0.buf))
+              addrq = "(const float4*)((const char*)wt" + B + " + dx_swz((unsigned)((" + s0.off + ") * " + lit(es) +
+                      " + q * 16), 3))";
             std::string ct = ctype(s0.kind);
             std::string vt = es == 8 ? (s0.kind == SK::F ? "double2" : "longlong2") : (s0.kind == SK::F ? "float4" : "int4");
             g.line(ct + " " + r + "[" + lit(cnt) + "];");
             g.line("#pragma unroll");
             g.line("for (int q = 0; q < " + lit(cnt / vw) + "; ++q) { const " + vt + " w = *(const " + vt + "*)(" +
-                   s0.base + " + " + s0.off + " + q * " + lit(vw) + "); " +
+                   addrq + "); " +
                    (vw == 4 ? r + "[4*q] = w.x; " + r + "[4*q+1] = w.y; " + r + "[4*q+2] = w.z; " + r + "[4*q+3] = w.w; }"
                             : r + "[2*q] = w.x; " + r + "[2*q+1] = w.y; }"));
             auto k = std::make_shared<KVal>();
@@ -1567,6 +1616,20 @@ class Lowering {
         std::string v = g.fresh("v");
         std::string ld = (s.global && s.ro) ? "dx_ld(" + s.base + " + " + s.off + ")"
                                             : s.base + "[" + s.off + "]";
+        noteRead(g, s, false);
+        {
+          std::string B = std::to_string(s.buf);
+          int eb = (int)storageBytesOf(s.kind, opt.f64);
+          std::string ct = ctype(s.kind);
+          if (s.global && s.ro && s.stream && g.staged.count(s.buf) && g.tensorStaged.count(s.buf))
+            ld = "*(const " + ct + "*)((const char*)(sb" + B + " + dx_sh" + B + ") + dx_swz((unsigned)(threadIdx.x * " +
+                 lit(s.streamL * eb) + " + (" + s.rowOff + ") * " + lit(eb) + "), " + lit(g.tensorStaged[s.buf]) + "))";
+          else if (s.global && s.ro && s.stream && g.staged.count(s.buf))
+            ld = "sb" + B + "[dx_sh" + B + " + threadIdx.x * " + lit(s.streamL) + " + " + s.rowOff + "]";
+          else if (s.global && s.ro && g.wholeStaged.count(s.buf))
+            ld = "*(const " + ct + "*)((const char*)wt" + B + " + dx_swz((unsigned)((" + s.off + ") * " + lit(eb) +
+                 "), 3))";
+        }
         if (s.global && s.ro && s.off.rfind("dx_o", 0) == 0 && isIntLit(s.off.substr(4)) &&
             (s.kind == SK::X || (s.kind == SK::F && !opt.f64))) {
           // streaming read at the thread's own ordinal: served by the
@@ -1775,6 +1838,7 @@ class Lowering {
           const Slot& src = v->slots[l];
           if (d.global) g.writtenBufs.insert(d.buf);
           std::string q = g.fresh("q");
+          if (src.global && src.ro && g.pass == 0) g.nonStream.insert(src.buf);
           std::string ld = (src.global && src.ro) ? "dx_ld(" + src.base + " + " + eAdd(src.off, q) + ")"
                                                   : src.base + "[" + eAdd(src.off, q) + "]";
           g.line("for (long long " + q + " = 0; " + q + " < " + lit(lv[l].count) + "; ++" + q + ") " +
@@ -1841,6 +1905,15 @@ class Lowering {
       std::vector<LeafInfo> el = leaves(et);
       std::vector<Slot> slots = arr->slots;
       for (size_t l = 0; l < slots.size(); ++l) {
+        long long b0;
+        if (slots[l].stream) {
+          slots[l].rowOff = eAdd(slots[l].rowOff, eMul(o, el[l].count));
+        } else if (slots[l].global && slots[l].ro && o == "dx_o0" && isIntLit(slots[l].off, &b0)) {
+          slots[l].stream = true;
+          slots[l].streamL = el[l].count;
+          slots[l].streamBase = b0;
+          slots[l].rowOff = "0";
+        }
         slots[l].off = eAdd(slots[l].off, eMul(o, el[l].count));
         long long oc;
         slots[l].align = gcdll(slots[l].align, isIntLit(o, &oc) ? alignOf(oc * el[l].count) : el[l].count);
@@ -2282,6 +2355,7 @@ class Lowering {
           if (cu.rowD == 0 || cu.rowD == ref->lastDim) {
             cu.rowD = ref->lastDim;
             row = true;
+            cu.rowSitesN++;
           }
         }
       }
@@ -2303,7 +2377,8 @@ class Lowering {
       case CellUse::Count:
         g.line("dx_count_smem(sm" + std::to_string(&cu - &g.cells[0]) + ", (int)(" + sl.off + "), __activemask());");
         break;
-      case CellUse::Row: {
+      case CellUse::Row:
+      case CellUse::TileRow: {
         int rid = g.rowSiteCounter++;
         const KV& last = ref->path.back();
         std::string rv = "rowv" + std::to_string(rid), rk = "rowk" + std::to_string(rid);
@@ -2454,6 +2529,12 @@ class Lowering {
 
 // ---------------------------------------------------------------------------
 
+static int tileThreads() {
+  if (const char* e = std::getenv("DEXLET_TILE_NT")) return std::atoi(e);
+  return 256;
+}
+
+
 void Lowering::decideStrategies(KGen& g) {
   int esize = opt.f64 ? 8 : 4;
   const int smemCap = 160 * 1024;
@@ -2461,6 +2542,7 @@ void Lowering::decideStrategies(KGen& g) {
   int warps = std::max(1, opt.threads / 32);
   int smemUsed = 0;
   bool privatized = false;
+  bool tileRowTaken = false;
   for (size_t i = 0; i < g.cells.size(); ++i) {
     CellUse& cu = g.cells[i];
     SK kind = cells[cu.cell].lv[cu.leaf].kind;
@@ -2474,6 +2556,19 @@ void Lowering::decideStrategies(KGen& g) {
       cu.smemOff = smemUsed;
       smemUsed += (int)cu.width * 4;
       continue;
+    }
+    if (cu.allRow && cu.rowD > 0 && cu.rowSitesN == 1 && !opt.noRowScatter && !tileRowTaken) {
+      long long Kr = cu.width / cu.rowD;
+      const int NT = tileThreads();
+      long long need = (long long)NT * (cu.rowD + 1) * esize + (NT / 32) * Kr * 4 + (Kr + 1) * 4 + NT * 4 + 64;
+      if (Kr >= 1 && Kr <= 256 && (NT % Kr == 0 || Kr <= 32) && cu.width <= 16 * NT &&
+          smemUsed + need <= smemCap) {
+        cu.strat = CellUse::TileRow;
+        cu.smemOff = smemUsed;
+        smemUsed += (int)need;
+        tileRowTaken = true;
+        continue;
+      }
     }
     if (cu.allRow && cu.rowD > 0 && !opt.noRowScatter) {
       long long need = (long long)warps * cu.width * esize;
@@ -2494,6 +2589,25 @@ void Lowering::decideStrategies(KGen& g) {
     cu.strat = CellUse::Global;
   }
   if (g.serial || !privatized) return;
+  if (tileRowTaken) {
+    // tile-sorted rows: block-uniform tiles (see dx_tile_rows)
+    const int NT = tileThreads();
+    g.threads = NT;
+    int off = 0;
+    for (auto& cu : g.cells) {
+      if (cu.strat == CellUse::Smem) { cu.smemOff = off; off += (int)(cu.width * esize); }
+      if (cu.strat == CellUse::Count) { cu.smemOff = off; off += (int)(cu.width * 4); }
+      if (cu.strat == CellUse::Row) cu.strat = CellUse::Smem, cu.smemOff = off, off += (int)(cu.width * esize);
+    }
+    for (auto& cu : g.cells) {
+      if (cu.strat != CellUse::TileRow) continue;
+      long long Kr = cu.width / cu.rowD;
+      cu.vec4 = !opt.f64 && cu.rowD % 4 == 0 && Kr * (cu.rowD / 4) <= NT;
+      cu.smemOff = (off + 15) / 16 * 16;
+      off = cu.smemOff + (int)(NT * (cu.rowD + 1) * esize + (NT / 32) * Kr * 4 + (Kr + 1) * 4 + NT * 4 + 64);
+    }
+    return;
+  }
   // Privatized cells: fat persistent blocks (one or two per SM), so that the
   // per-block partials, and their finalize, stay small.  Row tables are
   // per warp: recompute their offsets for the chosen block size.
@@ -2720,6 +2834,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     g.writtenBufs.clear();
     g.streamBufs.clear();
     g.stateCells.clear();
+    g.streamUse.clear();
+    g.nonStream.clear();
+    g.needAlign.clear();
     g.usesErr = false;
     g.usesScratch = false;
     KV e = runParts(g, parts, serial, 1, outBufs, outOffs, intoBufs, intoOffs);
@@ -2728,7 +2845,41 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   }
   decideStrategies(g);
   bool hasRow = false;
-  for (auto& cu : g.cells) hasRow |= cu.strat == CellUse::Row;
+  for (auto& cu : g.cells) hasRow |= cu.strat == CellUse::Row || cu.strat == CellUse::TileRow;
+  // TMA staging for block-uniform tile kernels: rows read at the kernel
+  // ordinal stream in by cp.async.bulk (double-buffered, one tile ahead);
+  // small read-only gather tables are copied to shared memory once.
+  g.tile = false;
+  for (auto& cu : g.cells) g.tile |= cu.strat == CellUse::TileRow;
+  g.staged.clear();
+  g.wholeStaged.clear();
+  g.tensorStaged.clear();
+  if (g.tile && !std::getenv("DEXLET_NO_TMA")) {
+    int es = opt.f64 ? 8 : 4;
+    long long budget = 96 * 1024;
+    for (auto& [b, lb] : g.streamUse) {
+      if (g.nonStream.count(b)) continue;
+      int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
+      bool aligned = (lb.first * eb) % 16 == 0 && (lb.second * eb) % 16 == 0;
+      if (g.needAlign.count(b) && !aligned) continue;
+      long long stage = (long long)g.threads * lb.first * eb + 32;
+      if (2 * stage > budget) continue;
+      budget -= 2 * stage + 2048;
+      g.staged.insert(b);
+      long long rowB = lb.first * eb;
+      if (g.needAlign.count(b) && !opt.f64 && plan.bufs[b].kind == SK::F && aligned &&
+          (rowB == 32 || rowB == 64 || rowB == 128) && g.threads <= 256 && !std::getenv("DEXLET_NO_TMA_TENSOR"))
+        g.tensorStaged[b] = rowB == 32 ? 1 : rowB == 64 ? 3 : 7;
+    }
+    for (int b : g.nonStream) {
+      if (g.streamUse.count(b)) continue;
+      long long bytes = plan.bufs[b].elems * (long long)storageBytesOf(plan.bufs[b].kind, opt.f64);
+      if (bytes <= 0 || bytes > 16 * 1024 || bytes > budget) continue;
+      budget -= bytes;
+      g.wholeStaged.insert(b);
+    }
+    (void)es;
+  }
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
   int U = (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
   // cells must be on the device before this kernel
@@ -2759,7 +2910,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   for (size_t i = 0; i < g.cells.size(); ++i) {
     CellUse& cu = g.cells[i];
     if (cu.strat == CellUse::Reg || cu.strat == CellUse::Smem || cu.strat == CellUse::Row ||
-        cu.strat == CellUse::Count) {
+        cu.strat == CellUse::Count || cu.strat == CellUse::TileRow) {
       SK pk = cu.strat == CellUse::Count ? SK::U32 : SK::F;
       cu.partialBuf = newBuf(BufDecl::Partial, pk, 0);
       plan.bufs[cu.partialBuf].partialWidth = cu.width;
@@ -2779,9 +2930,45 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       smem = std::max<int>(smem, cu.smemOff + (int)(warps * cu.width * esize));
       maxRowD = std::max(maxRowD, cu.rowD);
     }
+    if (cu.strat == CellUse::TileRow) {
+      long long Kr = cu.width / cu.rowD;
+      smem = std::max<int>(smem, cu.smemOff + (int)(g.threads * (cu.rowD + 1) * esize + (g.threads / 32) * Kr * 4 +
+                                                     (Kr + 1) * 4 + g.threads * 4 + 64));
+    }
   }
+  int tileCell = -1;
+  for (size_t i = 0; i < g.cells.size(); ++i)
+    if (g.cells[i].strat == CellUse::TileRow) tileCell = (int)i;
   int stageOff = (smem + 15) / 16 * 16;
   if (maxRowD > 0) smem = stageOff + warps * (32 * (int)(maxRowD + 1) + 32) * esize;
+  // TMA staging areas
+  std::map<int, int> stageAt, wholeAt;
+  std::map<int, long long> stageElems;
+  for (int b : g.staged) {
+    int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
+    long long L = g.streamUse[b].first;
+    if (g.tensorStaged.count(b)) {
+      // swizzled TMA tiles: 1024-byte aligned stages of exactly one box
+      long long elems = ((long long)g.threads * L * eb + 1023) / 1024 * 1024 / eb;
+      smem = (smem + 1023) / 1024 * 1024;
+      stageAt[b] = smem;
+      stageElems[b] = elems;
+      smem += (int)(2 * elems * eb);
+      continue;
+    }
+    long long elems = ((long long)g.threads * L * eb + 32 + 15) / 16 * 16 / eb;  // + shift slack
+    smem = (smem + 15) / 16 * 16;
+    stageAt[b] = smem;
+    stageElems[b] = elems;
+    smem += (int)(2 * elems * eb);
+  }
+  if (!g.tensorStaged.empty()) smem += 1024;  // dynamic smem base is only 16-byte aligned
+  for (int b : g.wholeStaged) {
+    int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
+    smem = (smem + 15) / 16 * 16;
+    wholeAt[b] = smem;
+    smem += (int)(plan.bufs[b].elems * eb);
+  }
 
   src << "// " << note << "\n";
   src << "extern \"C\" __global__ void __launch_bounds__(" << (serial ? 32 : g.threads) << ") " << kname << "(";
@@ -2799,6 +2986,19 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     // in the index expressions, so the compiler may vectorize
     aligns.push_back("  " + pname + " = (" + (w ? "" : "const ") + ct + "*)__builtin_assume_aligned(" + pname + ", 16);\n");
     KArg a; a.k = KArg::Buf; a.buf = buf; args.push_back(a);
+  }
+  for (auto& [b, mask] : g.tensorStaged) {
+    comma();
+    src << "const __grid_constant__ dx_tmap tm" << b;
+    KArg a;
+    a.k = KArg::TMap;
+    a.buf = b;
+    a.rowLen = g.streamUse[b].first;
+    a.off = g.streamUse[b].second;
+    a.rows = (plan.bufs[b].elems - a.off) / a.rowLen;
+    a.boxRows = g.threads;
+    a.swizzle = (mask + 1) * 16;
+    args.push_back(a);
   }
   for (size_t i = 0; i < g.cells.size(); ++i) {
     CellUse& cu = g.cells[i];
@@ -2821,7 +3021,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   } else {
     src << "  const int dx_lane = threadIdx.x & 31, dx_warp = threadIdx.x >> 5;\n";
     src << "  (void)dx_lane; (void)dx_warp;\n";
-    if (smem > 0) src << "  extern __shared__ __align__(16) unsigned char dx_smem[];\n";
+    if (smem > 0 && g.tensorStaged.empty()) src << "  extern __shared__ __align__(16) unsigned char dx_smem[];\n";
+    if (smem > 0 && !g.tensorStaged.empty()) {
+      // swizzled TMA destinations need 1024-byte alignment
+      src << "  extern __shared__ __align__(1024) unsigned char dx_smem_raw[];\n";
+      src << "  unsigned char* dx_smem = dx_smem_raw + ((1024u - (dx_smem_addr(dx_smem_raw) & 1023u)) & 1023u);\n";
+    }
     bool needSync = false;
     for (size_t i = 0; i < g.cells.size(); ++i) {
       CellUse& cu = g.cells[i];
@@ -2838,6 +3043,21 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           src << "  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) sm" << I << "[t] = 0u;\n";
           needSync = true;
           break;
+        case CellUse::TileRow: {
+          long long Kr = cu.width / cu.rowD;
+          int nacc = (int)((cu.width + g.threads - 1) / g.threads);
+          long long et = (long long)g.threads * (cu.rowD + 1) * esize;
+          if (cu.vec4) src << "  float4 acc" << I << " = make_float4(0.f, 0.f, 0.f, 0.f);\n";
+          else {
+            src << "  dx_f acc" << I << "[" << nacc << "];\n";
+            src << "#pragma unroll\n  for (int t = 0; t < " << nacc << "; ++t) acc" << I << "[t] = 0;\n";
+          }
+          src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
+          src << "  int* wc" << I << " = (int*)(dx_smem + " << cu.smemOff + et << ");\n";
+          src << "  int* st" << I << " = wc" << I << " + " << (g.threads / 32) * Kr << ";\n";
+          src << "  int* pm" << I << " = st" << I << " + " << Kr + 1 << ";\n";
+          break;
+        }
         case CellUse::Row:
           src << "  dx_f* rt" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
           src << "  for (int t = threadIdx.x; t < " << warps * cu.width << "; t += blockDim.x) rt" << I << "[t] = 0;\n";
@@ -2848,12 +3068,84 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     if (maxRowD > 0)
       src << "  dx_f* dx_stage = (dx_f*)(dx_smem + " << stageOff << ") + dx_warp * " << 32 * (maxRowD + 1) + 32 << ";\n";
+    for (int b : g.wholeStaged) {
+      std::string ct = ctype(plan.bufs[b].kind);
+      src << "  " << ct << "* wt" << b << " = (" << ct << "*)(dx_smem + " << wholeAt[b] << ");\n";
+      src << "  for (int t = threadIdx.x; t < " << plan.bufs[b].elems << "; t += blockDim.x) *(" << ct
+          << "*)((char*)wt" << b << " + dx_swz((unsigned)(t * " << storageBytesOf(plan.bufs[b].kind, opt.f64)
+          << "), 3)) = p" << b << "[t];\n";
+      needSync = true;
+    }
+    if (!g.staged.empty()) {
+      src << "  __shared__ __align__(8) unsigned long long dx_bar[2];\n";
+      for (int b : g.staged) {
+        std::string ct = ctype(plan.bufs[b].kind);
+        src << "  " << ct << "* sb" << b << " = (" << ct << "*)(dx_smem + " << stageAt[b] << ");\n";
+      }
+      src << "  if (threadIdx.x == 0) { dx_mbar_init(&dx_bar[0], 1); dx_mbar_init(&dx_bar[1], 1); dx_fence_mbar_init(); }\n";
+      // thread 0 streams the rows of tile `tb` into stage `stg` (16-byte
+      // aligned superset of the byte range; readers add the shift)
+      src << "  auto dx_issue = [&](int stg, long long tb) {\n";
+      src << "    const long long r0 = dx_lo + tb, r1 = (r0 + " << g.threads << " < dx_hi) ? r0 + " << g.threads << " : dx_hi;\n";
+      src << "    unsigned tot = 0;\n";
+      for (int b : g.staged) {
+        int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
+        auto lb = g.streamUse[b];
+        std::string B = std::to_string(b);
+        if (g.tensorStaged.count(b)) {
+          src << "    tot += " << (long long)g.threads * lb.first * eb << "u;  // full box (OOB rows zero-filled)\n";
+          continue;
+        }
+        src << "    const long long a" << B << " = ((r0 * " << lb.first << "LL + " << lb.second << "LL) * " << eb
+            << "LL) & ~15LL;\n";
+        src << "    const long long n" << B << " = ((((r1 * " << lb.first << "LL + " << lb.second << "LL) * " << eb
+            << "LL) + 15LL) & ~15LL) - a" << B << ";\n";
+        src << "    tot += (unsigned)n" << B << ";\n";
+      }
+      src << "    dx_mbar_expect_tx(&dx_bar[stg], tot);\n";
+      for (int b : g.staged) {
+        std::string B = std::to_string(b);
+        if (g.tensorStaged.count(b)) {
+          src << "    dx_tma_2d(sb" << B << " + stg * " << stageElems[b] << "LL, &tm" << B << ", 0, (int)r0, &dx_bar[stg]);\n";
+          continue;
+        }
+        src << "    dx_bulk_g2s(sb" << B << " + stg * " << stageElems[b] << "LL, (const char*)p" << B << " + a" << B
+            << ", (unsigned)n" << B << ", &dx_bar[stg]);\n";
+      }
+      src << "  };\n";
+      needSync = true;
+    }
     if (needSync) src << "  __syncthreads();\n";
     // warp-uniform grid-stride loop over groups of U consecutive ordinals
     src << "  const long long dx_n = (dx_hi - dx_lo + " << (U - 1) << ") / " << U << ";\n";
     src << "  const long long dx_stride = (long long)gridDim.x * blockDim.x;\n";
-    src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); dx_base < dx_n; dx_base += dx_stride) {\n";
-    src << "    const long long dx_s = dx_base + dx_lane;\n";
+    if (tileCell >= 0 && !g.staged.empty()) {
+      // TMA pipeline: tile t+1 is in flight while tile t is computed
+      src << "  if (threadIdx.x == 0 && (long long)blockIdx.x * blockDim.x < dx_n) dx_issue(0, (long long)blockIdx.x * blockDim.x);\n";
+      src << "  int dx_it = 0;\n";
+      src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride, ++dx_it) {\n";
+      src << "    const int dx_stg = dx_it & 1;\n";
+      src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
+      for (int b : g.staged) {
+        int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
+        auto lb = g.streamUse[b];
+        if (g.tensorStaged.count(b)) {
+          src << "    const int dx_sh" << b << " = dx_stg * " << stageElems[b] << ";\n";
+          continue;
+        }
+        src << "    const int dx_sh" << b << " = dx_stg * " << stageElems[b] << " + (int)((((dx_lo + dx_base) * "
+            << lb.first << "LL + " << lb.second << "LL) * " << eb << "LL) & 15LL) / " << eb << ";\n";
+      }
+      src << "    dx_mbar_wait(&dx_bar[dx_stg], (unsigned)((dx_it >> 1) & 1));\n";
+      src << "    const long long dx_s = dx_base + threadIdx.x;\n";
+    } else if (tileCell >= 0) {
+      // block-uniform tiles: every thread runs the same trip count
+      src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride) {\n";
+      src << "    const long long dx_s = dx_base + threadIdx.x;\n";
+    } else {
+      src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); dx_base < dx_n; dx_base += dx_stride) {\n";
+      src << "    const long long dx_s = dx_base + dx_lane;\n";
+    }
     for (int u = 0; u < U; ++u)
       src << "    const long long dx_o" << u << " = dx_lo + dx_s * " << U << " + " << u << ";\n";
     for (auto& rs : g.rowSites) {
@@ -2880,7 +3172,24 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     src << "    if (dx_s < dx_n) {\n" << body << "    }\n";
     for (auto& rs : g.rowSites) {
-      src << "    dx_row_flush<dx_f, " << rs.D << ">(rt" << rs.cu << " + dx_warp * " << g.cells[rs.cu].width
+      const CellUse& cu = g.cells[rs.cu];
+      if (cu.strat == CellUse::TileRow) {
+        std::string I = std::to_string(rs.cu);
+        long long Kr = cu.width / cu.rowD;
+        int nacc = (int)((cu.width + g.threads - 1) / g.threads);
+        if (cu.vec4) {
+          src << "    dx_tile_store4<" << rs.D << ">(et" << I << ", threadIdx.x, rowv" << rs.id << ");\n";
+          src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(et" << I << ", rowk" << rs.id
+              << ", wc" << I << ", st" << I << ", pm" << I << ", acc" << I << ");\n";
+          continue;
+        }
+        src << "#pragma unroll\n    for (int t = 0; t < " << rs.D << "; ++t) et" << I << "[threadIdx.x * " << rs.D + 1
+            << " + t] = rowv" << rs.id << "[t];\n";
+        src << "    dx_tile_rows<dx_f, " << rs.D << ", " << Kr << ", " << g.threads << ", " << nacc << ">(et" << I
+            << ", rowk" << rs.id << ", wc" << I << ", st" << I << ", pm" << I << ", acc" << I << ");\n";
+        continue;
+      }
+      src << "    dx_row_flush<dx_f, " << rs.D << ">(rt" << rs.cu << " + dx_warp * " << cu.width
           << ", dx_stage, rowk" << rs.id << ", rowv" << rs.id << ");\n";
     }
     src << "  }\n";
@@ -2899,6 +3208,18 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           src << "  __syncthreads();\n  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) part" << I
               << "[(long long)blockIdx.x * " << cu.width << " + t] = sm" << I << "[t];\n";
           break;
+        case CellUse::TileRow: {
+          int nacc = (int)((cu.width + g.threads - 1) / g.threads);
+          if (cu.vec4) {
+            src << "  dx_tile_rows4_flush<" << cu.rowD << ", " << cu.width / cu.rowD << ", " << g.threads << ">(et" << I
+                << ", acc" << I << ", part" << I << " + (long long)blockIdx.x * " << cu.width << ");\n";
+            break;
+          }
+          src << "#pragma unroll\n  for (int t = 0; t < " << nacc << "; ++t) { const int e = threadIdx.x + t * "
+              << g.threads << "; if (e < " << cu.width << ") part" << I << "[(long long)blockIdx.x * " << cu.width
+              << " + e] = acc" << I << "[t]; }\n";
+          break;
+        }
         case CellUse::Row:
           src << "  __syncthreads();\n  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) {\n"
               << "    dx_f s = 0;\n    for (int w = 0; w < " << warps << "; ++w) s += rt" << I << "[w * " << cu.width

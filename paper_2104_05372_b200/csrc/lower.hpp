@@ -49,11 +49,15 @@ struct BufDecl {
 };
 
 struct KArg {
-  enum K { Buf, I64 } k;
+  enum K { Buf, I64, TMap } k;
   int buf = -1;
   long long off = 0;   // Buf: element offset
   long long i = 0;     // I64 value
   int special = 0;     // 1: range lo, 2: range hi
+  // TMap: 2-D tensor map over buffer `buf` viewed as rows of `rowLen`
+  // elements starting at element `off`; box = boxRows x rowLen; swizzle bytes
+  long long rowLen = 0, rows = 0;
+  int boxRows = 0, swizzle = 0;
 };
 
 struct Step {

@@ -144,7 +144,8 @@ int Program::prepare() {
     BufDecl& d = plan.bufs[b];
     long long elems = d.elems;
     if (d.role == BufDecl::Partial) elems = (long long)grids[d.partialKernel] * d.partialWidth;
-    size_t bytes = (size_t)std::max(1LL, elems) * storageBytes(d.kind, f64);
+    // +16: TMA tile copies round their byte range up to 16 bytes
+    size_t bytes = (size_t)std::max(1LL, elems) * storageBytes(d.kind, f64) + 16;
     if (d.role == BufDecl::Input && boundInputs.count((int)b)) continue;  // bound later
     if (d.elems < 0) continue;                                              // dead
     if ((rc = dxrt::check(cuMemAlloc(&devptr[b], bytes), "cuMemAlloc"))) return rc;
@@ -168,6 +169,7 @@ int Program::prepare() {
     }
   }
   if (std::getenv("DEXLET_NO_GRAPH") || plan.world > 1) useGraph = false;
+  if ((rc = buildTensorMaps())) return rc;
   // finalize functions
   const char* fz[4] = {"dx_fin_f32", "dx_fin_f64", "dx_fin_count_f32", "dx_fin_count_f64"};
   for (int k = 0; k < 4; ++k)
@@ -175,6 +177,44 @@ int Program::prepare() {
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[0], mod, "dx_add_f32"), "add fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[1], mod, "dx_add_f64"), "add fn"))) return rc;
   prepared = true;
+  return DXC_OK;
+}
+
+// 2-D TMA descriptors for the streamed row tiles of tile kernels (rows of
+// `rowLen` elements, box = boxRows x rowLen, hardware swizzle).
+int Program::buildTensorMaps() {
+  if (!tmapsDirty) return DXC_OK;
+  tmaps.clear();
+  tmapOf.clear();
+  size_t n = 0;
+  for (auto& st : plan.steps)
+    for (auto& a : st.args) n += a.k == KArg::TMap;
+  tmaps.reserve(n);
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    const Step& st = plan.steps[i];
+    for (size_t j = 0; j < st.args.size(); ++j) {
+      const KArg& a = st.args[j];
+      if (a.k != KArg::TMap) continue;
+      size_t es = storageBytes(plan.bufs[a.buf].kind, plan.f64);
+      CUtensorMap m;
+      cuuint64_t dims[2] = {(cuuint64_t)a.rowLen, (cuuint64_t)a.rows};
+      cuuint64_t strides[1] = {(cuuint64_t)(a.rowLen * es)};
+      cuuint32_t box[2] = {(cuuint32_t)a.rowLen, (cuuint32_t)a.boxRows};
+      cuuint32_t estr[2] = {1, 1};
+      CUtensorMapSwizzle sw = a.swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                              : a.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_128B;
+      int rc = dxrt::check(cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                                  (void*)(devptr[a.buf] + a.off * es), dims, strides, box, estr,
+                                                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                           "cuTensorMapEncodeTiled");
+      if (rc) return rc;
+      tmapOf[{(int)i, (int)j}] = (int)tmaps.size();
+      tmaps.push_back(m);
+    }
+  }
+  tmapsDirty = false;
   return DXC_OK;
 }
 
@@ -207,6 +247,7 @@ int Program::run() {
   int rc;
   if (!prepared && (rc = prepare())) return rc;
   ctx->makeCurrent();
+  if (tmapsDirty && (rc = buildTensorMaps())) return rc;
   if (!useGraph) return issue();
   if (!graphExec) {
     // capture the whole plan once; replay it with a single launch per run
@@ -260,12 +301,21 @@ int Program::issue() {
           if (ka.k == KArg::Buf) {
             ptrs[a] = devptr[ka.buf] + ka.off * storageBytes(plan.bufs[ka.buf].kind, f64);
             argv[a] = &ptrs[a];
+          } else if (ka.k == KArg::TMap) {
+            argv[a] = &tmaps[tmapOf.at({(int)i, (int)a})];
           } else {
             ints[a] = ka.special == 1 ? ranges[i].first : ka.special == 2 ? ranges[i].second : ka.i;
             argv[a] = &ints[a];
           }
         }
+        int ev = -1;
+        if (timing) {
+          for (size_t e = 0; e < kernelEventStep.size(); ++e)
+            if (kernelEventStep[e] == (int)i) ev = (int)e;
+          if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].first, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
+        }
         if ((rc = launch(funcs[i], grids[i], s.threads, s.smem, argv.data()))) return rc;
+        if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].second, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
         ++launches;
         break;
       }
@@ -310,6 +360,10 @@ int Program::issue() {
 Program::~Program() {
   if (ctx) {
     ctx->makeCurrent();
+    for (auto& e : kernelEvents) {
+      cuEventDestroy(e.first);
+      cuEventDestroy(e.second);
+    }
     if (graphExec) cuGraphExecDestroy(graphExec);
     for (CUdeviceptr p : owned) cuMemFree(p);
   }
@@ -505,6 +559,7 @@ int dxl_program_bind_input_device(dxl_program* p, int input, int leaf, void* dev
   const InLeaf& l = p->plan.inputs[input][leaf];
   p->boundInputs.insert(l.buf);
   p->devptr[l.buf] = (CUdeviceptr)devptr;
+  p->tmapsDirty = true;
   if (p->graphExec) {  // kernel arguments are baked into the graph
     cuGraphExecDestroy(p->graphExec);
     p->graphExec = nullptr;
@@ -606,6 +661,45 @@ int dxl_program_output_device_ptr(dxl_program* p, int leaf, void** out) {
   *out = (void*)(p->devptr[o.buf] + o.off * storageBytes(o.kind, p->plan.f64));
   return DXC_OK;
 }
+
+int dxl_program_enable_kernel_timing(dxl_program* p, int on) {
+  if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+  p->ctx->makeCurrent();
+  if (p->graphExec) {
+    cuGraphExecDestroy(p->graphExec);
+    p->graphExec = nullptr;
+  }
+  p->timing = on != 0;
+  if (p->timing && p->kernelEvents.empty()) {
+    p->kernelNames.clear();
+    for (size_t i = 0; i < p->plan.steps.size(); ++i) {
+      if (p->plan.steps[i].k != Step::Kernel) continue;
+      CUevent a, b;
+      int rc = dxrt::check(cuEventCreate(&a, CU_EVENT_DEFAULT), "event");
+      if (!rc) rc = dxrt::check(cuEventCreate(&b, CU_EVENT_DEFAULT), "event");
+      if (rc) return rc;
+      p->kernelEvents.push_back({a, b});
+      p->kernelEventStep.push_back((int)i);
+      p->kernelNames += p->plan.steps[i].name + "\n";
+    }
+  }
+  return DXC_OK;
+}
+
+int dxl_program_kernel_times(dxl_program* p, float* ms, int cap, int* n) {
+  *n = (int)p->kernelEvents.size();
+  if (!p->timing) { setError("kernel timing not enabled"); return DXC_E_ARG; }
+  p->ctx->makeCurrent();
+  for (int i = 0; i < *n && i < cap; ++i) {
+    int rc = dxrt::check(cuEventSynchronize(p->kernelEvents[i].second), "event sync");
+    if (rc) return rc;
+    rc = dxrt::check(cuEventElapsedTime(&ms[i], p->kernelEvents[i].first, p->kernelEvents[i].second), "elapsed");
+    if (rc) return rc;
+  }
+  return DXC_OK;
+}
+
+const char* dxl_program_kernel_names(dxl_program* p) { return p->kernelNames.c_str(); }
 
 const char* dxl_program_source(dxl_program* p) { return p->plan.source.c_str(); }
 const char* dxl_program_plan(dxl_program* p) {

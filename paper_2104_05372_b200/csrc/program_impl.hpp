@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 
+#include <map>
 #include <set>
 #include <string>
 #include <utility>
@@ -38,8 +39,16 @@ struct Program {
   CUfunction finFn[4] = {};
   CUfunction addFn[2] = {};
   int launches = 0;
+  std::vector<CUtensorMap> tmaps;                  // TMA descriptors (kernel args)
+  std::map<std::pair<int, int>, int> tmapOf;        // (step, arg) -> tmaps index
+  bool tmapsDirty = true;
+  int buildTensorMaps();
   CUgraphExec graphExec = nullptr;
   bool useGraph = true;
+  bool timing = false;
+  std::vector<std::pair<CUevent, CUevent>> kernelEvents;  // per kernel step
+  std::vector<int> kernelEventStep;
+  std::string kernelNames;
 
   int prepare();
   int run();

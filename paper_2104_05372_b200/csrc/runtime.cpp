@@ -255,6 +255,7 @@ Ctx::~Ctx() {
   if (ctx) {
     cuCtxSetCurrent(ctx);
     for (auto& kv : modules) cuModuleUnload(kv.second);
+    if (scratch) cuMemFree(scratch);
     if (stream) cuStreamDestroy(stream);
     if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
     cuDevicePrimaryCtxRelease(dev);
@@ -413,6 +414,21 @@ int dxc_launch(dxc_ctx* ctx, dxc_module* mod, const char* kernel, unsigned grid,
   }
   return check(cuLaunchKernel(f, grid, 1, 1, block, 1, 1, smem, ctx->stream, args, nullptr),
                "cuLaunchKernel");
+}
+
+int dxc_l2_flush(dxc_ctx* ctx, size_t bytes) {
+  ctx->makeCurrent();
+  if (ctx->scratchBytes < bytes) {
+    if (ctx->scratch) cuMemFree(ctx->scratch);
+    ctx->scratch = 0;
+    ctx->scratchBytes = 0;
+    int rc = check(cuMemAlloc(&ctx->scratch, bytes), "cuMemAlloc scratch");
+    if (rc) return rc;
+    ctx->scratchBytes = bytes;
+  }
+  static unsigned char flip = 0;
+  flip ^= 0x5a;
+  return check(cuMemsetD8Async(ctx->scratch, flip, bytes, ctx->stream), "l2 flush");
 }
 
 int dxc_event_record(dxc_ctx* ctx, void** ev) {

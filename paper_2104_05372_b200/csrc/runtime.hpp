@@ -30,6 +30,8 @@ struct Ctx {
   int nranks = 1;
   int rank = 0;
   std::map<std::string, CUmodule> modules;
+  CUdeviceptr scratch = 0;
+  size_t scratchBytes = 0;
 
   static int create(int dev, Ctx** out);
   int makeCurrent();
