@@ -1,0 +1,129 @@
+"""GPU: known answers of the reference test suites, golden vectors, and
+full-size (BASELINE.json) parity through size-independent properties and the
+fp64 restatements (oracle/restate.py, pinned in tests/test_oracle.py).
+
+Tolerances: float outputs rtMaxRelDiff (eval.cpp:758-763) <= 1e-4 in f32,
+<= 1e-9 in f64 mode; integer/index outputs and histograms bit-exact."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_05372_b200 as dx
+from oracle import restate
+from paper_2104_05372_b200 import programs as P
+from tests.kat_cases import KATS
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("name,src,entry,expected,cite", KATS, ids=[k[0] for k in KATS])
+@pytest.mark.parametrize("f64", [False, True], ids=["f32", "f64"])
+def test_reference_kats_on_device(ctx, name, src, entry, expected, cite, f64):
+    got = dx.Program(src, entry, ctx=ctx, float64=f64)()
+    assert len(got) == len(expected), cite
+    for g, e in zip(got, expected):
+        np.testing.assert_allclose(g, e, rtol=0, atol=1e-12 if f64 else 1e-5, err_msg=cite)
+
+
+def _golden():
+    with open(os.path.join(HERE, "golden", "parity_golden.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_golden().keys()))
+def test_golden_vectors(ctx, name):
+    case = _golden()[name]
+    inputs = [[np.asarray(l, dtype=dt) for l, dt in zip(leaves, dts)]
+              for leaves, dts in zip(case["inputs"], case["input_dtypes"])]
+    for f64, tol in ((False, 1e-4), (True, 1e-9)):
+        got = dx.Program(case["source"], ctx=ctx, float64=f64)(*inputs)
+        for g, w, kind in zip(got, case["outputs"], case["output_kinds"]):
+            w = np.asarray(w, dtype=np.float64)
+            if kind == "float":
+                assert oracle.rel_diff(g, w) <= tol, (name, f64)
+            else:
+                np.testing.assert_array_equal(g.astype(np.int64), w.astype(np.int64))
+
+
+def test_kmeans_full_size(ctx):
+    """BASELINE configs[1]: n=1M, d=16, K=64, f32 vs the fp64 restatement."""
+    n, d, k = 1_000_000, 16, 64
+    pts, asg, cs = P.kmeans_inputs(n, d, k)
+    cost, dC = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx)(pts, asg, cs)
+    rc, rg = restate.kmeans_cost_grad(pts, asg, cs)
+    assert oracle.rel_diff(cost, np.array([rc])) <= 1e-4
+    assert oracle.rel_diff(dC, rg.ravel()) <= 1e-4
+
+
+def test_kmeans_full_size_f64_tight(ctx):
+    n, d, k = 1_000_000, 16, 64
+    pts, asg, cs = P.kmeans_inputs(n, d, k)
+    cost, dC = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx, float64=True)(pts, asg, cs)
+    rc, rg = restate.kmeans_cost_grad(pts, asg, cs)
+    assert oracle.rel_diff(cost, np.array([rc])) <= 1e-9
+    assert oracle.rel_diff(dC, rg.ravel()) <= 1e-9
+
+
+def test_histogram_full_size_bit_exact(ctx):
+    """BASELINE configs[3]: 2^28 int32 keys into 4096 bins, uniform and Zipf."""
+    n, k = 1 << 28, 4096
+    prog = dx.Program(P.histogram(n, k), ctx=ctx)
+    for zipf in (0.0, 1.1):
+        keys = P.histogram_inputs(n, k, seed=11, zipf=zipf)
+        (h,) = prog(keys)
+        np.testing.assert_array_equal(h, np.bincount(keys, minlength=k).astype(np.float64))
+        assert h.sum() == n  # checksum of counts
+
+
+def test_matmul_256_fwd_grad(ctx):
+    """BASELINE configs[0]: n=256 forward + gradient."""
+    x, y = P.matmul_inputs(256)
+    (z,) = dx.Program(P.matmul_fwd(256), ctx=ctx)(x, y)
+    assert oracle.rel_diff(z, restate.matmul_fwd(x, y).ravel()) <= 1e-4
+    loss, gx = dx.Program(P.matmul_grad(256), ctx=ctx)(x, y)
+    rl, rg = restate.matmul_grad(x, y)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-4
+    assert oracle.rel_diff(gx, rg.ravel()) <= 1e-4
+
+
+def test_mlp_small_width(ctx):
+    x, w1, w2 = P.mlp_inputs(256, 64, 64, 32)
+    loss, d1, d2 = dx.Program(P.mlp_grad(256, 64, 64, 32), ctx=ctx)(x, [w1, w2])
+    rl, r1, r2 = restate.mlp_grad(x, w1, w2)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-4
+    assert oracle.rel_diff(d1, r1.ravel()) <= 1e-4
+    assert oracle.rel_diff(d2, r2.ravel()) <= 1e-4
+
+
+def test_sharded_plan_single_rank_matches(ctx):
+    """(rank 0 of world 1) == unsharded; world>1 uses NCCL (not in this box)."""
+    n, d, k = 50_000, 16, 64
+    pts, asg, cs = P.kmeans_inputs(n, d, k)
+    a = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx)(pts, asg, cs)
+    b = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx, rank=0, world=1)(pts, asg, cs)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_device_resident_inputs_zero_copy(ctx):
+    """Inputs bound as device pointers (no H2D) give the same answer."""
+    import torch
+    n, d, k = 10_000, 16, 8
+    pts, asg, cs = P.kmeans_inputs(n, d, k)
+    prog = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx)
+    want = prog(pts, asg, cs)
+    tp = torch.from_numpy(pts).cuda()
+    ta = torch.from_numpy(asg).cuda()
+    tc = torch.from_numpy(cs).cuda()
+    torch.cuda.synchronize()
+    prog.bind_input_device(0, 0, tp.data_ptr())
+    prog.bind_input_device(1, 0, ta.data_ptr())
+    prog.bind_input_device(2, 0, tc.data_ptr())
+    prog.run()
+    got = [prog.get_output(0), prog.get_output(1)]
+    for x, y in zip(got, want):
+        assert oracle.rel_diff(x, y) <= 1e-6

@@ -1,0 +1,89 @@
+"""CPU: structure of the lowering plans (which kernel class / Accum strategy
+each benchmark program gets) and evidence in the compiled sm_100a code."""
+import ctypes
+import os
+import shutil
+import subprocess
+import tempfile
+
+import pytest
+
+import paper_2104_05372_b200 as dx
+from paper_2104_05372_b200 import programs as P
+
+
+def _kernels(plan):
+    return [l for l in plan.splitlines() if " kernel " in l]
+
+
+def _cubin(source):
+    lib = dx.lib()
+    lib.dxc_module_cubin.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_size_t,
+                                     ctypes.POINTER(ctypes.c_size_t)]
+    n = ctypes.c_size_t()
+    assert lib.dxc_module_cubin(source.encode(), None, 0, ctypes.byref(n)) == 0
+    buf = ctypes.create_string_buffer(n.value)
+    assert lib.dxc_module_cubin(source.encode(), buf, n.value, ctypes.byref(n)) == 0
+    return buf.raw
+
+
+def _sass(source):
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump unavailable")
+    with tempfile.NamedTemporaryFile(suffix=".cubin", delete=False) as f:
+        f.write(_cubin(source))
+        path = f.name
+    try:
+        return subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    finally:
+        os.unlink(path)
+
+
+def test_kmeans_value_and_grad_is_one_fused_kernel():
+    """Forward tape inlined into both consumers (no HBM tape), the cotangent
+    broadcast folded (accum-to-map), cost and gradient loops fused
+    horizontally: one kernel + two finalizes."""
+    prog = dx.Program(P.kmeans_cost_grad(100_000, 16, 64), ctx=None)
+    ks = _kernels(prog.plan)
+    assert len(ks) == 1, prog.plan
+    src = prog.source
+    assert "dx_tile_rows4<16, 64" in src          # tile-sorted row reduction for dC
+    assert "dx_block_sum(rp" in src               # register partial for the cost
+    assert "dx_tma_2d(" in src                    # TMA tensor tiles of the points
+    sass = _sass(src)
+    assert "UTMALDG.2D" in sass and "UBLKCP" in sass
+
+
+def test_histogram_uses_exact_shared_counters():
+    prog = dx.Program(P.histogram(1 << 20, 4096), ctx=None)
+    assert len(_kernels(prog.plan)) == 1
+    assert "dx_count_smem" in prog.source
+    assert "count" in prog.plan  # finalize of u32 counters scaled by the constant
+    sass = _sass(prog.source)
+    assert "ATOMS" in sass and "LDG.E.128" in sass
+
+
+def test_matmul_forward_flattens_perfect_nest():
+    prog = dx.Program(P.matmul_fwd(64), ctx=None)
+    ks = _kernels(prog.plan)
+    assert len(ks) == 1 and "n=4096" in ks[0], prog.plan
+
+
+def test_state_loop_runs_on_one_device_thread():
+    """`get`/`:=` on an outer cell blocks chunking (ParScan, eval.cpp:548-600):
+    the loop becomes a serial kernel, never a CPU loop."""
+    prog = dx.Program(P.cumulative(50), ctx=None)
+    ks = _kernels(prog.plan)
+    assert len(ks) == 1 and "serial" in ks[0]
+
+
+def test_dead_cells_are_not_allocated():
+    prog = dx.Program(P.kmeans_grad(10_000, 16, 8), ctx=None)
+    # the n-element cotangent broadcast cell of the transposed sum is never
+    # materialized: no zero-fill of 10000 elements remains
+    assert "(10000)" not in prog.plan
+
+
+def test_sharded_plan_allreduces_cells():
+    prog = dx.Program(P.kmeans_cost_grad(1000, 16, 8), ctx=None, rank=1, world=2)
+    assert prog.plan.count("allreduce") == 2
