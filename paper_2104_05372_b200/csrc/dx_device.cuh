@@ -437,6 +437,7 @@ __device__ __forceinline__ void dx_fin2(const P* part, int nblk, long long width
 
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_f32(const float* p, int n, long long w, float* c) { dx_fin2<float, float>(p, n, w, 1.0f, c, false); }
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_f64(const double* p, int n, long long w, double* c) { dx_fin2<double, double>(p, n, w, 1.0, c, false); }
+extern "C" __global__ void __launch_bounds__(1024) dx_fin_f32d(const float* p, int n, long long w, double* c) { dx_fin2<double, float>(p, n, w, 1.0, c, false); }
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_count_f32(const unsigned* p, int n, long long w, float s, float* c) { dx_fin2<float, unsigned>(p, n, w, s, c, true); }
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_count_f64(const unsigned* p, int n, long long w, double s, double* c) { dx_fin2<double, unsigned>(p, n, w, s, c, true); }
 
@@ -446,6 +447,13 @@ extern "C" __global__ void dx_add_f32(float* c, const float* s, long long n) {
 }
 extern "C" __global__ void dx_add_f64(double* c, const double* s, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) c[i] += s[i];
+}
+// Element-type conversion copies (f32 values into f64 cells and back).
+extern "C" __global__ void dx_cvt_f32_f64(double* d, const float* s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = s[i];
+}
+extern "C" __global__ void dx_cvt_f64_f32(float* d, const double* s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = (float)s[i];
 }
 // Bounds check of uploaded index leaves (fromOrdinal's check, index_set.cpp:99-106).
 extern "C" __global__ void dx_check_index(const int* x, long long n, int size, int* bad) {

@@ -137,6 +137,7 @@ static size_t storageBytesOf(SK k, bool f64 = false) {
   switch (k) {
     case SK::F: return f64 ? 8 : 4;
     case SK::I: return 8;
+    case SK::D: return 8;
     default: return 4;
   }
 }
@@ -487,6 +488,7 @@ class Lowering {
   std::string ctype(SK k) const {
     switch (k) {
       case SK::F: return "dx_f";
+      case SK::D: return "double";
       case SK::I: return "long long";
       case SK::X: return "int";
       case SK::U32: return "unsigned";
@@ -620,7 +622,7 @@ class Lowering {
     c.lv = leaves(payload);
     c.accum = accum;
     for (auto& l : c.lv) {
-      SK k = l.kind;
+      SK k = (l.kind == SK::F && !opt.f64) ? SK::D : l.kind;  // cells accumulate in f64
       int b = newBuf(BufDecl::Cell, k, l.count);
       c.bufs.push_back(b);
       c.host.emplace_back(l.count, 0.0);
@@ -655,8 +657,9 @@ class Lowering {
       u.k = Step::Upload;
       u.buf = c.bufs[l];
       u.elems = (long long)c.host[l].size();
-      int cb = newBuf(BufDecl::Const, c.lv[l].kind, u.elems);
-      if (c.lv[l].kind == SK::F) plan.bufs[cb].initF = c.host[l];
+      SK ck = plan.bufs[c.bufs[l]].kind;
+      int cb = newBuf(BufDecl::Const, ck, u.elems);
+      if (ck == SK::F || ck == SK::D) plan.bufs[cb].initF = c.host[l];
       else for (double v : c.host[l]) plan.bufs[cb].initI.push_back((long long)v);
       u.buf2 = cb;
       addStep(u);
@@ -1226,7 +1229,7 @@ class Lowering {
         std::vector<LeafInfo> lv = leaves(v->ty);
         for (size_t l = 0; l < lv.size(); ++l) {
           Step s;
-          s.k = Step::CopyBuf;
+          s.k = plan.bufs[bufs[base + l]].kind == plan.bufs[v->bufs[l]].kind ? Step::CopyBuf : Step::Convert;
           s.buf = bufs[base + l];
           s.off = offs[base + l];
           s.buf2 = v->bufs[l];
@@ -1243,7 +1246,7 @@ class Lowering {
         return;
       }
       case HVal::Const: {
-        int cb = newBuf(BufDecl::Const, v->ty->k == DType::Float ? SK::F : (v->ty->k == DType::Int ? SK::I : SK::X), 1);
+        int cb = newBuf(BufDecl::Const, plan.bufs[bufs[base]].kind, 1);
         if (v->ty->k == DType::Float) plan.bufs[cb].initF = {v->f};
         else plan.bufs[cb].initI = {v->i};
         Step u; u.k = Step::Upload; u.buf = cb; u.buf2 = cb; u.elems = 1; addStep(u);
@@ -1469,7 +1472,7 @@ class Lowering {
           s.global = true;
           s.ro = true;
           s.input = plan.bufs[h->bufs[l]].role == BufDecl::Input;
-          s.kind = lv[l].kind;
+          s.kind = plan.bufs[h->bufs[l]].kind;
           slots.push_back(s);
         }
         return viewSlots(g, h->ty, slots);
@@ -1486,7 +1489,7 @@ class Lowering {
           s.base = "";  // resolved per strategy at the access
           s.off = lit(h->offs[l]);
           s.global = true;
-          s.kind = c.lv[l].kind;
+          s.kind = plan.bufs[c.bufs[l]].kind;
           s.cellLeaf = (int)l;
           k->slots.push_back(s);
         }
@@ -1556,14 +1559,15 @@ class Lowering {
             t->a->k != DType::Table && t->a->k != DType::Pair) {
           const Slot& s0 = slots[base];
           long long cnt = leaves(t)[0].count;
-          int es = (s0.kind == SK::F && opt.f64) || s0.kind == SK::I ? 8 : 4;
+          int es = (int)storageBytesOf(s0.kind, opt.f64);
+          const bool fl = s0.kind == SK::F || s0.kind == SK::D;
           int vw = 16 / es;  // elements per 16-byte load
           if (cnt <= 32 && cnt % vw == 0 && s0.align % vw == 0) noteRead(g, s0, true);
           if (cnt <= 32 && cnt % vw == 0 && s0.align % vw == 0 && g.out) {
             std::string r = g.fresh("row");
             std::string B = std::to_string(s0.buf);
             // address of the q-th 16-byte block of the row
-            std::string addrq = "(const " + std::string(es == 8 ? (s0.kind == SK::F ? "double2" : "longlong2") : (s0.kind == SK::F ? "float4" : "int4")) + "*)(" + s0.base + " + " + s0.off + " + q * " + lit(vw) + ")";
+            std::string addrq = "(const " + std::string(es == 8 ? (fl ? "double2" : "longlong2") : (fl ? "float4" : "int4")) + "*)(" + s0.base + " + " + s0.off + " + q * " + lit(vw) + ")";
             if (s0.stream && g.staged.count(s0.buf) && g.tensorStaged.count(s0.buf))
               addrq = "(const float4*)((const char*)(sb" + B + " + dx_sh" + B + ") + dx_swz((unsigned)(threadIdx.x * " +
                       lit(s0.streamL * es) + " + (" + s0.rowOff + ") * " + lit(es) + " + q * 16), " +
@@ -1574,8 +1578,8 @@ class Lowering {
             else if (g.wholeStaged.count(s0.buf))
               addrq = "(const float4*)((const char*)wt" + B + " + dx_swz((unsigned)((" + s0.off + ") * " + lit(es) +
                       " + q * 16), 3))";
-            std::string ct = ctype(s0.kind);
-            std::string vt = es == 8 ? (s0.kind == SK::F ? "double2" : "longlong2") : (s0.kind == SK::F ? "float4" : "int4");
+            std::string ct = fl ? "dx_f" : ctype(s0.kind);
+            std::string vt = es == 8 ? (fl ? "double2" : "longlong2") : (fl ? "float4" : "int4");
             g.line(ct + " " + r + "[" + lit(cnt) + "];");
             g.line("#pragma unroll");
             g.line("for (int q = 0; q < " + lit(cnt / vw) + "; ++q) { const " + vt + " w = *(const " + vt + "*)(" +
@@ -1637,7 +1641,7 @@ class Lowering {
           g.streamBufs.insert(s.buf);
           if (g.pass == 1 && g.U > 1) ld = "pf" + std::to_string(s.buf) + "_" + s.off.substr(4);
         }
-        g.line(ctype(s.kind) + " " + v + " = " + ld + ";");
+        g.line((t->k == DType::Float ? std::string("dx_f") : ctype(s.kind)) + " " + v + " = " + ld + ";");
         if (t->k == DType::Idx && s.input) {
           g.usesErr = true;
           g.line(v + " = dx_chk_idx(" + v + ", " + lit(size(t->desc)) + ", dx_bad);");
@@ -2728,7 +2732,7 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
         s2.base = param(g, outBufs[l], true);
         s2.off = eAdd(lit(outOffs[l]), eMul(oo, el[l].count));
         s2.global = true;
-        s2.kind = el[l].kind;
+        s2.kind = plan.bufs[outBufs[l]].kind;
         slots.push_back(s2);
       }
       storeK(g, elem, slots);
@@ -2889,7 +2893,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     Cell& c = cells[cu.cell];
     cu.targetBuf = c.bufs[cu.leaf];
     if (g.sharded) {
-      cu.targetBuf = newBuf(BufDecl::Temp, c.lv[cu.leaf].kind, cu.width);
+      cu.targetBuf = newBuf(BufDecl::Temp, plan.bufs[c.bufs[cu.leaf]].kind, cu.width);
       Step z; z.k = Step::Zero; z.buf = cu.targetBuf; z.elems = cu.width; addStep(z);
     }
   }
@@ -3400,6 +3404,7 @@ std::string Plan::summary() const {
       case Step::Allreduce: o << "allreduce b" << s.buf << " (" << s.elems << ")"; break;
       case Step::AddBuf: o << "add b" << s.buf << " += b" << s.buf2; break;
       case Step::CopyBuf: o << "copy b" << s.buf << "+" << s.off << " <- b" << s.buf2 << "+" << s.off2 << " (" << s.elems << ")"; break;
+      case Step::Convert: o << "convert b" << s.buf << "+" << s.off << " <- b" << s.buf2 << "+" << s.off2 << " (" << s.elems << ")"; break;
     }
     o << "\n";
   }
@@ -3454,7 +3459,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
         std::vector<LeafInfo> lv = leaves(v->ty);
         for (size_t l = 0; l < lv.size(); ++l) {
           OutLeaf o;
-          o.kind = lv[l].kind;
+          o.kind = L.plan.bufs[v->bufs[l]].kind;
           o.count = lv[l].count;
           o.desc = lv[l].desc;
           o.buf = v->bufs[l];

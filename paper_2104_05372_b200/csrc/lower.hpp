@@ -18,7 +18,9 @@ namespace dexlet {
 namespace dev {
 
 // Storage kinds of plan buffers.
-enum class SK { F, I, X, U32 };  // Float (f32|f64), Int (i64), Index (i32), counters
+// Float (f32|f64 per mode), Int (i64), Index (i32), counters, and D: Float
+// Accum/State cells, always f64 in HBM (the reference accumulates in double).
+enum class SK { F, I, X, U32, D };
 
 // Resolved device type of a value (index-set sizes concrete).
 struct DType;
@@ -61,7 +63,7 @@ struct KArg {
 };
 
 struct Step {
-  enum K { Zero, Upload, Kernel, Finalize, Allreduce, AddBuf, CopyBuf } k;
+  enum K { Zero, Upload, Kernel, Finalize, Allreduce, AddBuf, CopyBuf, Convert } k;
   int buf = -1, buf2 = -1;
   long long off = 0, off2 = 0, elems = 0;
   // Kernel

@@ -47,6 +47,7 @@ static int errCodeToStatus(ErrCode c) {
 size_t storageBytes(SK k, bool f64) {
   switch (k) {
     case SK::F: return f64 ? 8 : 4;
+    case SK::D: return 8;
     case SK::I: return 8;
     case SK::X: return 4;
     case SK::U32: return 4;
@@ -176,6 +177,9 @@ int Program::prepare() {
     if ((rc = dxrt::check(cuModuleGetFunction(&finFn[k], mod, fz[k]), "finalize fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[0], mod, "dx_add_f32"), "add fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[1], mod, "dx_add_f64"), "add fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&finF32D, mod, "dx_fin_f32d"), "finalize fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[0], mod, "dx_cvt_f32_f64"), "cvt fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[1], mod, "dx_cvt_f64_f32"), "cvt fn"))) return rc;
   prepared = true;
   return DXC_OK;
 }
@@ -220,7 +224,8 @@ int Program::buildTensorMaps() {
 
 std::vector<char> Program::convertInit(const BufDecl& d) const {
   size_t es = storageBytes(d.kind, plan.f64);
-  long long n = d.kind == SK::F ? (long long)d.initF.size() : (long long)d.initI.size();
+  const bool fl = d.kind == SK::F || d.kind == SK::D;
+  long long n = fl ? (long long)d.initF.size() : (long long)d.initI.size();
   std::vector<char> out((size_t)std::max(1LL, n) * es, 0);
   for (long long i = 0; i < n; ++i) {
     char* p = out.data() + i * es;
@@ -229,6 +234,7 @@ std::vector<char> Program::convertInit(const BufDecl& d) const {
         if (plan.f64) { double v = d.initF[i]; std::memcpy(p, &v, 8); }
         else { float v = (float)d.initF[i]; std::memcpy(p, &v, 4); }
         break;
+      case SK::D: { double v = d.initF[i]; std::memcpy(p, &v, 8); break; }
       case SK::I: { long long v = d.initI[i]; std::memcpy(p, &v, 8); break; }
       case SK::X:
       case SK::U32: { int v = (int)d.initI[i]; std::memcpy(p, &v, 4); break; }
@@ -292,6 +298,20 @@ int Program::issue() {
           return rc;
         break;
       }
+      case Step::Convert: {
+        // f32 <-> f64 element conversion (values into f64 cells)
+        size_t ed = storageBytes(plan.bufs[s.buf].kind, f64), esrc = storageBytes(plan.bufs[s.buf2].kind, f64);
+        CUdeviceptr d = devptr[s.buf] + s.off * ed, src = devptr[s.buf2] + s.off2 * esrc;
+        long long n = s.elems;
+        void* args[3] = {&d, &src, &n};
+        if (ed == esrc) {
+          if ((rc = dxrt::check(cuMemcpyDtoDAsync(d, src, (size_t)n * ed, st), "copy"))) return rc;
+        } else if ((rc = launch(ed == 8 ? cvtFn[0] : cvtFn[1], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0,
+                                args))) {
+          return rc;
+        }
+        break;
+      }
       case Step::Kernel: {
         std::vector<CUdeviceptr> ptrs(s.args.size());
         std::vector<long long> ints(s.args.size());
@@ -324,14 +344,17 @@ int Program::issue() {
         int nblk = grids[s.kernelStep];
         long long w = s.elems;
         unsigned g = (unsigned)((w + 31) / 32);
+        const bool dcell = f64 || plan.bufs[s.buf].kind == SK::D;
         if (s.fin == Step::Count) {
           float sf = (float)s.scale;
           double sd = s.scale;
-          void* args[5] = {&part, &nblk, &w, f64 ? (void*)&sd : (void*)&sf, &cell};
-          if ((rc = launch(finFn[f64 ? 3 : 2], g, 1024, 0, args))) return rc;
+          void* args[5] = {&part, &nblk, &w, dcell ? (void*)&sd : (void*)&sf, &cell};
+          if ((rc = launch(finFn[dcell ? 3 : 2], g, 1024, 0, args))) return rc;
         } else {
           void* args[4] = {&part, &nblk, &w, &cell};
-          if ((rc = launch(finFn[f64 ? 1 : 0], g, 1024, 0, args))) return rc;
+          // partials are dx_f; cells f64 (SK::D) or dx_f
+          CUfunction fn = f64 ? finFn[1] : (plan.bufs[s.buf].kind == SK::D ? finF32D : finFn[0]);
+          if ((rc = launch(fn, g, 1024, 0, args))) return rc;
         }
         ++launches;
         break;
@@ -339,7 +362,7 @@ int Program::issue() {
       case Step::Allreduce: {
         size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
         SK k = plan.bufs[s.buf].kind;
-        int dt = k == SK::F ? (f64 ? DXC_F64 : DXC_F32) : k == SK::I ? DXC_I64 : DXC_I32;
+        int dt = k == SK::D ? DXC_F64 : k == SK::F ? (f64 ? DXC_F64 : DXC_F32) : k == SK::I ? DXC_I64 : DXC_I32;
         if ((rc = ctx->allreduceSum(devptr[s.buf] + s.off * es, (size_t)s.elems, dt))) return rc;
         break;
       }
@@ -347,7 +370,8 @@ int Program::issue() {
         CUdeviceptr c = devptr[s.buf], src = devptr[s.buf2];
         long long n = s.elems;
         void* args[3] = {&c, &src, &n};
-        if ((rc = launch(addFn[f64 ? 1 : 0], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args)))
+        const bool dk = f64 || plan.bufs[s.buf].kind == SK::D;
+        if ((rc = launch(addFn[dk ? 1 : 0], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args)))
           return rc;
         ++launches;
         break;
@@ -449,7 +473,9 @@ int dxl_program_input_num_leaves(dxl_program* p, int input, int* out) {
   return DXC_OK;
 }
 
-static int leafKind(SK k) { return k == SK::F ? DXC_LEAF_FLOAT : k == SK::I ? DXC_LEAF_INT : DXC_LEAF_INDEX; }
+static int leafKind(SK k) {
+  return (k == SK::F || k == SK::D) ? DXC_LEAF_FLOAT : k == SK::I ? DXC_LEAF_INT : DXC_LEAF_INDEX;
+}
 
 int dxl_program_input_leaf(dxl_program* p, int input, int leaf, int* kind, int64_t* count) {
   if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
@@ -498,6 +524,7 @@ static std::vector<char> convertIn(const void* host, int dtype, SK kind, bool f6
         if (f64) std::memcpy(p, &dv, 8);
         else { float f = (float)dv; std::memcpy(p, &f, 4); }
         break;
+      case SK::D: std::memcpy(p, &dv, 8); break;
       case SK::I: std::memcpy(p, &iv, 8); break;
       case SK::X: {
         if (iv < 0 || iv >= idxSize) {
@@ -592,8 +619,8 @@ int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype) {
   size_t es = storageBytes(o.kind, f64);
   if (o.host) {
     raw.resize(es);
-    if (o.kind == SK::F) {
-      if (f64) std::memcpy(raw.data(), &o.hostF[0], 8);
+    if (o.kind == SK::F || o.kind == SK::D) {
+      if (es == 8) std::memcpy(raw.data(), &o.hostF[0], 8);
       else { float f = (float)o.hostF[0]; std::memcpy(raw.data(), &f, 4); }
     } else if (o.kind == SK::I) {
       std::memcpy(raw.data(), &o.hostI[0], 8);
@@ -604,7 +631,7 @@ int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype) {
   } else {
     if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
     p->ctx->makeCurrent();
-    bool direct = (o.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) ||
+    bool direct = (o.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) || (o.kind == SK::D && dtype == DXC_F64) ||
                   (o.kind == SK::X && dtype == DXC_I32) || (o.kind == SK::I && dtype == DXC_I64);
     int rc;
     int flag = 0;
@@ -633,7 +660,8 @@ int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype) {
     const char* s = raw.data() + i * es;
     switch (o.kind) {
       case SK::F:
-        if (f64) std::memcpy(&dv, s, 8);
+      case SK::D:
+        if (es == 8) std::memcpy(&dv, s, 8);
         else { float f; std::memcpy(&f, s, 4); dv = f; }
         iv = (long long)dv;
         break;
@@ -710,7 +738,7 @@ const char* dxl_program_plan(dxl_program* p) {
 int dxl_program_num_launches(dxl_program* p, int* out) {
   int n = 0;
   for (auto& s : p->plan.steps)
-    if (s.k == Step::Kernel || s.k == Step::Finalize || s.k == Step::AddBuf) ++n;
+    if (s.k == Step::Kernel || s.k == Step::Finalize || s.k == Step::AddBuf || s.k == Step::Convert) ++n;
   *out = n;
   return DXC_OK;
 }

@@ -38,6 +38,8 @@ struct Program {
   std::vector<std::vector<char>> staging;
   CUfunction finFn[4] = {};
   CUfunction addFn[2] = {};
+  CUfunction finF32D = nullptr;
+  CUfunction cvtFn[2] = {};
   int launches = 0;
   std::vector<CUtensorMap> tmaps;                  // TMA descriptors (kernel args)
   std::map<std::pair<int, int>, int> tmapOf;        // (step, arg) -> tmaps index
