@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--ref-sample", type=int, default=10_000,
                     help="points per reference step (bounded CPU sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="for ncu runs: skip clock sampling, e2e and the CPU baseline")
     return ap.parse_args()
 
 
@@ -234,13 +236,13 @@ def main():
     # The clock sampler (100 ms period) starts before the warm-up; the same
     # workload keeps running untimed until it has under-load samples, then
     # the K timed steps follow, then a short untimed tail.
-    clocks = Clocks(local)
+    clocks = Clocks(local) if not args.profile else None
     for _ in range(args.warmup):
         ctx.l2_flush()
         prog.run()
-    t_end = time.time() + 5.0
+    t_end = time.time() + (5.0 if clocks else 0.0)
     t_min = time.time() + 0.6
-    while time.time() < t_end and (clocks.lines() < 3 or time.time() < t_min):
+    while clocks and time.time() < t_end and (clocks.lines() < 3 or time.time() < t_min):
         for _ in range(20):
             ctx.l2_flush()
             prog.run()
@@ -258,13 +260,13 @@ def main():
         for name, ms in prog.kernel_times():
             kern.setdefault(name, []).append(ms)
     barrier()
-    t_tail = time.time() + 0.3
+    t_tail = time.time() + (0.3 if clocks else 0.0)
     while time.time() < t_tail:
         for _ in range(20):
             ctx.l2_flush()
             prog.run()
         ctx.sync()
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (--profile)"]}
     ms_local = statistics.mean(step_ms)
     # dominant kernel
     dom = max(kern.items(), key=lambda kv: statistics.mean(kv[1]))
@@ -285,7 +287,7 @@ def main():
     h2d = sum(b for _, b in hp.values())
     d2h = 4 + K * D * 4
     e2e_ms = []
-    for i in range(args.warmup + args.steps):
+    for i in range(0 if args.profile else args.warmup + args.steps):
         ctx.l2_flush()
         e0 = ctx.event()
         prog.set_input_ptr(0, 0, hp["pts"][0], dx.DXC_F32)
@@ -300,7 +302,7 @@ def main():
         ctx.destroy_event(e1)
         if i >= args.warmup:
             e2e_ms.append(ms)
-    e2e_local = statistics.mean(e2e_ms)
+    e2e_local = statistics.mean(e2e_ms) if e2e_ms else float("nan")
 
     # ---- max over ranks --------------------------------------------------------
     ms_step, e2e_step, dom_ms_max = ms_local, e2e_local, dom_ms
@@ -335,7 +337,7 @@ def main():
             "gpu_launches": launches_per_run * args.steps,
             "clocks": clk,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.profile:
             try:
                 cores = os.cpu_count() or 1
                 rate, sec, _ = reference_rate(10_000, cores, 3)

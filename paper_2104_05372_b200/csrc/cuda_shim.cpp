@@ -55,6 +55,7 @@ SHIM(cuMemFree, (CUdeviceptr p), (p))
 SHIM(cuMemHostAlloc, (void** p, size_t n, unsigned int f), (p, n, f))
 SHIM(cuMemFreeHost, (void* p), (p))
 SHIM(cuMemcpyHtoD, (CUdeviceptr d, const void* s, size_t n), (d, s, n))
+SHIM(cuMemcpyDtoH, (void* d, CUdeviceptr s, size_t n), (d, s, n))
 SHIM(cuMemcpyHtoDAsync, (CUdeviceptr d, const void* s, size_t n, CUstream st), (d, s, n, st))
 SHIM(cuMemcpyDtoHAsync, (void* d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
 SHIM(cuMemcpyDtoDAsync, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))

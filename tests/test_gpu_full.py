@@ -127,3 +127,15 @@ def test_device_resident_inputs_zero_copy(ctx):
     got = [prog.get_output(0), prog.get_output(1)]
     for x, y in zip(got, want):
         assert oracle.rel_diff(x, y) <= 1e-6
+
+
+def test_cpp_evalExprDevice_selftest():
+    """C++ drop-in API (include/dexlet_device.hpp): reference-parsed programs,
+    env-bound RtVal inputs, evalExprDevice instead of evalExpr."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(HERE), "paper_2104_05372_b200", "bin", "dexlet_device_selftest")
+    if not os.path.exists(exe):
+        pytest.fail("selftest binary missing: run __graft_entry__.build()")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("PASS") == 10, out.stdout
