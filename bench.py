@@ -42,6 +42,46 @@ METRIC = "kmeans fwd+grad evals/s (1M points/GPU, d=16, K=64)"
 UNIT = "evals/s"
 
 
+def config_spec(name, world):
+    """Workloads of BASELINE.json configs.  The default (driver) run is
+    kmeans = configs[1]; the others are for DESIGN.md measurements."""
+    from paper_2104_05372_b200 import programs as P
+    if name == "kmeans":
+        n = N_PER_GPU * world
+        pts, asg, cs = kmeans_inputs_fast(n, D, K)
+        return dict(metric=METRIC, src=P.kmeans_cost_grad(n, D, K), inputs=[[pts], [asg], [cs]],
+                    bound="hbm", work=N_PER_GPU * D * 4 + N_PER_GPU * 4 + 2 * K * D * 4,
+                    work_basis="n*d*4 (points) + n*4 (assignments) + 2*K*d*4 (centroids in, dC out)",
+                    workload="kmeans cost+grad, n=1M points per GPU, d=16, K=64, fixed assignments "
+                             "(BASELINE configs[1]); value_and_grad via linearize+transpose",
+                    extra={"n_total": n, "d": D, "k": K}, out_bytes=4 + K * D * 4)
+    if name == "histogram":
+        n, k = (1 << 28) * world, 4096
+        keys = P.histogram_inputs(n, k)
+        return dict(metric="histogram evals/s (2^28 int32 keys/GPU into 4096 bins)", src=P.histogram(n, k),
+                    inputs=[[keys]], bound="hbm", work=(1 << 28) * 4 + k * 4,
+                    work_basis="n*4 (keys) + k*4 (bins)", workload="index-set histogram h!(p.i) += 1.0, "
+                    "2^28 uniform keys per GPU, 4096 bins, bit-exact (BASELINE configs[3])",
+                    extra={"n_total": n, "bins": k}, out_bytes=k * 8)
+    if name == "matmul":
+        n = 256
+        x, y = P.matmul_inputs(n)
+        return dict(metric="matmul n=256 fwd+grad evals/s", src=P.matmul_grad(n), inputs=[[x], [y]],
+                    bound="tensor", work=4 * n ** 3, work_basis="2n^3 (forward) + 2n^3 (dX) flops",
+                    workload="pointful matmul sum(x.y) value and gradient wrt x, n=256 (BASELINE configs[0])",
+                    extra={"n": n}, out_bytes=4 + n * n * 4)
+    if name == "mlp":
+        b, i, h, o = 8192 * world, 1024, 1024, 1024
+        x, w1, w2 = P.mlp_inputs(b, i, h, o)
+        return dict(metric="MLP fwd+grad evals/s (batch 8192/GPU, 1024^3, square activation)",
+                    src=P.mlp_grad(b, i, h, o), inputs=[[x], [w1, w2]], bound="tensor",
+                    work=2 * (2 * 8192 * 1024 * 1024) * 2 + 3 * 8192 * 1024 * 1024 * 2,
+                    work_basis="fwd 2 GEMMs + bwd dW2, dH, dW1 (2*B*1024^2 flops each)",
+                    workload="2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) "
+                             "(BASELINE configs[4])", extra={"batch_total": b}, out_bytes=4 + 2 * 1024 * 1024 * 4)
+    raise SystemExit(f"unknown config {name}")
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -51,6 +91,7 @@ def parse():
     ap.add_argument("--ref-sample", type=int, default=10_000,
                     help="points per reference step (bounded CPU sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="kmeans", choices=["kmeans", "histogram", "matmul", "mlp"])
     ap.add_argument("--profile", action="store_true",
                     help="for ncu runs: skip clock sampling, e2e and the CPU baseline")
     return ap.parse_args()
@@ -132,13 +173,17 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def peaks():
+def peaks(bound="hbm"):
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        if bound == "hbm":
+            return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(j["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    if bound == "hbm":
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+    return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s bf16)"
 
 
 def traffic_per_launch():
@@ -215,13 +260,11 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         ctx.init_comm(obj[0], world, rank)
 
-    n = N_PER_GPU * world
-    pts, asg, cs = kmeans_inputs_fast(n, D, K)
-    src = P.kmeans_cost_grad(n, D, K)
-    prog = dx.Program(src, ctx=ctx, rank=rank, world=world)
-    prog.set_input(0, 0, pts)
-    prog.set_input(1, 0, asg)
-    prog.set_input(2, 0, cs)
+    spec = config_spec(args.config, world)
+    prog = dx.Program(spec["src"], ctx=ctx, rank=rank, world=world)
+    for i, leaves in enumerate(spec["inputs"]):
+        for l, arr in enumerate(leaves):
+            prog.set_input(i, l, arr)
     prog.enable_kernel_timing(True)
     launches_per_run = prog.num_launches()
 
@@ -274,28 +317,33 @@ def main():
 
     # ---- end to end through the C-ABI with host buffers ----------------------
     import ctypes
-    hp = {}
-    for name, arr in (("pts", pts), ("asg", asg), ("cs", cs)):
+    host = []  # pinned copies of every input leaf
+    for i, leaves in enumerate(spec["inputs"]):
+        for l, arr in enumerate(leaves):
+            arr = np.ascontiguousarray(arr)
+            p = ctypes.c_void_p()
+            dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
+            ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
+            dt = {np.dtype(np.float32): dx.DXC_F32, np.dtype(np.int32): dx.DXC_I32}[arr.dtype]
+            host.append((i, l, p.value, arr.nbytes, dt))
+    outs = []
+    for leaf, (kind, count) in enumerate(prog.output_leaves()):
         p = ctypes.c_void_p()
-        dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
-        ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
-        hp[name] = (p.value, arr.nbytes)
-    out_cost = ctypes.c_void_p()
-    out_grad = ctypes.c_void_p()
-    dx.lib().dxc_host_alloc(8, ctypes.byref(out_cost))
-    dx.lib().dxc_host_alloc(K * D * 4, ctypes.byref(out_grad))
-    h2d = sum(b for _, b in hp.values())
-    d2h = 4 + K * D * 4
+        nb = count * (4 if kind != dx.LEAF_INT else 8)
+        dx.lib().dxc_host_alloc(nb, ctypes.byref(p))
+        outs.append((leaf, p.value, dx.DXC_F32 if kind == dx.LEAF_FLOAT else
+                     (dx.DXC_I32 if kind == dx.LEAF_INDEX else dx.DXC_I64), nb))
+    h2d = sum(h[3] for h in host)
+    d2h = sum(o[3] for o in outs)
     e2e_ms = []
     for i in range(0 if args.profile else args.warmup + args.steps):
         ctx.l2_flush()
         e0 = ctx.event()
-        prog.set_input_ptr(0, 0, hp["pts"][0], dx.DXC_F32)
-        prog.set_input_ptr(1, 0, hp["asg"][0], dx.DXC_I32)
-        prog.set_input_ptr(2, 0, hp["cs"][0], dx.DXC_F32)
+        for (inp, l, ptr, nb, dt) in host:
+            prog.set_input_ptr(inp, l, ptr, dt)
         prog.run()
-        prog.get_output_ptr(0, out_cost.value, dx.DXC_F32)
-        prog.get_output_ptr(1, out_grad.value, dx.DXC_F32)
+        for (leaf, ptr, dt, nb) in outs:
+            prog.get_output_ptr(leaf, ptr, dt)
         e1 = ctx.event()
         ms = ctx.elapsed_ms(e0, e1)
         ctx.destroy_event(e0)
@@ -313,31 +361,30 @@ def main():
         ms_step, e2e_step, dom_ms_max = [float(x) for x in t.tolist()]
 
     if rank == 0:
-        peak, peak_kind = peaks()
-        n_local = N_PER_GPU
-        alg_bytes = n_local * D * 4 + n_local * 4 + 2 * K * D * 4
-        achieved = alg_bytes / (dom_ms_max * 1e-3) / 1e9
-        tr = traffic_per_launch()
+        peak, peak_kind = peaks(spec["bound"])
+        work = spec["work"]
+        achieved = work / (dom_ms_max * 1e-3) / (1e9 if spec["bound"] == "hbm" else 1e12)
+        tr = traffic_per_launch() if args.config == "kmeans" else None
         line = {
-            "metric": METRIC, "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
+            "metric": spec["metric"], "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded N(0,1) points, centroids sampled from points, nearest-centroid assignments)",
-            "config": {"workload": "kmeans cost+grad, n=1M points per GPU, d=16, K=64, fixed assignments "
-                                   "(BASELINE configs[1]); value_and_grad via linearize+transpose",
-                       "n_total": n, "d": D, "k": K, "parallelism": f"points sharded x{world} + NCCL allreduce",
-                       "l2": "flushed before every timed step (256 MB scratch write, outside the events)"},
-            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": tr, "kernel_ms": dom_ms_max,
-                         "algorithmic_bytes": alg_bytes,
-                         "bytes_basis": "n*d*4 (points) + n*4 (assignments) + 2*K*d*4 (centroids in, dC out)"},
+            "data": "synthetic (seeded; see paper_2104_05372_b200/programs.py)",
+            "config": dict({"workload": spec["workload"],
+                            "parallelism": f"outer loop sharded x{world} + NCCL allreduce of Accum cells",
+                            "l2": "flushed before every timed step (256 MB scratch write, outside the events)"},
+                           **spec["extra"]),
+            "roofline": {"bound": spec["bound"], "kernel": dom[0], "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s" if spec["bound"] == "hbm" else "TFLOP/s",
+                         "frac": achieved / peak, "traffic": tr, "kernel_ms": dom_ms_max,
+                         "algorithmic_work": work, "work_basis": spec["work_basis"],
+                         "all_kernels_ms": {k: statistics.mean(v) for k, v in kern.items()}},
             "e2e": {"value": world * 1000.0 / e2e_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
             "gpu_launches": launches_per_run * args.steps,
             "clocks": clk,
         }
-        if world == 1 and not args.no_cpu_baseline and not args.profile:
+        if world == 1 and not args.no_cpu_baseline and not args.profile and args.config == "kmeans":
             try:
                 cores = os.cpu_count() or 1
                 rate, sec, _ = reference_rate(10_000, cores, 3)
