@@ -49,6 +49,7 @@ SHIM(cuLaunchKernel,
      (CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz,
       unsigned smem, CUstream s, void** params, void** extra),
      (f, gx, gy, gz, bx, by, bz, smem, s, params, extra))
+SHIM(cuLaunchKernelEx, (const CUlaunchConfig* c, CUfunction f, void** params, void** extra), (c, f, params, extra))
 SHIM(cuOccupancyMaxActiveBlocksPerMultiprocessor, (int* n, CUfunction f, int b, size_t smem), (n, f, b, smem))
 SHIM(cuMemAlloc, (CUdeviceptr* p, size_t n), (p, n))
 SHIM(cuMemFree, (CUdeviceptr p), (p))
@@ -59,6 +60,7 @@ SHIM(cuMemcpyDtoH, (void* d, CUdeviceptr s, size_t n), (d, s, n))
 SHIM(cuMemcpyHtoDAsync, (CUdeviceptr d, const void* s, size_t n, CUstream st), (d, s, n, st))
 SHIM(cuMemcpyDtoHAsync, (void* d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
 SHIM(cuMemcpyDtoDAsync, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+SHIM(cuMemsetD8, (CUdeviceptr d, unsigned char v, size_t n), (d, v, n))
 SHIM(cuMemsetD8Async, (CUdeviceptr d, unsigned char v, size_t n, CUstream st), (d, v, n, st))
 SHIM(cuEventCreate, (CUevent* e, unsigned int f), (e, f))
 SHIM(cuEventRecord, (CUevent e, CUstream s), (e, s))

@@ -368,16 +368,19 @@ __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* 
     if (lane == 31) start[K] = inc;
   }
   __syncthreads();
-  if (key >= 0) perm[start[key] + wcnt[warp * K + key] + rank] = tid;
+  // perm holds the swizzled byte offset of each row's block 0, so block jb is
+  // one XOR away: (t*D*4 + 16*s(t)) ^ 16*jb  (see dx_tile_store4)
+  if (key >= 0) perm[start[key] + wcnt[warp * K + key] + rank] = tid * (D * 4) + (((tid >> 1) & (NB - 1)) << 4);
   __syncthreads();
   if (tid < P * NS) {
     const int p = tid % P, sp = tid / P;
-    const int k = p / NB, jb = p % NB;
+    const int k = p / NB, jb16 = (p % NB) << 4;
     const int q1 = start[k + 1];
+    const char* base = reinterpret_cast<const char*>(etile);
     float4 a = acc;
+#pragma unroll 4
     for (int q = start[k] + sp; q < q1; q += NS) {
-      const int r = perm[q];
-      const float4 w = reinterpret_cast<const float4*>(etile + r * D)[jb ^ ((r >> 1) & (NB - 1))];
+      const float4 w = *reinterpret_cast<const float4*>(base + (perm[q] ^ jb16));
       a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
     }
     acc = a;
@@ -433,6 +436,58 @@ __device__ __forceinline__ void dx_fin2(const P* part, int nblk, long long width
     __syncthreads();
   }
   if (ty == 0 && c < width) cell[c] += counts ? red[0][tx] * scale : red[0][tx];
+}
+
+// ---- in-kernel finalize (cooperative launch: every block is resident) ----
+// Grid barrier on a persistent counter: each launch adds gridDim.x, so the
+// target of this launch is the next multiple of gridDim.x.
+__device__ __forceinline__ void dx_grid_barrier(unsigned* counter) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    const unsigned target = (prev / gridDim.x + 1u) * gridDim.x;
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+// Cooperative fold of per-block partials [nblk][width] into `cell`: block b
+// owns columns [8b, 8b+8); thread (c, g) sums rows g, g+R, ... in order, then a
+// fixed tree over the R row groups.  Deterministic for a fixed grid.
+template <class T, class P>
+__device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T scale, T* cell, bool counts) {
+  constexpr int C = 8;
+  const int R = (blockDim.x / C) < 32 ? (blockDim.x / C) : 32;
+  __shared__ T red[32][C];
+  const int tx = threadIdx.x % C, ty = threadIdx.x / C;
+  const int nblk = gridDim.x;
+  for (long long c0 = (long long)blockIdx.x * C; c0 < width; c0 += (long long)gridDim.x * C) {  // block-uniform
+    const long long c = c0 + tx;
+    T s = T(0);
+    if (c < width && ty < R) {
+      if (counts) {
+        unsigned long long u = 0;
+        for (int b = ty; b < nblk; b += R) u += (unsigned long long)part[(long long)b * width + c];
+        s = (T)u;
+      } else {
+        for (int b = ty; b < nblk; b += R) s += (T)part[(long long)b * width + c];
+      }
+    }
+    if (ty < R) red[ty][tx] = s;
+    __syncthreads();
+    for (int h = 16; h > 0; h >>= 1) {
+      if (ty < h && ty + h < R) red[ty][tx] += red[ty + h][tx];
+      __syncthreads();
+    }
+    if (ty == 0 && c < width) cell[c] += counts ? red[0][tx] * scale : red[0][tx];
+    __syncthreads();
+  }
 }
 
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_f32(const float* p, int n, long long w, float* c) { dx_fin2<float, float>(p, n, w, 1.0f, c, false); }

@@ -444,6 +444,7 @@ struct KGen {
   int rowSiteCounter = 0;
   int accumSiteCounter = 0;
   int U = 1;                      // ordinals per thread
+  std::map<std::string, int> freshCell;  // local scalar Accum cells still zero -> loop depth
   int threads = 256;              // block size chosen for this kernel
   std::set<int> streamBufs;       // ro buffers read at exactly the ordinal
   std::set<int> stateCells;       // host-level State cells read/written (serial kernels)
@@ -2009,6 +2010,20 @@ class Lowering {
         case BinOp::Less: break;
       }
     }
+    // Identities that only change the sign of a zero result (the reference's
+    // `0.0 + x` / `0.0 - x` from zeroed Accum cells and transposed negations):
+    // x+0 -> x, 0+x -> x, x-0 -> x, 0-x -> -x, x*1 -> x, 1*x -> x.
+    if (l->ty->k == DType::Float && r->ty->k == DType::Float) {
+      if (op == BinOp::Add && l->isConst && l->cf == 0.0) return r;
+      if ((op == BinOp::Add || op == BinOp::Sub) && r->isConst && r->cf == 0.0) return l;
+      if (op == BinOp::Mul && l->isConst && l->cf == 1.0) return r;
+      if ((op == BinOp::Mul || op == BinOp::Div) && r->isConst && r->cf == 1.0) return l;
+      if (op == BinOp::Sub && l->isConst && l->cf == 0.0) {
+        std::string v = g.fresh("f");
+        g.line("const dx_f " + v + " = -(" + r->e + ");");
+        return kScalar(tFloat(), v, lev);
+      }
+    }
     std::string v = g.fresh("f");
     const char* o = "+";
     switch (op) {
@@ -2276,11 +2291,15 @@ class Lowering {
     if (!ra) fail(ErrCode::Internal, "runAccum reached the lowering unannotated", e->span);
     DTy payload = resolveType(ra->payload, kernelLook(g, s));
     std::vector<Slot> slots = localArrays(g, payload, true);
+    std::vector<LeafInfo> plv = leaves(payload);
+    for (size_t l = 0; l < slots.size(); ++l)
+      if (plv[l].count == 1) g.freshCell[slots[l].base] = (int)g.loopStack.size();
     auto ref = std::make_shared<KVal>();
     ref->k = KVal::Ref;
     ref->ty = tRef(payload);
     ref->slots = slots;
     KV res = kexpr(g, kbind(s, r.action.ref, ref), r.action.body, nullptr);
+    for (auto& sl : slots) g.freshCell.erase(sl.base);
     return kPair(res, viewSlots(g, payload, slots));
   }
 
@@ -2332,7 +2351,14 @@ class Lowering {
                    const KV& val, Span sp) {
     const Slot& sl = ref->slots[leaf];
     if (ref->cell < 0) {  // thread-local cell
-      g.line(sl.base + "[" + sl.off + "] += " + valE + ";");
+      auto fr = g.freshCell.find(sl.base);
+      if (fr != g.freshCell.end() && fr->second == (int)g.loopStack.size() && sl.off == "0") {
+        // first write into a zeroed cell, executed at most once: a store
+        g.line(sl.base + "[0] = " + valE + ";");
+      } else {
+        g.line(sl.base + "[" + sl.off + "] += " + valE + ";");
+      }
+      if (fr != g.freshCell.end()) g.freshCell.erase(fr);
       return;
     }
     int site = g.accumSiteCounter++;
@@ -2386,7 +2412,9 @@ class Lowering {
         int rid = g.rowSiteCounter++;
         const KV& last = ref->path.back();
         std::string rv = "rowv" + std::to_string(rid), rk = "rowk" + std::to_string(rid);
-        g.line(rv + "[" + last->e + "] += " + valE + ";");
+        // one row site per cell, directly in the loop over the row's columns:
+        // every column is written exactly once per iteration
+        g.line(rv + "[" + last->e + "] " + (cu.rowSitesN == 1 ? "=" : "+=") + " " + valE + ";");
         g.line(rk + " = (int)((" + ref->prefixOff + ") / " + lit(cu.rowD) + "LL);");
         if ((int)g.rowSites.size() <= rid)
           g.rowSites.push_back({(int)(&cu - &g.cells[0]), cu.rowD, rid});
@@ -2921,6 +2949,17 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
   }
 
+  // In-kernel finalize: a cooperative launch (all blocks resident) lets the
+  // blocks meet at a grid barrier and fold the partials themselves.
+  bool coop = false;
+  for (auto& cu : g.cells) coop |= cu.partialBuf >= 0;
+  if (serial || std::getenv("DEXLET_NO_COOP")) coop = false;
+  int syncBuf = -1;
+  if (coop) {
+    syncBuf = newBuf(BufDecl::Sync, SK::U32, 1);
+    param(g, syncBuf, true);
+  }
+
   // Assemble source.
   std::ostringstream src;
   int warps = std::max(1, g.threads / 32);
@@ -3232,6 +3271,18 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         default: break;
       }
     }
+    if (coop) {
+      src << "  dx_grid_barrier(p" << syncBuf << ");\n";
+      for (size_t i = 0; i < g.cells.size(); ++i) {
+        CellUse& cu = g.cells[i];
+        if (cu.partialBuf < 0) continue;
+        std::string ct = ctype(plan.bufs[cu.targetBuf].kind);
+        bool counts = cu.strat == CellUse::Count;
+        src << "  dx_coop_fold<" << ct << ", " << (counts ? "unsigned" : "dx_f") << ">(part" << i << ", "
+            << cu.width << "LL, (" << ct << ")" << litF(counts ? cu.constVal : 1.0, true) << ", " << cu.pname
+            << ", " << (counts ? "true" : "false") << ");\n";
+      }
+    }
     src << "}\n\n";
   }
   plan.source += src.str();
@@ -3256,6 +3307,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   ks.threads = serial ? 32 : g.threads;
   ks.smem = smem;
   ks.minGrid = U;
+  ks.coop = coop;
   ks.note = note;
   addStep(ks);
   int kstep = (int)plan.steps.size() - 1;
@@ -3265,7 +3317,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   // Finalize privatized partials into the cell (fixed block order).
   for (size_t i = 0; i < g.cells.size(); ++i) {
     CellUse& cu = g.cells[i];
-    if (cu.partialBuf < 0) continue;
+    if (cu.partialBuf < 0 || coop) continue;
     Step f;
     f.k = Step::Finalize;
     f.buf = cu.targetBuf;
@@ -3395,7 +3447,8 @@ std::string Plan::summary() const {
       case Step::Zero: o << "zero b" << s.buf << " (" << s.elems << ")"; break;
       case Step::Upload: o << "upload b" << s.buf << " <- const b" << s.buf2 << " (" << s.elems << ")"; break;
       case Step::Kernel:
-        o << "kernel " << s.name << (s.serial ? " serial" : "") << " n=" << s.total << " smem=" << s.smem << "  // " << s.note;
+        o << "kernel " << s.name << (s.serial ? " serial" : "") << (s.coop ? " coop" : "") << " n=" << s.total
+          << " smem=" << s.smem << "  // " << s.note;
         break;
       case Step::Finalize:
         o << "finalize b" << s.buf << " <- partials b" << s.buf2 << " w=" << s.elems

@@ -40,7 +40,7 @@ void leavesOf(const DTy& t, std::vector<LeafInfo>& out, long long mult = 1);
 std::string showType(const DTy& t);
 
 struct BufDecl {
-  enum Role { Input, Cell, Output, Partial, Const, Temp, Flag } role;
+  enum Role { Input, Cell, Output, Partial, Const, Temp, Flag, Sync } role;  // Sync: zeroed once, persistent
   SK kind;
   long long elems;
   int input = -1, leaf = -1;
@@ -74,7 +74,8 @@ struct Step {
   bool sharded = false;
   int threads = 256;
   int smem = 0;           // dynamic shared memory bytes
-  int minGrid = 0;        // informational
+  int minGrid = 0;        // ordinals per thread (U)
+  bool coop = false;      // cooperative launch (in-kernel grid barrier + finalize)
   // Finalize: partial buf -> cell (buf, off, elems = width)
   enum FinK { Seq, Tree, Count } fin = Seq;
   int kernelStep = -1;

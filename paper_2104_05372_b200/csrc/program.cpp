@@ -151,6 +151,7 @@ int Program::prepare() {
     if (d.elems < 0) continue;                                              // dead
     if ((rc = dxrt::check(cuMemAlloc(&devptr[b], bytes), "cuMemAlloc"))) return rc;
     owned.push_back(devptr[b]);
+    if (d.role == BufDecl::Sync && (rc = dxrt::check(cuMemsetD8(devptr[b], 0, bytes), "memset sync"))) return rc;
     if (d.role == BufDecl::Const) {
       std::vector<char> host = convertInit(d);
       if ((rc = dxrt::check(cuMemcpyHtoD(devptr[b], host.data(), host.size()), "upload const"))) return rc;
@@ -334,7 +335,21 @@ int Program::issue() {
             if (kernelEventStep[e] == (int)i) ev = (int)e;
           if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].first, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
         }
-        if ((rc = launch(funcs[i], grids[i], s.threads, s.smem, argv.data()))) return rc;
+        if (s.coop) {
+          CUlaunchConfig cfg = {};
+          cfg.gridDimX = grids[i]; cfg.gridDimY = 1; cfg.gridDimZ = 1;
+          cfg.blockDimX = s.threads; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+          cfg.sharedMemBytes = s.smem;
+          cfg.hStream = st;
+          CUlaunchAttribute attr;
+          attr.id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+          attr.value.cooperative = 1;
+          cfg.attrs = &attr;
+          cfg.numAttrs = 1;
+          if ((rc = dxrt::check(cuLaunchKernelEx(&cfg, funcs[i], argv.data(), nullptr), "cuLaunchKernelEx(coop)"))) return rc;
+        } else if ((rc = launch(funcs[i], grids[i], s.threads, s.smem, argv.data()))) {
+          return rc;
+        }
         if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].second, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
         ++launches;
         break;
