@@ -300,57 +300,42 @@ __device__ __forceinline__ void dx_tile_store4(float* etile, int t, const float 
 // Vectorized variant of dx_tile_rows: thread tid owns (key k, column block jb)
 // pair p = tid % P (P = K*D/4) and split s = tid / P of the bucket (elements
 // q = start + s, s + NS, ...), accumulating a float4 in registers.
+// Four block barriers per tile: [rows + warp counts] | [one warp: prefix over
+// warps per key + scan over keys] | [scatter of row offsets] | [reduce; the
+// warp counts are re-zeroed for the next tile].  wcnt must be zero on entry
+// (zero it once before the first tile).
 template <int D, int K, int NT>
 __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* wcnt, int* start, int* perm,
                                               float4& acc) {
   constexpr int NB = D / 4, P = K * NB;
   constexpr int NS = P >= NT ? 1 : NT / P;
   constexpr int NW = NT / 32;
-  constexpr int SUBS = (NT / K) < 32 ? (NT / K) : 32;
-  constexpr int WPS = (NW + SUBS - 1) / SUBS;
+  constexpr int PER = (K + 31) / 32;
   static_assert(P <= NT, "one (key, block) pair per thread at most");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned peers = __match_any_sync(DX_FULL, key);
   const int rank = __popc(peers & ((1u << lane) - 1u));
-  for (int i = tid; i < NW * K; i += NT) wcnt[i] = 0;
-  __syncthreads();
   if (rank == 0 && key >= 0) wcnt[warp * K + key] = __popc(peers);
   __syncthreads();
-  if (tid < K * SUBS) {
-    const int k = tid / SUBS, sub = tid % SUBS;
-    int c[WPS];
-    int loc = 0;
-#pragma unroll
-    for (int q = 0; q < WPS; ++q) {
-      const int w = sub * WPS + q;
-      c[q] = w < NW ? wcnt[w * K + k] : 0;
-      loc += c[q];
-    }
-    int inc = loc;
-#pragma unroll
-    for (int o = 1; o < SUBS; o <<= 1) {
-      const int y = __shfl_up_sync(DX_FULL, inc, o, SUBS);
-      if (sub >= o) inc += y;
-    }
-    int run = inc - loc;
-#pragma unroll
-    for (int q = 0; q < WPS; ++q) {
-      const int w = sub * WPS + q;
-      if (w < NW) wcnt[w * K + k] = run;
-      run += c[q];
-    }
-    if (sub == SUBS - 1) start[k + 1] = inc;
-  }
-  __syncthreads();
   if (warp == 0) {
-    constexpr int PER = (K + 31) / 32;
-    int v[PER];
+    // lane owns keys lane*PER .. lane*PER+PER-1: exclusive prefix over the
+    // warps in place, bucket sizes, then a warp scan over the keys
+    int tot[PER];
     int loc = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int k = lane * PER + q;
-      v[q] = k < K ? start[k + 1] : 0;
-      loc += v[q];
+      int run = 0;
+      if (k < K) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const int c = wcnt[w * K + k];
+          wcnt[w * K + k] = run;
+          run += c;
+        }
+      }
+      tot[q] = run;
+      loc += run;
     }
     int inc = loc;
 #pragma unroll
@@ -363,7 +348,7 @@ __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* 
     for (int q = 0; q < PER; ++q) {
       const int k = lane * PER + q;
       if (k < K) start[k] = run;
-      run += v[q];
+      run += tot[q];
     }
     if (lane == 31) start[K] = inc;
   }
@@ -372,6 +357,7 @@ __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* 
   // one XOR away: (t*D*4 + 16*s(t)) ^ 16*jb  (see dx_tile_store4)
   if (key >= 0) perm[start[key] + wcnt[warp * K + key] + rank] = tid * (D * 4) + (((tid >> 1) & (NB - 1)) << 4);
   __syncthreads();
+  for (int i = tid; i < NW * K; i += NT) wcnt[i] = 0;  // ready for the next tile
   if (tid < P * NS) {
     const int p = tid % P, sp = tid / P;
     const int k = p / NB, jb16 = (p % NB) << 4;

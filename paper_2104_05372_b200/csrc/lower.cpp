@@ -403,6 +403,7 @@ struct CellUse {
   long long rowD = 0;
   int rowSitesN = 0;     // row-eligible accumulation sites (pass 0)
   bool vec4 = false;     // TileRow with float4 column blocks (f32, D % 4 == 0)
+  int aliasStage = -1;   // TMA-staged stream buffer whose stage doubles as the row tile
   long long width = 0;
   int partialBuf = -1;
   int targetBuf = -1;   // cell leaf buffer or its delta (sharded)
@@ -2589,7 +2590,8 @@ void Lowering::decideStrategies(KGen& g) {
       smemUsed += (int)cu.width * 4;
       continue;
     }
-    if (cu.allRow && cu.rowD > 0 && cu.rowSitesN == 1 && !opt.noRowScatter && !tileRowTaken) {
+    if (cu.allRow && cu.rowD > 0 && cu.rowSitesN == 1 && !opt.noRowScatter && !tileRowTaken &&
+        !std::getenv("DEXLET_NO_TILEROW")) {
       long long Kr = cu.width / cu.rowD;
       const int NT = tileThreads();
       long long need = (long long)NT * (cu.rowD + 1) * esize + (NT / 32) * Kr * 4 + (Kr + 1) * 4 + NT * 4 + 64;
@@ -2882,7 +2884,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   // ordinal stream in by cp.async.bulk (double-buffered, one tile ahead);
   // small read-only gather tables are copied to shared memory once.
   g.tile = false;
-  for (auto& cu : g.cells) g.tile |= cu.strat == CellUse::TileRow;
+  for (auto& cu : g.cells) g.tile |= cu.strat == CellUse::TileRow || cu.strat == CellUse::Row;
   g.staged.clear();
   g.wholeStaged.clear();
   g.tensorStaged.clear();
@@ -2911,6 +2913,13 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       g.wholeStaged.insert(b);
     }
     (void)es;
+  }
+  for (auto& cu : g.cells) {
+    cu.aliasStage = -1;
+    if (cu.strat != CellUse::TileRow || !cu.vec4) continue;
+    for (auto& [b, mask] : g.tensorStaged)
+      if (g.streamUse[b].first == cu.rowD && plan.bufs[b].kind == SK::F && !std::getenv("DEXLET_NO_ALIAS"))
+        cu.aliasStage = b;
   }
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
   int U = (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
@@ -2975,8 +2984,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     if (cu.strat == CellUse::TileRow) {
       long long Kr = cu.width / cu.rowD;
-      smem = std::max<int>(smem, cu.smemOff + (int)(g.threads * (cu.rowD + 1) * esize + (g.threads / 32) * Kr * 4 +
-                                                     (Kr + 1) * 4 + g.threads * 4 + 64));
+      long long etB = cu.aliasStage >= 0 ? 0 : (long long)g.threads * (cu.rowD + 1) * esize;
+      smem = std::max<int>(smem, cu.smemOff + (int)(etB + (g.threads / 32) * Kr * 4 + (Kr + 1) * 4 + g.threads * 4 + 64));
     }
   }
   int tileCell = -1;
@@ -3089,7 +3098,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         case CellUse::TileRow: {
           long long Kr = cu.width / cu.rowD;
           int nacc = (int)((cu.width + g.threads - 1) / g.threads);
-          long long et = (long long)g.threads * (cu.rowD + 1) * esize;
+          long long et = cu.aliasStage >= 0 ? 0 : (long long)g.threads * (cu.rowD + 1) * esize;
           if (cu.vec4) src << "  float4 acc" << I << " = make_float4(0.f, 0.f, 0.f, 0.f);\n";
           else {
             src << "  dx_f acc" << I << "[" << nacc << "];\n";
@@ -3099,6 +3108,10 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           src << "  int* wc" << I << " = (int*)(dx_smem + " << cu.smemOff + et << ");\n";
           src << "  int* st" << I << " = wc" << I << " + " << (g.threads / 32) * Kr << ";\n";
           src << "  int* pm" << I << " = st" << I << " + " << Kr + 1 << ";\n";
+          if (cu.vec4) {
+            src << "  for (int t = threadIdx.x; t < " << (g.threads / 32) * Kr << "; t += blockDim.x) wc" << I << "[t] = 0;\n";
+            needSync = true;
+          }
           break;
         }
         case CellUse::Row:
@@ -3162,7 +3175,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     // warp-uniform grid-stride loop over groups of U consecutive ordinals
     src << "  const long long dx_n = (dx_hi - dx_lo + " << (U - 1) << ") / " << U << ";\n";
     src << "  const long long dx_stride = (long long)gridDim.x * blockDim.x;\n";
-    if (tileCell >= 0 && !g.staged.empty()) {
+    if ((tileCell >= 0 || g.tile) && !g.staged.empty()) {
       // TMA pipeline: tile t+1 is in flight while tile t is computed
       src << "  if (threadIdx.x == 0 && (long long)blockIdx.x * blockDim.x < dx_n) dx_issue(0, (long long)blockIdx.x * blockDim.x);\n";
       src << "  int dx_it = 0;\n";
@@ -3221,8 +3234,14 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         long long Kr = cu.width / cu.rowD;
         int nacc = (int)((cu.width + g.threads - 1) / g.threads);
         if (cu.vec4) {
-          src << "    dx_tile_store4<" << rs.D << ">(et" << I << ", threadIdx.x, rowv" << rs.id << ");\n";
-          src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(et" << I << ", rowk" << rs.id
+          // The output rows may overwrite the TMA stage holding this tile's
+          // input rows when the shapes and swizzles agree: thread t only ever
+          // reads its own staged row before writing its own output row.
+          std::string etp = "et" + I;
+          if (cu.aliasStage >= 0)
+            etp = "(sb" + std::to_string(cu.aliasStage) + " + dx_sh" + std::to_string(cu.aliasStage) + ")";
+          src << "    dx_tile_store4<" << rs.D << ">(" << etp << ", threadIdx.x, rowv" << rs.id << ");\n";
+          src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(" << etp << ", rowk" << rs.id
               << ", wc" << I << ", st" << I << ", pm" << I << ", acc" << I << ");\n";
           continue;
         }
@@ -3235,6 +3254,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "    dx_row_flush<dx_f, " << rs.D << ">(rt" << rs.cu << " + dx_warp * " << cu.width
           << ", dx_stage, rowk" << rs.id << ", rowv" << rs.id << ");\n";
     }
+    if (tileCell < 0 && g.tile && !g.staged.empty())
+      src << "    __syncthreads();  // every thread is done with this TMA stage\n";
     src << "  }\n";
     src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
     // epilogue: block partials
@@ -3254,7 +3275,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         case CellUse::TileRow: {
           int nacc = (int)((cu.width + g.threads - 1) / g.threads);
           if (cu.vec4) {
-            src << "  dx_tile_rows4_flush<" << cu.rowD << ", " << cu.width / cu.rowD << ", " << g.threads << ">(et" << I
+            std::string scratch = cu.aliasStage >= 0 ? "sb" + std::to_string(cu.aliasStage) : "et" + I;
+            src << "  dx_tile_rows4_flush<" << cu.rowD << ", " << cu.width / cu.rowD << ", " << g.threads << ">(" << scratch
                 << ", acc" << I << ", part" << I << " + (long long)blockIdx.x * " << cu.width << ");\n";
             break;
           }
