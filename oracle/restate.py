@@ -31,6 +31,13 @@ def matmul_fwd(x, y):
     return np.asarray(x, np.float64) @ np.asarray(y, np.float64)
 
 
+def contraction(x, y, x_kmajor=True, y_kmajor=False):
+    """C[i][l] = sum_j x(i,j) y(j,l) in fp64 (programs.contraction)."""
+    a = np.asarray(x, np.float64) if x_kmajor else np.asarray(x, np.float64).T
+    b = np.asarray(y, np.float64).T if y_kmajor else np.asarray(y, np.float64)
+    return a @ b
+
+
 def matmul_grad(x, y):
     """loss = sum(x . y); d loss / d x = ones . y^T."""
     x = np.asarray(x, np.float64)

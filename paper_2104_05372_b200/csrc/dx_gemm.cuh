@@ -1,0 +1,258 @@
+// dx_gemm.cuh — hand-written sm_100a tensor-core GEMM for dense contraction
+// nests (`for i k. sum (for j. A.i.j * B.j.k)` recognized by the lowering).
+//
+//   C[m][n] (+)= sum_k A[m][k] * B[n][k]        (A, B K-major fp32 in HBM)
+//
+// tcgen05.mma kind::tf32, cta_group::1, M = 128, N = BN, fp32 accumulators in
+// TMEM.  fp32 parity with the f64 reference (<= 1e-4) uses 3xTF32: the MMA
+// reads the raw fp32 operands (tf32 = their top 19 bits) plus the residuals
+// lo = x - tf32(x) (dx_tf32_lo), and accumulates hi*hi + hi*lo + lo*hi.
+// Operand tiles arrive by TMA (2-D tensor maps, SWIZZLE_128B, box 32 x rows)
+// into a STAGES-deep mbarrier ring; one elected thread issues the MMAs and
+// releases stages with tcgen05.commit; four epilogue warps drain TMEM with
+// tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = tile rows) chunk by chunk.
+
+#define DX_GEMM_BM 128
+#define DX_GEMM_BK 32  // fp32 per 128-byte swizzle row
+
+__device__ __forceinline__ unsigned long long dx_umma_desc_sw128(unsigned saddr) {
+  // K-major, SWIZZLE_128B canonical layout: 8-row x 128 B atoms, SBO = 1024 B
+  return (unsigned long long)((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <int BN>
+__device__ __forceinline__ unsigned dx_idesc_tf32() {
+  // c_format F32 (bit 4), a/b format TF32 (2 at bits 7, 10), K-major, N>>3 at 17, M>>4 at 24
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(DX_GEMM_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void dx_umma_tf32(unsigned tmem, unsigned long long da, unsigned long long db,
+                                             unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void dx_umma_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   dx_smem_addr(bar))
+               : "memory");
+}
+
+// mbarrier wait with a bound: a descriptor/TMA fault traps (launch error)
+// instead of spinning forever.
+__device__ __forceinline__ void dx_mbar_wait_bounded(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  for (long long it = 0; it < (1LL << 26); ++it) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(dx_smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+  }
+  __trap();
+}
+
+__device__ __forceinline__ float dx_tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+extern "C" __global__ void dx_tf32_lo(const float* __restrict__ x, float* __restrict__ lo, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    lo[i] = x[i] - dx_tf32_trunc(x[i]);
+}
+
+// dst[c][r] = src[r][c]  (rows x cols fp32), 32x32 smem tiles, 256 threads,
+// one tile per block (1-D grid over row tiles x column tiles)
+extern "C" __global__ void __launch_bounds__(256) dx_transpose_f32(const float* __restrict__ src,
+                                                                   float* __restrict__ dst, long long rows,
+                                                                   long long cols) {
+  __shared__ float t[32][33];
+  const long long ct = (cols + 31) / 32;
+  const long long r0 = (long long)(blockIdx.x / ct) * 32, c0 = (long long)(blockIdx.x % ct) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = ty; k < 32; k += 8) {
+    const long long r = r0 + k, c = c0 + tx;
+    if (r < rows && c < cols) t[k][tx] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const long long c = c0 + k, r = r0 + tx;
+    if (r < rows && c < cols) dst[c * rows + r] = t[tx][k];
+  }
+}
+
+__device__ __forceinline__ void dx_mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dx_smem_addr(bar)) : "memory");
+}
+
+#define DX_TMEM_LD32(taddr, v)                                                                                    \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"           \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                   \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),           \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),     \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),   \
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])    \
+      : "r"(taddr))
+
+// Accumulation precision.  The tensor core adds into its fp32 accumulator
+// with truncation, so a long K drifts (measured 1.5e-4 rel at K = 1024 with
+// one accumulator).  Two remedies, both free on TMEM: the large hi*hi
+// products and the small residual products (hi*lo + lo*hi, ~2^-11 smaller)
+// go to separate accumulators, and every DX_GEMM_CHUNK k-blocks the
+// epilogue warps promote both into fp32 registers with round-to-nearest
+// adds.  Accumulators are double-buffered in TMEM (4 x BN columns) so the
+// promotion of chunk c overlaps the MMAs of chunk c+1.
+#define DX_GEMM_CHUNK 4
+
+// Warps 0-3: epilogue (warp w owns TMEM lanes / tile rows 32w..32w+31);
+// warp 4: TMA producer; warp 5: MMA issuer.  mode 0: C = acc, 1: C += acc.
+template <int BN, int STAGES, class CT>
+__device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap* tal, const dx_tmap* tb,
+                                               const dx_tmap* tbl, long long M, long long N, long long K, CT* C,
+                                               long long ldc, long long mode) {
+  constexpr unsigned A_BYTES = DX_GEMM_BM * 128, B_BYTES = BN * 128;
+  constexpr unsigned STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  constexpr unsigned TMEM_COLS = 4 * BN;
+  static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
+  extern __shared__ __align__(1024) unsigned char dx_gemm_smem_raw[];
+  unsigned char* smem = dx_gemm_smem_raw + ((1024u - (dx_smem_addr(dx_gemm_smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ unsigned tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NT = (int)((N + BN - 1) / BN);
+  const int m0 = (int)(blockIdx.x / NT) * DX_GEMM_BM, n0 = (int)(blockIdx.x % NT) * BN;
+  const int KB = (int)((K + DX_GEMM_BK - 1) / DX_GEMM_BK);
+  const int NC = (KB + DX_GEMM_CHUNK - 1) / DX_GEMM_CHUNK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      dx_mbar_init(&full[s], 1);
+      dx_mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      dx_mbar_init(&tfull[b], 1);
+      dx_mbar_init(&tempty[b], 4);
+    }
+    dx_fence_mbar_init();
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = tmem_base;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) dx_mbar_wait_bounded(&empty[s], (unsigned)(((kb / STAGES) - 1) & 1));
+        unsigned char* st = smem + s * STAGE_BYTES;
+        dx_mbar_expect_tx(&full[s], STAGE_BYTES);
+        dx_tma_2d(st, ta, kb * DX_GEMM_BK, m0, &full[s]);
+        dx_tma_2d(st + A_BYTES, tal, kb * DX_GEMM_BK, m0, &full[s]);
+        dx_tma_2d(st + 2 * A_BYTES, tb, kb * DX_GEMM_BK, n0, &full[s]);
+        dx_tma_2d(st + 2 * A_BYTES + B_BYTES, tbl, kb * DX_GEMM_BK, n0, &full[s]);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const unsigned idesc = dx_idesc_tf32<BN>();
+      for (int c = 0; c < NC; ++c) {
+        const int b = c & 1;
+        if (c >= 2) dx_mbar_wait_bounded(&tempty[b], (unsigned)(((c >> 1) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned tbig = tmem + (unsigned)(b * 2 * BN), tsmall = tbig + BN;
+        const int k1 = min(KB, (c + 1) * DX_GEMM_CHUNK);
+        for (int kb = c * DX_GEMM_CHUNK; kb < k1; ++kb) {
+          const int s = kb % STAGES;
+          dx_mbar_wait_bounded(&full[s], (unsigned)((kb / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const unsigned st = dx_smem_addr(smem + s * STAGE_BYTES);
+          const unsigned first = kb == c * DX_GEMM_CHUNK;
+#pragma unroll
+          for (int kk = 0; kk < DX_GEMM_BK / 8; ++kk) {
+            const unsigned long long ah = dx_umma_desc_sw128(st + kk * 32);
+            const unsigned long long al = dx_umma_desc_sw128(st + A_BYTES + kk * 32);
+            const unsigned long long bh = dx_umma_desc_sw128(st + 2 * A_BYTES + kk * 32);
+            const unsigned long long bl = dx_umma_desc_sw128(st + 2 * A_BYTES + B_BYTES + kk * 32);
+            const unsigned accum = !(first && kk == 0);
+            dx_umma_tf32(tbig, ah, bh, idesc, accum);
+            dx_umma_tf32(tsmall, ah, bl, idesc, accum);
+            dx_umma_tf32(tsmall, al, bh, idesc, 1u);
+          }
+          dx_umma_commit(&empty[s]);  // frees the stage once these MMAs retire
+        }
+        dx_umma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    // epilogue warps: promote each chunk into fp32 registers (RN adds)
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    const unsigned lanebase = tmem + ((unsigned)(warp * 32) << 16);
+    for (int c = 0; c < NC; ++c) {
+      const int b = c & 1;
+      dx_mbar_wait_bounded(&tfull[b], (unsigned)((c >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < BN / 32; ++q) {
+        unsigned vb[32], vs[32];
+        DX_TMEM_LD32(lanebase + (unsigned)(b * 2 * BN + q * 32), vb);
+        DX_TMEM_LD32(lanebase + (unsigned)(b * 2 * BN + BN + q * 32), vs);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[q * 32 + j] += __uint_as_float(vb[j]) + __uint_as_float(vs[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) dx_mbar_arrive(&tempty[b]);
+    }
+    const long long row = m0 + warp * 32 + lane;
+    if (row < M) {
+      CT* out = C + row * ldc + n0;
+      const bool vec = sizeof(CT) == 4 && n0 + BN <= N && ((ldc | n0) & 3) == 0 &&
+                       ((reinterpret_cast<unsigned long long>(C) & 15) == 0);
+      if (vec && mode == 0) {
+#pragma unroll
+        for (int j = 0; j < BN; j += 4)
+          *reinterpret_cast<float4*>(out + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN; ++j) {
+          if (n0 + j < N) {
+            if (mode == 0) out[j] = (CT)acc[j];
+            else out[j] += (CT)acc[j];
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+#define DX_GEMM_SMEM(BN, STAGES) (STAGES * (2 * DX_GEMM_BM * 128 + 2 * (BN)*128) + 1024)
+
+extern "C" __global__ void __launch_bounds__(192, 1)
+    dx_gemm_tf32x3_n128(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
+                        const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
+                        long long N, long long K, float* C, long long ldc, long long mode) {
+  dx_gemm_tf32x3<128, 3, float>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode);
+}
+extern "C" __global__ void __launch_bounds__(192, 1)
+    dx_gemm_tf32x3_n128_d(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
+                          const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
+                          long long N, long long K, double* C, long long ldc, long long mode) {
+  dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode);
+}

@@ -33,6 +33,7 @@
 
 #include "dexlet/errors.hpp"
 #include "dexlet/printer.hpp"
+#include "runtime.hpp"
 
 namespace dexlet {
 namespace dev {
@@ -1401,6 +1402,8 @@ class Lowering {
   // Kernel drivers (defined after KGen helpers).
   HV loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool serial, Span sp);
   HV loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs);
+  HV tryGemm(const HV& lz, const std::vector<DescPtr>& dims, const std::vector<Name>& binders, const ExprPtr& body,
+             const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs);
   HV serialKernel(const HEnvP& env, const ExprPtr& e, const ValuePtr& annot);
 
   // ------------------------------------------------------------------
@@ -3423,6 +3426,7 @@ HV Lowering::loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs,
     binders.push_back(inner->binder);
     body = inner->body;
   }
+  if (HV gm = tryGemm(lz, dims, binders, body, intoBufs, intoOffs)) return gm;
   DescPtr all = dims[0];
   for (size_t i = 1; i < dims.size(); ++i) all = descPair(all, dims[i]);
   // a flattened kernel iterates the pair set; its output layout is the
@@ -3445,6 +3449,193 @@ HV Lowering::loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs,
     return h;
   }
   return r;
+}
+
+// ---------------------------------------------------------------------------
+// Dense contractions on the tensor cores.
+//
+// Recognizes the flattened nest the front end produces for `for i k. sum (for
+// j. P.i.j * Q.j.k)` (parser.cpp:697-723 elabSum -> runAccum over `acc +=`):
+//
+//   for i k. let hd = runAccum \h acc. (let t = for j. (..reads..; acc += a*b); ())
+//            let st = snd hd; st
+//
+// where each factor is a 2-level read of a Float matrix indexed by one output
+// dimension and the contraction index j (either order).  It becomes
+// C[M=|i|][N=|k|] = A[M][K] . B[N][K]^T on dx_gemm_tf32x3 (tcgen05, TMEM,
+// TMA): operands stored j-major are transposed once, and the tf32 residuals
+// for 3xTF32 are produced by dx_tf32_lo.  f32 mode, one rank; everything else
+// stays on the generic loop kernels.
+HV Lowering::tryGemm(const HV& lz, const std::vector<DescPtr>& dims, const std::vector<Name>& binders,
+                     const ExprPtr& body, const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs) {
+  if (plan.f64 || plan.world > 1 || dims.size() != 2 || opt.noGemm || std::getenv("DEXLET_NO_GEMM")) return nullptr;
+  const auto* l1 = as<ELet>(body);
+  if (!l1) return nullptr;
+  const auto* ra = as<ERunAccum>(l1->bound);
+  const auto* l2 = as<ELet>(l1->body);
+  if (!ra || !l2) return nullptr;
+  const auto* sn = as<ESnd>(l2->bound);
+  const auto* r2 = as<ERet>(l2->body);
+  if (!sn || !r2) return nullptr;
+  const auto* snv = as<VVar>(sn->v);
+  const auto* rv = as<VVar>(r2->value);
+  if (!snv || snv->name != l1->binder || !rv || rv->name != l2->binder) return nullptr;
+  const Name acc = ra->action.ref;
+  const auto* l3 = as<ELet>(ra->action.body);
+  if (!l3) return nullptr;
+  const auto* fj = as<EFor>(l3->bound);
+  if (!fj || !as<ERet>(l3->body)) return nullptr;
+  DescPtr dj;
+  try {
+    dj = resolveDesc(fj->annot, hostLook(lz->env));
+  } catch (const DexError&) {
+    return nullptr;
+  }
+  // symbolic walk of the j body: reads base.(idx...) and one product
+  struct Sym {
+    int kind = 0;  // 0 read, 1 product, 2 effect
+    HV base;
+    std::vector<int> idx;
+    std::shared_ptr<Sym> a, b;
+  };
+  std::map<Name, Sym> syms;
+  auto loopVar = [&](const ValuePtr& v) -> int {
+    const auto* vv = as<VVar>(v);
+    if (!vv) return -1;
+    if (vv->name == binders[0]) return 0;
+    if (vv->name == binders[1]) return 1;
+    if (vv->name == fj->binder) return 2;
+    return -1;
+  };
+  std::shared_ptr<Sym> prod;
+  ExprPtr cur = fj->body;
+  while (const auto* l = as<ELet>(cur)) {
+    Sym s;
+    if (const auto* ix = as<EIndex>(l->bound)) {
+      int lv = loopVar(ix->idx);
+      const auto* av = as<VVar>(ix->arr);
+      if (lv < 0 || !av) return nullptr;
+      auto it = syms.find(av->name);
+      if (it != syms.end()) {
+        if (it->second.kind != 0) return nullptr;
+        s = it->second;
+      } else {
+        HV h = hlookup(lz->env, av->name);
+        if (!h || (h->k != HVal::Buf && h->k != HVal::Lazy)) return nullptr;
+        s.base = h;
+      }
+      s.idx.push_back(lv);
+    } else if (const auto* bo = as<EBinOp>(l->bound)) {
+      const auto* x = as<VVar>(bo->l);
+      const auto* y = as<VVar>(bo->r);
+      if (bo->op != BinOp::Mul || !x || !y || !syms.count(x->name) || !syms.count(y->name)) return nullptr;
+      const Sym &sx = syms[x->name], &sy = syms[y->name];
+      if (sx.kind != 0 || sy.kind != 0 || sx.idx.size() != 2 || sy.idx.size() != 2) return nullptr;
+      s.kind = 1;
+      s.a = std::make_shared<Sym>(sx);
+      s.b = std::make_shared<Sym>(sy);
+    } else if (const auto* rt = as<ERet>(l->bound)) {
+      const auto* v = as<VVar>(rt->value);
+      if (!v || !syms.count(v->name)) return nullptr;
+      s = syms[v->name];
+    } else if (const auto* ac = as<EAccum>(l->bound)) {
+      const auto* r = as<VVar>(ac->ref);
+      const auto* v = as<VVar>(ac->value);
+      if (!r || r->name != acc || !v || !syms.count(v->name) || syms[v->name].kind != 1 || prod) return nullptr;
+      prod = std::make_shared<Sym>(syms[v->name]);
+      s.kind = 2;
+    } else {
+      return nullptr;
+    }
+    syms[l->binder] = s;
+    cur = l->body;
+  }
+  if (!prod || !as<ERet>(cur)) return nullptr;
+  auto uses = [](const Sym& f, int d) { return f.idx[0] == d || f.idx[1] == d; };
+  std::shared_ptr<Sym> P = prod->a, Q = prod->b;
+  if (!(uses(*P, 0) && uses(*P, 2))) std::swap(P, Q);
+  if (!(uses(*P, 0) && uses(*P, 2) && uses(*Q, 1) && uses(*Q, 2))) return nullptr;
+  const long long M = size(dims[0]), N = size(dims[1]), K = size(dj);
+  if (M <= 0 || N <= 0 || K <= 0 || K % 4 != 0 || M > (1LL << 31) || N > (1LL << 31)) return nullptr;
+  auto operand = [&](const Sym& f) -> std::pair<int, long long> {
+    HV h = f.base->k == HVal::Lazy ? materialize(f.base) : f.base;
+    if (h->k != HVal::Buf || h->bufs.size() != 1 || plan.bufs[h->bufs[0]].kind != SK::F) return {-1, 0};
+    return {h->bufs[0], h->offs[0]};
+  };
+  auto [pb, po] = operand(*P);
+  auto [qb, qo] = operand(*Q);
+  if (pb < 0 || qb < 0) return nullptr;
+  plan.gemm = true;
+  auto kstep = [&](const std::string& name, int threads, int smem, long long grid, std::vector<KArg> args,
+                   const std::string& note) {
+    Step st;
+    st.k = Step::Kernel;
+    st.name = name;
+    st.threads = threads;
+    st.smem = smem;
+    st.fixedGrid = grid;
+    st.total = grid;
+    st.args = std::move(args);
+    st.note = note;
+    addStep(st);
+    plan.numKernels++;
+  };
+  auto bufArg = [](int b, long long off) { KArg a; a.k = KArg::Buf; a.buf = b; a.off = off; return a; };
+  auto intArg = [](long long v) { KArg a; a.k = KArg::I64; a.i = v; return a; };
+  // K-major operand [rows][K]: direct when stored that way and 16-byte aligned, else transposed
+  auto kmajor = [&](const Sym& f, int b, long long off, long long rows, int outDim) -> std::pair<int, long long> {
+    if (f.idx[0] == outDim && off % 4 == 0) return {b, off};
+    int t = newBuf(BufDecl::Temp, SK::F, rows * K);
+    if (f.idx[0] == outDim) {
+      Step c; c.k = Step::CopyBuf; c.buf = t; c.buf2 = b; c.off2 = off; c.elems = rows * K; addStep(c);
+    } else {
+      kstep("dx_transpose_f32", 256, 0, ((K + 31) / 32) * ((rows + 31) / 32),
+            {bufArg(b, off), bufArg(t, 0), intArg(K), intArg(rows)}, "transpose gemm operand");
+    }
+    return {t, 0};
+  };
+  auto [ab, ao] = kmajor(*P, pb, po, M, 0);
+  auto [bb, bo] = kmajor(*Q, qb, qo, N, 1);
+  auto lo = [&](int b, long long off, long long n) {
+    int t = newBuf(BufDecl::Temp, SK::F, n);
+    kstep("dx_tf32_lo", 256, 0, std::min<long long>((n + 255) / 256, 148 * 16),
+          {bufArg(b, off), bufArg(t, 0), intArg(n)}, "tf32 residual");
+    return t;
+  };
+  int al = lo(ab, ao, M * K), bl = lo(bb, bo, N * K);
+  int cb;
+  long long co = 0;
+  if (intoBufs) {
+    cb = (*intoBufs)[0];
+    co = (*intoOffs)[0];
+  } else {
+    cb = newBuf(BufDecl::Output, SK::F, M * N);
+  }
+  auto tmap = [&](int b, long long off, long long rows) {
+    KArg a;
+    a.k = KArg::TMap;
+    a.buf = b;
+    a.off = off;
+    a.rowLen = K;
+    a.rows = rows;
+    a.boxRows = rows >= 128 ? 128 : 128;  // partial tiles: TMA zero-fills out-of-range rows
+    a.boxCols = 32;
+    a.swizzle = 128;
+    return a;
+  };
+  const int BN = 128, STAGES = 3;
+  KArg tb = tmap(bb, bo, N), tbl = tmap(bl, 0, N);
+  tb.boxRows = tbl.boxRows = BN;
+  kstep("dx_gemm_tf32x3_n128", 192, STAGES * (2 * 128 * 128 + 2 * BN * 128) + 1024, ((M + 127) / 128) * ((N + BN - 1) / BN),
+        {tmap(ab, ao, M), tmap(al, 0, M), tb, tbl, intArg(M), intArg(N), intArg(K), bufArg(cb, co), intArg(N), intArg(0)},
+        "tcgen05 gemm " + std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K) + " (materialize " +
+            printName(lz->binder) + ")");
+  auto h = std::make_shared<HVal>();
+  h->k = HVal::Buf;
+  h->ty = tTable(dims[0], tTable(dims[1], tFloat()));
+  h->bufs = {cb};
+  h->offs = {co};
+  return h;
 }
 
 HV Lowering::serialKernel(const HEnvP& env, const ExprPtr& e, const ValuePtr& annot) {
@@ -3569,7 +3760,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
     if (st.buf >= 0) live[st.buf] = true;
     if (st.buf2 >= 0) live[st.buf2] = true;
     for (auto& a : st.args)
-      if (a.k == KArg::Buf && a.buf >= 0) live[a.buf] = true;
+      if ((a.k == KArg::Buf || a.k == KArg::TMap) && a.buf >= 0) live[a.buf] = true;
   }
   std::vector<Step> kept;
   for (auto& st : L.plan.steps) {
@@ -3590,6 +3781,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
   for (size_t b = 0; b < L.plan.bufs.size(); ++b)
     if (!live[b]) L.plan.bufs[b].elems = -1;  // not allocated
   L.plan.steps = std::move(kept);
+  if (L.plan.gemm) L.plan.source += std::string("\n") + dxrt::gemmSource();
   return std::move(L.plan);
 }
 

@@ -60,6 +60,7 @@ struct KArg {
   // elements starting at element `off`; box = boxRows x rowLen; swizzle bytes
   long long rowLen = 0, rows = 0;
   int boxRows = 0, swizzle = 0;
+  int boxCols = 0;     // box width in elements (0: the whole row)
 };
 
 struct Step {
@@ -76,6 +77,7 @@ struct Step {
   int smem = 0;           // dynamic shared memory bytes
   int minGrid = 0;        // ordinals per thread (U)
   bool coop = false;      // cooperative launch (in-kernel grid barrier + finalize)
+  long long fixedGrid = 0;  // >0: launch exactly this many blocks (tile kernels: GEMM, transpose)
   // Finalize: partial buf -> cell (buf, off, elems = width)
   enum FinK { Seq, Tree, Count } fin = Seq;
   int kernelStep = -1;
@@ -114,6 +116,7 @@ struct Plan {
   DTy outputType;
   int errFlagBuf = -1;          // E-bounds flag raised by fused index checks
   int numKernels = 0;
+  bool gemm = false;            // uses the tcgen05 contraction kernels (dx_gemm.cuh)
   std::string summary() const;
 };
 
@@ -123,6 +126,7 @@ struct LowerOptions {
   int threads = 256;
   bool noFusion = false;
   bool noRowScatter = false;
+  bool noGemm = false;
 };
 
 // Lowers `e` (first-order, post-optimize) whose free variables are the

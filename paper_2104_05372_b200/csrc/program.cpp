@@ -125,6 +125,10 @@ int Program::prepare() {
       hi = b;
     }
     ranges[i] = {lo, hi};
+    if (s.fixedGrid > 0) {
+      grids[i] = (int)s.fixedGrid;
+      continue;
+    }
     if (s.serial) {
       grids[i] = 1;
       continue;
@@ -204,7 +208,7 @@ int Program::buildTensorMaps() {
       CUtensorMap m;
       cuuint64_t dims[2] = {(cuuint64_t)a.rowLen, (cuuint64_t)a.rows};
       cuuint64_t strides[1] = {(cuuint64_t)(a.rowLen * es)};
-      cuuint32_t box[2] = {(cuuint32_t)a.rowLen, (cuuint32_t)a.boxRows};
+      cuuint32_t box[2] = {(cuuint32_t)(a.boxCols > 0 ? a.boxCols : a.rowLen), (cuuint32_t)a.boxRows};
       cuuint32_t estr[2] = {1, 1};
       CUtensorMapSwizzle sw = a.swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                               : a.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B

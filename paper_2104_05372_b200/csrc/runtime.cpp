@@ -27,6 +27,7 @@
 #include <unordered_map>
 
 #include "dx_device_src.inc"  // kDxDeviceSource: hand-written device runtime
+#include "dx_gemm_src.inc"    // kDxGemmSource: tcgen05 GEMM for contraction nests
 
 namespace dxrt {
 
@@ -36,6 +37,7 @@ void setError(const std::string& msg) { g_lastError = msg; }
 const std::string& lastError() { return g_lastError; }
 
 const char* deviceRuntimeSource() { return kDxDeviceSource; }
+const char* gemmSource() { return kDxGemmSource; }
 
 static bool g_cuInit = false;
 static std::mutex g_mu;

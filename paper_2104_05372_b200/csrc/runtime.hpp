@@ -17,6 +17,7 @@ int ensureInit();
 // NVRTC: prepend the device runtime, compile for sm_100a, return the cubin.
 int compileCubin(const std::string& source, std::string& cubin);
 const char* deviceRuntimeSource();
+const char* gemmSource();  // dx_gemm.cuh: tcgen05 contraction kernels
 int loadNccl();
 
 struct Ctx {

@@ -24,6 +24,25 @@ def matmul_fwd(n: int) -> str:
             f"for i k. sum (for j. (x.i.j) * (y.j.k))\n")
 
 
+def contraction(m: int, n: int, k: int, x_kmajor: bool = True, y_kmajor: bool = False) -> str:
+    """Rectangular `for i l. sum for j. x.(i,j) * y.(j,l)` with either storage
+    order of each operand (x_kmajor: x is (Fin m)=>(Fin k); y_kmajor: y is
+    (Fin n)=>(Fin k)).  The tcgen05 GEMM path's parity cases."""
+    xt = _mat(m, k) if x_kmajor else _mat(k, m)
+    yt = _mat(n, k) if y_kmajor else _mat(k, n)
+    xr = "x.i.j" if x_kmajor else "x.j.i"
+    yr = "y.l.j" if y_kmajor else "y.j.l"
+    return (f"main = \\x:{xt}. \\y:{yt}. "
+            f"for i l. sum (for j. ({xr}) * ({yr}))\n")
+
+
+def contraction_inputs(m: int, n: int, k: int, x_kmajor: bool = True, y_kmajor: bool = False, seed: int = 20211):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (m, k) if x_kmajor else (k, m)).astype(np.float32)
+    y = rng.uniform(-1, 1, (n, k) if y_kmajor else (k, n)).astype(np.float32)
+    return x, y
+
+
 def matmul_grad(n: int) -> str:
     """config 1: value and gradient of sum(x . y) w.r.t. x (linearize + transpose)."""
     return (f"main = \\x:{_mat(n, n)}. \\y:{_mat(n, n)}.\n"

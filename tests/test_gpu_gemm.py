@@ -1,0 +1,68 @@
+"""GPU: dense contraction nests on the tcgen05 GEMM (dx_gemm.cuh) vs the fp64
+restatement (oracle/restate.py, pinned against the reference in
+tests/test_oracle.py) and, at small sizes, the reference evaluator itself.
+
+Tolerance: rtMaxRelDiff (eval.cpp:758-763) <= 1e-4 (f32 mode; 3xTF32 products
+accumulate in fp32 in TMEM, K-ordered within a tile)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_05372_b200 as dx
+from oracle import restate
+from paper_2104_05372_b200 import programs as P
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (64, 64, 64, True, False),
+    (256, 256, 256, True, False),
+    (200, 136, 68, True, False),     # ragged M, N; K not a multiple of 32
+    (130, 260, 32, False, True),     # both operands transposed relative to the natural order
+    (128, 128, 4, True, True),       # K below one k-block
+    (1000, 520, 1024, False, False),
+    (384, 128, 4096, True, True),    # long K: many pipeline wraps
+    (1, 1, 8, True, False),          # single element
+]
+
+
+@pytest.mark.parametrize("m,n,k,xk,yk", SHAPES)
+def test_contraction_on_tensor_cores(ctx, m, n, k, xk, yk):
+    src = P.contraction(m, n, k, xk, yk)
+    x, y = P.contraction_inputs(m, n, k, xk, yk)
+    prog = dx.Program(src, ctx=ctx)
+    assert "tcgen05 gemm" in prog.plan
+    (c,) = prog(x, y)
+    want = restate.contraction(x, y, xk, yk)
+    assert oracle.rel_diff(c, want.ravel()) <= 1e-4
+    if m * n * k <= 1 << 21:
+        (r,) = oracle.RefProgram(src)(x, y)
+        assert oracle.rel_diff(c, r) <= 1e-4
+
+
+def test_gemm_repeat_deterministic(ctx):
+    m, n, k = 512, 384, 512
+    src = P.contraction(m, n, k)
+    x, y = P.contraction_inputs(m, n, k)
+    prog = dx.Program(src, ctx=ctx)
+    a = prog(x, y)[0]
+    b = prog(x, y)[0]
+    np.testing.assert_array_equal(a, b)
+
+
+def test_gemm_precision_beats_plain_tf32(ctx):
+    """3xTF32: error ~fp32 rounding, far below a single tf32 pass (~1e-3)."""
+    m = n = k = 512
+    x, y = P.contraction_inputs(m, n, k, seed=7)
+    (c,) = dx.Program(P.contraction(m, n, k), ctx=ctx)(x, y)
+    want = restate.contraction(x, y)
+    err = np.abs(c.reshape(m, n) - want).max() / np.abs(want).max()
+    assert err < 2e-6, err
+
+
+def test_matmul_fwd_uses_gemm(ctx):
+    x, y = P.matmul_inputs(256)
+    prog = dx.Program(P.matmul_fwd(256), ctx=ctx)
+    assert "tcgen05 gemm 256x256x256" in prog.plan
+    (z,) = prog(x, y)
+    assert oracle.rel_diff(z, restate.matmul_fwd(x, y).ravel()) <= 1e-4

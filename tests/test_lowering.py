@@ -58,13 +58,17 @@ def test_histogram_uses_exact_shared_counters():
     prog = dx.Program(P.histogram(1 << 20, 4096), ctx=None)
     assert len(_kernels(prog.plan)) == 1
     assert "dx_count_smem" in prog.source
-    assert "count" in prog.plan  # finalize of u32 counters scaled by the constant
+    # u32 counters folded in fixed block order and scaled by the constant,
+    # after the in-kernel grid barrier (cooperative launch) or by a finalize step
+    assert "dx_coop_fold<double, unsigned>" in prog.source or "count" in prog.plan
     sass = _sass(prog.source)
     assert "ATOMS" in sass and "LDG.E.128" in sass
 
 
 def test_matmul_forward_flattens_perfect_nest():
-    prog = dx.Program(P.matmul_fwd(64), ctx=None)
+    """The generic path flattens `for i k.` into one 4096-ordinal kernel (the
+    f64 parity mode keeps it; f32 mode sends this nest to the GEMM)."""
+    prog = dx.Program(P.matmul_fwd(64), ctx=None, float64=True)
     ks = _kernels(prog.plan)
     assert len(ks) == 1 and "n=4096" in ks[0], prog.plan
 
@@ -87,3 +91,20 @@ def test_dead_cells_are_not_allocated():
 def test_sharded_plan_allreduces_cells():
     prog = dx.Program(P.kmeans_cost_grad(1000, 16, 8), ctx=None, rank=1, world=2)
     assert prog.plan.count("allreduce") == 2
+
+
+def test_contraction_recognized_as_gemm():
+    """`for i l. sum for j. x*y` lowers to the tcgen05 GEMM in f32 mode, with a
+    transpose only for operands stored j-major; f64 parity mode and K % 4 != 0
+    keep the generic loop kernel."""
+    p = dx.Program(P.contraction(200, 136, 68, True, False), ctx=None).plan
+    assert "tcgen05 gemm 200x136x68" in p and p.count("dx_transpose_f32") == 1
+    p = dx.Program(P.contraction(64, 64, 64, True, True), ctx=None).plan
+    assert "tcgen05 gemm" in p and "dx_transpose_f32" not in p
+    p = dx.Program(P.contraction(64, 64, 64, False, False), ctx=None).plan
+    assert p.count("dx_transpose_f32") == 2
+    src = dx.Program(P.contraction(64, 64, 64), ctx=None).source
+    sass = _sass(src)
+    assert "UTCHMMA" in sass and "UTMALDG.2D" in sass and "LDTM" in sass  # tcgen05.mma, TMA, tcgen05.ld
+    assert "tcgen05" not in dx.Program(P.contraction(64, 64, 64), ctx=None, float64=True).plan
+    assert "tcgen05" not in dx.Program(P.contraction(64, 64, 6), ctx=None).plan
