@@ -75,7 +75,7 @@ def config_spec(name, world):
         x, w1, w2 = P.mlp_inputs(b, i, h, o)
         return dict(metric="MLP fwd+grad evals/s (batch 8192/GPU, 1024^3, square activation)",
                     src=P.mlp_grad(b, i, h, o), inputs=[[x], [w1, w2]], bound="tensor",
-                    work=2 * (2 * 8192 * 1024 * 1024) * 2 + 3 * 8192 * 1024 * 1024 * 2,
+                    work=5 * 2 * 8192 * 1024 * 1024,
                     work_basis="fwd 2 GEMMs + bwd dW2, dH, dW1 (2*B*1024^2 flops each)",
                     workload="2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) "
                              "(BASELINE configs[4])", extra={"batch_total": b}, out_bytes=4 + 2 * 1024 * 1024 * 4)

@@ -489,6 +489,9 @@ extern "C" __global__ void dx_add_f32(float* c, const float* s, long long n) {
 extern "C" __global__ void dx_add_f64(double* c, const double* s, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) c[i] += s[i];
 }
+extern "C" __global__ void dx_add_f64_f32(double* c, const float* s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) c[i] += (double)s[i];
+}
 // Element-type conversion copies (f32 values into f64 cells and back).
 extern "C" __global__ void dx_cvt_f32_f64(double* d, const float* s, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = s[i];

@@ -4,9 +4,10 @@
 //   C[m][n] (+)= sum_k A[m][k] * B[n][k]        (A, B K-major fp32 in HBM)
 //
 // tcgen05.mma kind::tf32, cta_group::1, M = 128, N = BN, fp32 accumulators in
-// TMEM.  fp32 parity with the f64 reference (<= 1e-4) uses 3xTF32: the MMA
-// reads the raw fp32 operands (tf32 = their top 19 bits) plus the residuals
-// lo = x - tf32(x) (dx_tf32_lo), and accumulates hi*hi + hi*lo + lo*hi.
+// TMEM.  fp32 parity with the f64 reference (<= 1e-4) uses 3xTF32: every
+// operand arrives as an exact-tf32 pair hi + lo (dx_tf32_split, written by the
+// generated operand prologues of contract.inc) and the MMA accumulates
+// hi*hi + hi*lo + lo*hi.
 // Operand tiles arrive by TMA (2-D tensor maps, SWIZZLE_128B, box 32 x rows)
 // into a STAGES-deep mbarrier ring; one elected thread issues the MMAs and
 // releases stages with tcgen05.commit; four epilogue warps drain TMEM with
@@ -56,30 +57,16 @@ __device__ __forceinline__ void dx_mbar_wait_bounded(unsigned long long* bar, un
 }
 
 __device__ __forceinline__ float dx_tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-
-extern "C" __global__ void dx_tf32_lo(const float* __restrict__ x, float* __restrict__ lo, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    lo[i] = x[i] - dx_tf32_trunc(x[i]);
+// round to the nearest tf32 (10 explicit mantissa bits): the tensor core then
+// reads the value exactly instead of truncating it
+__device__ __forceinline__ float dx_tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
-
-// dst[c][r] = src[r][c]  (rows x cols fp32), 32x32 smem tiles, 256 threads,
-// one tile per block (1-D grid over row tiles x column tiles)
-extern "C" __global__ void __launch_bounds__(256) dx_transpose_f32(const float* __restrict__ src,
-                                                                   float* __restrict__ dst, long long rows,
-                                                                   long long cols) {
-  __shared__ float t[32][33];
-  const long long ct = (cols + 31) / 32;
-  const long long r0 = (long long)(blockIdx.x / ct) * 32, c0 = (long long)(blockIdx.x % ct) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int k = ty; k < 32; k += 8) {
-    const long long r = r0 + k, c = c0 + tx;
-    if (r < rows && c < cols) t[k][tx] = src[r * cols + c];
-  }
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const long long c = c0 + k, r = r0 + tx;
-    if (r < rows && c < cols) dst[c * rows + r] = t[tx][k];
-  }
+// 3xTF32 split of a double: v ~ hi + lo with hi, lo exact tf32 values
+// (error ~2^-24 |v|, the fp32 rounding level)
+__device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
+  hi = dx_tf32_rn((float)v);
+  lo = dx_tf32_rn((float)(v - (double)hi));
 }
 
 __device__ __forceinline__ void dx_mbar_arrive(unsigned long long* bar) {
@@ -104,7 +91,7 @@ __device__ __forceinline__ void dx_mbar_arrive(unsigned long long* bar) {
 // epilogue warps promote both into fp32 registers with round-to-nearest
 // adds.  Accumulators are double-buffered in TMEM (4 x BN columns) so the
 // promotion of chunk c overlaps the MMAs of chunk c+1.
-#define DX_GEMM_CHUNK 4
+#define DX_GEMM_CHUNK 1
 
 // Warps 0-3: epilogue (warp w owns TMEM lanes / tile rows 32w..32w+31);
 // warp 4: TMA producer; warp 5: MMA issuer.  mode 0: C = acc, 1: C += acc.

@@ -58,6 +58,11 @@ static DTy tUnit() { static DTy t = mkT(DType::Unit); return t; }
 static DTy tIdx(DescPtr d) { return mkT(DType::Idx, std::move(d)); }
 static DTy tPair(DTy a, DTy b) { return mkT(DType::Pair, nullptr, std::move(a), std::move(b)); }
 static DTy tTable(DescPtr d, DTy e) { return mkT(DType::Table, std::move(d), std::move(e)); }
+// Type of the table-of-pairs held as a Zip of `depth` table levels.
+static DTy zipTy(const DTy& ta, const DTy& tb, int depth) {
+  if (depth == 0) return tPair(ta, tb);
+  return tTable(ta->desc, zipTy(ta->a, tb->a, depth - 1));
+}
 static DTy tRef(DTy p) { return mkT(DType::Ref, nullptr, std::move(p)); }
 static DTy tSum(DTy a, DTy b) { return mkT(DType::Sum, nullptr, std::move(a), std::move(b)); }
 // Is this core type an index set (Unit, Fin, pairs/sums of index sets)?
@@ -211,11 +216,13 @@ static HV hlookup(const HEnvP& e, const Name& n) {
 
 struct LazyState {
   HV materialized;
+  HV split;  // Zip: cheap components lazy, the rest materialized (splitMaterialize)
 };
 
 struct HVal {
-  enum K { Const, Unit, Pair, Buf, Ref, Lazy } k;
+  enum K { Const, Unit, Pair, Buf, Ref, Lazy, Zip } k;
   DTy ty;
+  int zipDepth = 0;   // Zip: table levels above the pair (a, b: tables of its two halves)
   double f = 0;       // Const Float
   long long i = 0;    // Const Int / Idx ordinal
   HV a, b;            // Pair
@@ -347,8 +354,9 @@ struct LazyK {
 };
 
 struct KVal {
-  enum K { Scalar, Unit, Pair, Table, Ref, Lazy, Sum } k;
+  enum K { Scalar, Unit, Pair, Table, Ref, Lazy, Sum, Zip } k;
   DTy ty;
+  int zipDepth = 0;   // Zip: table levels above the pair (a, b: the two halves)
   std::string e;      // Scalar expression; Sum: tag expression (0 = Left)
   int level = -1;
   bool isConst = false;
@@ -804,6 +812,13 @@ class Lowering {
 
   // Cheap loop bodies are recomputed at every use instead of materialized.
   bool cheapBody(const ExprPtr& body) {
+    // a perfect-nest wrapper `let t = for k. B; t` is as cheap as B per element
+    if (const auto* l = as<ELet>(body)) {
+      const auto* f = as<EFor>(l->bound);
+      const auto* r = as<ERet>(l->body);
+      const auto* rv = r ? as<VVar>(r->value) : nullptr;
+      if (f && rv && rv->name == l->binder && pureBody(f->body)) return cheapBody(f->body);
+    }
     int stmts = 0;
     bool heavy = false;
     std::function<void(const ExprPtr&)> scan = [&](const ExprPtr& e) {
@@ -1166,7 +1181,72 @@ class Lowering {
         return hUnit();
       }
     }
+    if (HV r = hostAccumTables(ref, v)) return r;
     return serialKernel(env, e, annot);
+  }
+
+  // Structurally zero lazy tables (`view i. 0.0`, the zero cotangents of
+  // the pair-of-tables accumulations in transposed programs).
+  static bool zeroBody(const ExprPtr& e) {
+    const auto* r = as<ERet>(e);
+    if (!r) return false;
+    std::function<bool(const ValuePtr&)> zv = [&](const ValuePtr& v) -> bool {
+      if (const auto* f = as<VLitFloat>(v)) return f->v == 0.0;
+      if (const auto* w = as<VView>(v)) return zeroBody(w->body);
+      if (const auto* p = as<VPair>(v)) return zv(p->l) && zv(p->r);
+      return false;
+    };
+    return zv(r->value);
+  }
+
+  // `ref += v` at host level with v a (pair of) device tables: one parallel
+  // add per leaf into the cell (zero views skipped), never a serial kernel.
+  HV hostAccumTables(const HV& ref, const HV& v) {
+    struct Add {
+      size_t leaf;
+      HV src;
+    };
+    std::vector<Add> adds;
+    std::function<bool(const HV&, size_t)> walk = [&](const HV& x, size_t base) -> bool {
+      switch (x->k) {
+        case HVal::Pair: return walk(x->a, base) && walk(x->b, base + numLeaves(x->a->ty));
+        case HVal::Unit: return true;
+        case HVal::Const: return x->ty->k == DType::Float && x->f == 0.0;
+        case HVal::Lazy:
+          if (x->st->materialized) return walk(x->st->materialized, base);
+          if (zeroBody(x->body)) return true;
+          if (!x->ty || x->ty->k != DType::Table) return false;
+          adds.push_back({base, x});
+          return true;
+        case HVal::Buf:
+          if (x->ty->k != DType::Table) return false;
+          adds.push_back({base, x});
+          return true;
+        default: return false;
+      }
+    };
+    if (!walk(v, 0)) return nullptr;
+    for (auto& a : adds) {
+      std::vector<LeafInfo> lv = leaves(a.src->ty);
+      for (size_t l = 0; l < lv.size(); ++l)
+        if (lv[l].kind != SK::F) return nullptr;
+    }
+    cellToDevice(ref->cell);
+    for (auto& a : adds) {
+      HV src = a.src->k == HVal::Lazy ? materialize(a.src) : a.src;
+      std::vector<LeafInfo> lv = leaves(src->ty);
+      for (size_t l = 0; l < lv.size(); ++l) {
+        Step st;
+        st.k = Step::AddBuf;
+        st.buf = cells[ref->cell].bufs[a.leaf + l];
+        st.off = ref->offs[a.leaf + l];
+        st.buf2 = src->bufs[l];
+        st.off2 = src->offs[l];
+        st.elems = lv[l].count;
+        addStep(st);
+      }
+    }
+    return hUnit();
   }
 
   HV hostRunAccum(const HEnvP& env, const ERunAccum& r, const ExprPtr& e) {
@@ -1246,6 +1326,11 @@ class Lowering {
         std::vector<int> b(bufs.begin() + base, bufs.end());
         std::vector<long long> o(offs.begin() + base, offs.end());
         materializeInto(v, b, o);
+        return;
+      }
+      case HVal::Zip: {  // table of pairs: leaves of the first half, then the second
+        copyValueInto(v->a, bufs, offs, sp, base);
+        copyValueInto(v->b, bufs, offs, sp, base + numLeaves(v->a->ty));
         return;
       }
       case HVal::Const: {
@@ -1402,8 +1487,12 @@ class Lowering {
   // Kernel drivers (defined after KGen helpers).
   HV loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool serial, Span sp);
   HV loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs);
-  HV tryGemm(const HV& lz, const std::vector<DescPtr>& dims, const std::vector<Name>& binders, const ExprPtr& body,
-             const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs);
+  HV splitMaterialize(const HV& lz);
+  ValuePtr typeValue(const DTy& t);
+  HV contractNest(const HEnvP& env, const EFor& f, const DescPtr& d);
+  HV contractMaterialize(const HV& lz, const std::vector<DescPtr>& dims, const std::vector<Name>& binders,
+                         const ExprPtr& body, const std::vector<int>* intoBufs,
+                         const std::vector<long long>* intoOffs);
   HV serialKernel(const HEnvP& env, const ExprPtr& e, const ValuePtr& annot);
 
   // ------------------------------------------------------------------
@@ -1500,8 +1589,18 @@ class Lowering {
         }
         return k;
       }
+      case HVal::Zip: {
+        auto k = std::make_shared<KVal>();
+        k->k = KVal::Zip;
+        k->ty = h->ty;
+        k->zipDepth = h->zipDepth;
+        k->a = importHost(g, h->a);
+        k->b = importHost(g, h->b);
+        return k;
+      }
       case HVal::Lazy: {
         if (h->st->materialized) return importHost(g, h->st->materialized);
+        if (h->st->split) return importHost(g, h->st->split);
         auto k = std::make_shared<KVal>();
         k->k = KVal::Lazy;
         k->ty = h->ty;
@@ -1930,6 +2029,18 @@ class Lowering {
       }
       return viewSlots(g, et, slots);
     }
+    if (arr->k == KVal::Zip) {
+      KV ai = indexK(g, s, arr->a, idx, sp), bi = indexK(g, s, arr->b, idx, sp);
+      if (arr->zipDepth <= 1) return kPair(ai, bi);
+      auto k = std::make_shared<KVal>();
+      k->k = KVal::Zip;
+      k->zipDepth = arr->zipDepth - 1;
+      k->ty = arr->ty->a;
+      k->level = std::max(ai->level, bi->level);
+      k->a = ai;
+      k->b = bi;
+      return k;
+    }
     if (arr->k == KVal::Lazy) {
       const auto& lz = arr->lz;
       // uniqueness: every active loop is covered by the lazy's creation
@@ -1945,7 +2056,8 @@ class Lowering {
         if (!cov.count(id)) unique = false;
       if (!unique && !lz->cheap) {
         if (lz->hostOrigin) {
-          HV m = materialize(lz->hostOrigin);
+          HV m = splitMaterialize(lz->hostOrigin);
+          if (!m) m = materialize(lz->hostOrigin);
           return indexK(g, s, importHost(g, m), idx, sp);
         }
         if (!g.matLocal.count(lz->key)) {
@@ -3387,6 +3499,7 @@ HV Lowering::loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool 
     kb.note = "serial loop " + printName(f.binder);
     return requestKernel(kb, true, nullptr, nullptr);
   }
+  if (HV gm = contractNest(env, f, d)) return gm;
   KernelBody kb;
   kb.desc = d;
   kb.dims = {d};
@@ -3426,7 +3539,7 @@ HV Lowering::loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs,
     binders.push_back(inner->binder);
     body = inner->body;
   }
-  if (HV gm = tryGemm(lz, dims, binders, body, intoBufs, intoOffs)) return gm;
+  if (HV gm = contractMaterialize(lz, dims, binders, body, intoBufs, intoOffs)) return gm;
   DescPtr all = dims[0];
   for (size_t i = 1; i < dims.size(); ++i) all = descPair(all, dims[i]);
   // a flattened kernel iterates the pair set; its output layout is the
@@ -3452,191 +3565,211 @@ HV Lowering::loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs,
 }
 
 // ---------------------------------------------------------------------------
-// Dense contractions on the tensor cores.
+// Split materialization of tuple-valued lazy tables.
 //
-// Recognizes the flattened nest the front end produces for `for i k. sum (for
-// j. P.i.j * Q.j.k)` (parser.cpp:697-723 elabSum -> runAccum over `acc +=`):
-//
-//   for i k. let hd = runAccum \h acc. (let t = for j. (..reads..; acc += a*b); ())
-//            let st = snd hd; st
-//
-// where each factor is a 2-level read of a Float matrix indexed by one output
-// dimension and the contraction index j (either order).  It becomes
-// C[M=|i|][N=|k|] = A[M][K] . B[N][K]^T on dx_gemm_tf32x3 (tcgen05, TMEM,
-// TMA): operands stored j-major are transposed once, and the tf32 residuals
-// for 3xTF32 are produced by dx_tf32_lo.  f32 mode, one rank; everything else
-// stays on the generic loop kernels.
-HV Lowering::tryGemm(const HV& lz, const std::vector<DescPtr>& dims, const std::vector<Name>& binders,
-                     const ExprPtr& body, const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs) {
-  if (plan.f64 || plan.world > 1 || dims.size() != 2 || opt.noGemm || std::getenv("DEXLET_NO_GEMM")) return nullptr;
-  const auto* l1 = as<ELet>(body);
-  if (!l1) return nullptr;
-  const auto* ra = as<ERunAccum>(l1->bound);
-  const auto* l2 = as<ELet>(l1->body);
-  if (!ra || !l2) return nullptr;
-  const auto* sn = as<ESnd>(l2->bound);
-  const auto* r2 = as<ERet>(l2->body);
-  if (!sn || !r2) return nullptr;
-  const auto* snv = as<VVar>(sn->v);
-  const auto* rv = as<VVar>(r2->value);
-  if (!snv || snv->name != l1->binder || !rv || rv->name != l2->binder) return nullptr;
-  const Name acc = ra->action.ref;
-  const auto* l3 = as<ELet>(ra->action.body);
-  if (!l3) return nullptr;
-  const auto* fj = as<EFor>(l3->bound);
-  if (!fj || !as<ERet>(l3->body)) return nullptr;
-  DescPtr dj;
-  try {
-    dj = resolveDesc(fj->annot, hostLook(lz->env));
-  } catch (const DexError&) {
-    return nullptr;
-  }
-  // symbolic walk of the j body: reads base.(idx...) and one product
-  struct Sym {
-    int kind = 0;  // 0 read, 1 product, 2 effect
-    HV base;
-    std::vector<int> idx;
-    std::shared_ptr<Sym> a, b;
-  };
-  std::map<Name, Sym> syms;
-  auto loopVar = [&](const ValuePtr& v) -> int {
-    const auto* vv = as<VVar>(v);
-    if (!vv) return -1;
-    if (vv->name == binders[0]) return 0;
-    if (vv->name == binders[1]) return 1;
-    if (vv->name == fj->binder) return 2;
-    return -1;
-  };
-  std::shared_ptr<Sym> prod;
-  ExprPtr cur = fj->body;
-  while (const auto* l = as<ELet>(cur)) {
-    Sym s;
-    if (const auto* ix = as<EIndex>(l->bound)) {
-      int lv = loopVar(ix->idx);
-      const auto* av = as<VVar>(ix->arr);
-      if (lv < 0 || !av) return nullptr;
-      auto it = syms.find(av->name);
-      if (it != syms.end()) {
-        if (it->second.kind != 0) return nullptr;
-        s = it->second;
-      } else {
-        HV h = hlookup(lz->env, av->name);
-        if (!h || (h->k != HVal::Buf && h->k != HVal::Lazy)) return nullptr;
-        s.base = h;
-      }
-      s.idx.push_back(lv);
-    } else if (const auto* bo = as<EBinOp>(l->bound)) {
-      const auto* x = as<VVar>(bo->l);
-      const auto* y = as<VVar>(bo->r);
-      if (bo->op != BinOp::Mul || !x || !y || !syms.count(x->name) || !syms.count(y->name)) return nullptr;
-      const Sym &sx = syms[x->name], &sy = syms[y->name];
-      if (sx.kind != 0 || sy.kind != 0 || sx.idx.size() != 2 || sy.idx.size() != 2) return nullptr;
-      s.kind = 1;
-      s.a = std::make_shared<Sym>(sx);
-      s.b = std::make_shared<Sym>(sy);
-    } else if (const auto* rt = as<ERet>(l->bound)) {
-      const auto* v = as<VVar>(rt->value);
-      if (!v || !syms.count(v->name)) return nullptr;
-      s = syms[v->name];
-    } else if (const auto* ac = as<EAccum>(l->bound)) {
-      const auto* r = as<VVar>(ac->ref);
-      const auto* v = as<VVar>(ac->value);
-      if (!r || r->name != acc || !v || !syms.count(v->name) || syms[v->name].kind != 1 || prod) return nullptr;
-      prod = std::make_shared<Sym>(syms[v->name]);
-      s.kind = 2;
-    } else {
-      return nullptr;
+// LinFor (autodiff.cpp:230-255) turns every forward loop into a tape whose
+// elements pair the primal with its partials, e.g. per (bb, h2) of the MLP
+// `(for ii. (x, (w1, x*w1)), (z, z*z))`.  Materializing such a table stores
+// the cheap inner triples (B*H*I of them: 100 GB at the MLP config) only to
+// read back values recomputable from the inputs.  Instead the element tuple
+// is split: components cheap to recompute stay a lazy projection (inlined at
+// each use), the others are materialized as their own table (where the
+// contraction lowering can pick them up).  The result is a Zip: the table of
+// pairs held as a pair of tables over the same index levels.
+ValuePtr Lowering::typeValue(const DTy& t) {
+  if (!t) return nullptr;
+  switch (t->k) {
+    case DType::Float: return vBase(BaseKind::Float);
+    case DType::Int: return vBase(BaseKind::Int);
+    case DType::Unit: return vBase(BaseKind::Unit);
+    case DType::Pair: {
+      ValuePtr a = typeValue(t->a), b = typeValue(t->b);
+      return a && b ? vPairType(a, b) : nullptr;
     }
-    syms[l->binder] = s;
+    case DType::Table: {
+      ValuePtr e = typeValue(t->a);
+      if (!e || t->desc->kind != IndexSetDesc::Kind::Fin) return nullptr;
+      return vArray(vFin(vInt(size(t->desc))), e);
+    }
+    default: return nullptr;
+  }
+}
+
+HV Lowering::splitMaterialize(const HV& lz) {
+  if (lz->k != HVal::Lazy) return nullptr;
+  if (lz->st->split) return lz->st->split;
+  if (opt.noFusion || std::getenv("DEXLET_NO_SPLIT")) return nullptr;
+  // the perfect nest (as loopKernelLazy flattens it)
+  std::vector<const ELet*> wraps;
+  std::vector<const EFor*> fors;
+  std::vector<DescPtr> descs = {lz->desc};
+  ExprPtr body = lz->body;
+  while (true) {
+    const auto* l = as<ELet>(body);
+    if (!l) break;
+    const auto* inner = as<EFor>(l->bound);
+    const auto* ret = as<ERet>(l->body);
+    if (!inner || !ret) break;
+    const auto* rv = as<VVar>(ret->value);
+    if (!rv || rv->name != l->binder || !pureBody(inner->body)) break;
+    DescPtr d2;
+    try {
+      d2 = resolveDesc(inner->annot, hostLook(lz->env));
+    } catch (const DexError&) {
+      break;
+    }
+    wraps.push_back(l);
+    fors.push_back(inner);
+    descs.push_back(d2);
+    body = inner->body;
+  }
+  std::vector<const ELet*> chain;
+  ExprPtr cur = body;
+  while (const auto* l = as<ELet>(cur)) {
+    chain.push_back(l);
     cur = l->body;
   }
-  if (!prod || !as<ERet>(cur)) return nullptr;
-  auto uses = [](const Sym& f, int d) { return f.idx[0] == d || f.idx[1] == d; };
-  std::shared_ptr<Sym> P = prod->a, Q = prod->b;
-  if (!(uses(*P, 0) && uses(*P, 2))) std::swap(P, Q);
-  if (!(uses(*P, 0) && uses(*P, 2) && uses(*Q, 1) && uses(*Q, 2))) return nullptr;
-  const long long M = size(dims[0]), N = size(dims[1]), K = size(dj);
-  if (M <= 0 || N <= 0 || K <= 0 || K % 4 != 0 || M > (1LL << 31) || N > (1LL << 31)) return nullptr;
-  auto operand = [&](const Sym& f) -> std::pair<int, long long> {
-    HV h = f.base->k == HVal::Lazy ? materialize(f.base) : f.base;
-    if (h->k != HVal::Buf || h->bufs.size() != 1 || plan.bufs[h->bufs[0]].kind != SK::F) return {-1, 0};
-    return {h->bufs[0], h->offs[0]};
-  };
-  auto [pb, po] = operand(*P);
-  auto [qb, qo] = operand(*Q);
-  if (pb < 0 || qb < 0) return nullptr;
-  plan.gemm = true;
-  auto kstep = [&](const std::string& name, int threads, int smem, long long grid, std::vector<KArg> args,
-                   const std::string& note) {
-    Step st;
-    st.k = Step::Kernel;
-    st.name = name;
-    st.threads = threads;
-    st.smem = smem;
-    st.fixedGrid = grid;
-    st.total = grid;
-    st.args = std::move(args);
-    st.note = note;
-    addStep(st);
-    plan.numKernels++;
-  };
-  auto bufArg = [](int b, long long off) { KArg a; a.k = KArg::Buf; a.buf = b; a.off = off; return a; };
-  auto intArg = [](long long v) { KArg a; a.k = KArg::I64; a.i = v; return a; };
-  // K-major operand [rows][K]: direct when stored that way and 16-byte aligned, else transposed
-  auto kmajor = [&](const Sym& f, int b, long long off, long long rows, int outDim) -> std::pair<int, long long> {
-    if (f.idx[0] == outDim && off % 4 == 0) return {b, off};
-    int t = newBuf(BufDecl::Temp, SK::F, rows * K);
-    if (f.idx[0] == outDim) {
-      Step c; c.k = Step::CopyBuf; c.buf = t; c.buf2 = b; c.off2 = off; c.elems = rows * K; addStep(c);
-    } else {
-      kstep("dx_transpose_f32", 256, 0, ((K + 31) / 32) * ((rows + 31) / 32),
-            {bufArg(b, off), bufArg(t, 0), intArg(K), intArg(rows)}, "transpose gemm operand");
-    }
-    return {t, 0};
-  };
-  auto [ab, ao] = kmajor(*P, pb, po, M, 0);
-  auto [bb, bo] = kmajor(*Q, qb, qo, N, 1);
-  auto lo = [&](int b, long long off, long long n) {
-    int t = newBuf(BufDecl::Temp, SK::F, n);
-    kstep("dx_tf32_lo", 256, 0, std::min<long long>((n + 255) / 256, 148 * 16),
-          {bufArg(b, off), bufArg(t, 0), intArg(n)}, "tf32 residual");
-    return t;
-  };
-  int al = lo(ab, ao, M * K), bl = lo(bb, bo, N * K);
-  int cb;
-  long long co = 0;
-  if (intoBufs) {
-    cb = (*intoBufs)[0];
-    co = (*intoOffs)[0];
-  } else {
-    cb = newBuf(BufDecl::Output, SK::F, M * N);
+  const auto* rt = as<ERet>(cur);
+  if (!rt || !as<VPair>(rt->value)) return nullptr;
+  DTy et = lz->ty;
+  for (size_t i = 0; i < descs.size(); ++i) {
+    if (!et || et->k != DType::Table) return nullptr;
+    et = et->a;
   }
-  auto tmap = [&](int b, long long off, long long rows) {
-    KArg a;
-    a.k = KArg::TMap;
-    a.buf = b;
-    a.off = off;
-    a.rowLen = K;
-    a.rows = rows;
-    a.boxRows = rows >= 128 ? 128 : 128;  // partial tiles: TMA zero-fills out-of-range rows
-    a.boxCols = 32;
-    a.swizzle = 128;
-    return a;
+  if (!et || et->k != DType::Pair) return nullptr;
+  std::map<Name, const ELet*> defs;
+  for (const ELet* l : chain) defs[l->binder] = l;
+  std::map<Name, bool> memo;
+  std::function<bool(const Name&)> cheapName = [&](const Name& n) -> bool {
+    auto d = defs.find(n);
+    if (d == defs.end()) return true;  // binder or outer value
+    auto m = memo.find(n);
+    if (m != memo.end()) return m->second;
+    memo[n] = false;
+    const ExprPtr& b = d->second->bound;
+    bool ok;
+    if (const auto* f = as<EFor>(b)) ok = pureBody(f->body) && cheapBody(f->body);
+    else ok = !as<ERunAccum>(b) && !as<ERunState>(b) && !as<ECase>(b) && !as<EApp>(b);
+    if (ok)
+      for (const Name& fv : freeVars(b))
+        if (!cheapName(fv)) ok = false;
+    memo[n] = ok;
+    return ok;
   };
-  const int BN = 128, STAGES = 3;
-  KArg tb = tmap(bb, bo, N), tbl = tmap(bl, 0, N);
-  tb.boxRows = tbl.boxRows = BN;
-  kstep("dx_gemm_tf32x3_n128", 192, STAGES * (2 * 128 * 128 + 2 * BN * 128) + 1024, ((M + 127) / 128) * ((N + BN - 1) / BN),
-        {tmap(ab, ao, M), tmap(al, 0, M), tb, tbl, intArg(M), intArg(N), intArg(K), bufArg(cb, co), intArg(N), intArg(0)},
-        "tcgen05 gemm " + std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K) + " (materialize " +
-            printName(lz->binder) + ")");
-  auto h = std::make_shared<HVal>();
-  h->k = HVal::Buf;
-  h->ty = tTable(dims[0], tTable(dims[1], tFloat()));
-  h->bufs = {cb};
-  h->offs = {co};
-  return h;
+  auto cheapVal = [&](const ValuePtr& v) {
+    for (const Name& fv : freeVars(v))
+      if (!cheapName(fv)) return false;
+    return true;
+  };
+  std::function<bool(const ValuePtr&)> anyCheap = [&](const ValuePtr& v) -> bool {
+    if (const auto* p = as<VPair>(v)) return anyCheap(p->l) || anyCheap(p->r);
+    return cheapVal(v);
+  };
+  std::function<bool(const ValuePtr&)> allCheap = [&](const ValuePtr& v) -> bool {
+    if (const auto* p = as<VPair>(v)) return allCheap(p->l) && allCheap(p->r);
+    return cheapVal(v);
+  };
+  // Table-valued components whose own elements are mixed tuples (a tape of
+  // tapes, e.g. matmul `for i. (for k. (for j. (x, (y, x*y)), sum_j), sum_k)`)
+  // are split recursively first; the other projections then read the split
+  // (bound to a fresh name) instead of recomputing it.
+  std::map<Name, HV> shared;
+  std::map<Name, Name> sharedName;
+  const int depth = (int)descs.size();
+  std::function<bool(const ValuePtr&)> tupleTable = [&](const ValuePtr& v) -> bool {
+    const auto* x = as<VVar>(v);
+    if (!x || !defs.count(x->name)) return false;
+    const auto* f = as<EFor>(defs[x->name]->bound);
+    if (!f || !pureBody(f->body) || cheapName(x->name)) return false;
+    ExprPtr c = f->body;
+    while (const auto* l = as<ELet>(c)) c = l->body;
+    const auto* r = as<ERet>(c);
+    return r && as<VPair>(r->value);
+  };
+  std::function<bool(const ValuePtr&)> hasTupleTable = [&](const ValuePtr& v) -> bool {
+    if (const auto* p = as<VPair>(v)) return hasTupleTable(p->l) || hasTupleTable(p->r);
+    return tupleTable(v);
+  };
+  if ((!anyCheap(rt->value) && !hasTupleTable(rt->value)) || allCheap(rt->value)) return nullptr;
+  HEnvP penv = lz->env;
+  auto projection = [&](const ValuePtr& v, const DTy& vty, bool mat) -> HV {
+    ExprPtr inner = eRet(v);
+    NameSet need = freeVars(v);
+    for (auto it = chain.rbegin(); it != chain.rend(); ++it) {
+      const ELet* l = *it;
+      if (!need.count(l->binder)) continue;
+      auto sh = sharedName.find(l->binder);
+      if (sh != sharedName.end()) {
+        // let t = Z.b0.b1...  (the recursive split of this component)
+        std::vector<Name> bs = {lz->binder};
+        for (auto* f : fors) bs.push_back(f->binder);
+        std::vector<Name> tmp;
+        for (size_t i = 0; i < bs.size(); ++i) tmp.push_back(NameSupply::fresh("zip"));
+        inner = eLet(l->binder, l->annot, eRet(vVar(tmp.back())), inner);
+        for (size_t i = bs.size(); i-- > 0;)
+          inner = eLet(tmp[i], nullptr, eIndex(vVar(i == 0 ? sh->second : tmp[i - 1]), vVar(bs[i])), inner);
+        continue;
+      }
+      inner = eLet(l->binder, l->annot, l->bound, inner);
+      for (const Name& n : freeVars(l->bound)) need.insert(n);
+    }
+    DTy ty = vty;
+    for (size_t i = fors.size(); i-- > 0;) {
+      ty = tTable(descs[i + 1], ty);
+      inner = eLet(wraps[i]->binder, typeValue(ty), eFor(fors[i]->binder, fors[i]->annot, inner),
+                   eRet(vVar(wraps[i]->binder)));
+    }
+    auto h = std::make_shared<HVal>(*lz);
+    h->body = inner;
+    h->ty = tTable(lz->desc, ty);
+    h->env = penv;
+    h->cheap = cheapBody(inner);
+    h->st = std::make_shared<LazyState>();
+    return mat ? materialize(h) : HV(h);
+  };
+  // recursive splits of tuple-valued table components (before their readers)
+  std::function<void(const ValuePtr&, const DTy&)> pre = [&](const ValuePtr& v, const DTy& vty) {
+    if (const auto* p = as<VPair>(v)) {
+      if (vty->k != DType::Pair) return;
+      pre(p->l, vty->a);
+      pre(p->r, vty->b);
+      return;
+    }
+    if (!tupleTable(v)) return;
+    const Name& t = as<VVar>(v)->name;
+    if (shared.count(t)) return;
+    HV P = projection(v, vty, false);
+    HV S = splitMaterialize(P);
+    if (!S) S = materialize(P);
+    shared[t] = S;
+    Name z = NameSupply::fresh("zip");
+    sharedName[t] = z;
+    penv = hbind(penv, z, S);
+  };
+  pre(rt->value, et);
+  std::function<HV(const ValuePtr&, const DTy&)> split = [&](const ValuePtr& v, const DTy& vty) -> HV {
+    if (const auto* x = as<VVar>(v))
+      if (shared.count(x->name)) return shared[x->name];
+    if (allCheap(v)) return projection(v, vty, false);
+    const auto* p = as<VPair>(v);
+    if (p && (anyCheap(v) || hasTupleTable(v)) && vty->k == DType::Pair) {
+      HV a = split(p->l, vty->a), b = split(p->r, vty->b);
+      auto z = std::make_shared<HVal>();
+      z->k = HVal::Zip;
+      z->zipDepth = depth;
+      z->a = a;
+      z->b = b;
+      z->ty = zipTy(a->ty, b->ty, depth);
+      return z;
+    }
+    return projection(v, vty, true);
+  };
+  HV r = split(rt->value, et);
+  lz->st->split = r;
+  return r;
 }
+
+#include "contract.inc"
 
 HV Lowering::serialKernel(const HEnvP& env, const ExprPtr& e, const ValuePtr& annot) {
   KernelBody kb;
@@ -3735,6 +3868,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
         return;
       }
       case HVal::Lazy: out(L.materialize(v)); return;
+      case HVal::Zip: out(L.materialize(v->a)); out(L.materialize(v->b)); return;
       case HVal::Ref: notLowerable("reference escaping the program");
     }
   };
@@ -3781,7 +3915,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
   for (size_t b = 0; b < L.plan.bufs.size(); ++b)
     if (!live[b]) L.plan.bufs[b].elems = -1;  // not allocated
   L.plan.steps = std::move(kept);
-  if (L.plan.gemm) L.plan.source += std::string("\n") + dxrt::gemmSource();
+  if (L.plan.gemm) L.plan.source = std::string(dxrt::gemmSource()) + "\n" + L.plan.source;
   return std::move(L.plan);
 }
 

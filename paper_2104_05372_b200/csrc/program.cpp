@@ -182,6 +182,7 @@ int Program::prepare() {
     if ((rc = dxrt::check(cuModuleGetFunction(&finFn[k], mod, fz[k]), "finalize fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[0], mod, "dx_add_f32"), "add fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&addFn[1], mod, "dx_add_f64"), "add fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&addFn[2], mod, "dx_add_f64_f32"), "add fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&finF32D, mod, "dx_fin_f32d"), "finalize fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[0], mod, "dx_cvt_f32_f64"), "cvt fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[1], mod, "dx_cvt_f64_f32"), "cvt fn"))) return rc;
@@ -386,11 +387,12 @@ int Program::issue() {
         break;
       }
       case Step::AddBuf: {
-        CUdeviceptr c = devptr[s.buf], src = devptr[s.buf2];
+        const size_t ec = storageBytes(plan.bufs[s.buf].kind, f64), esrc = storageBytes(plan.bufs[s.buf2].kind, f64);
+        CUdeviceptr c = devptr[s.buf] + s.off * ec, src = devptr[s.buf2] + s.off2 * esrc;
         long long n = s.elems;
         void* args[3] = {&c, &src, &n};
-        const bool dk = f64 || plan.bufs[s.buf].kind == SK::D;
-        if ((rc = launch(addFn[dk ? 1 : 0], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args)))
+        const int fn = ec == 4 ? 0 : esrc == 8 ? 1 : 2;
+        if ((rc = launch(addFn[fn], (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args)))
           return rc;
         ++launches;
         break;

@@ -37,7 +37,7 @@ struct Program {
   std::vector<std::pair<long long, long long>> ranges;
   std::vector<std::vector<char>> staging;
   CUfunction finFn[4] = {};
-  CUfunction addFn[2] = {};
+  CUfunction addFn[3] = {};  // f32 += f32, f64 += f64, f64 += f32
   CUfunction finF32D = nullptr;
   CUfunction cvtFn[2] = {};
   int launches = 0;

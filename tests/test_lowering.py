@@ -94,17 +94,27 @@ def test_sharded_plan_allreduces_cells():
 
 
 def test_contraction_recognized_as_gemm():
-    """`for i l. sum for j. x*y` lowers to the tcgen05 GEMM in f32 mode, with a
-    transpose only for operands stored j-major; f64 parity mode and K % 4 != 0
-    keep the generic loop kernel."""
-    p = dx.Program(P.contraction(200, 136, 68, True, False), ctx=None).plan
-    assert "tcgen05 gemm 200x136x68" in p and p.count("dx_transpose_f32") == 1
-    p = dx.Program(P.contraction(64, 64, 64, True, True), ctx=None).plan
-    assert "tcgen05 gemm" in p and "dx_transpose_f32" not in p
-    p = dx.Program(P.contraction(64, 64, 64, False, False), ctx=None).plan
-    assert p.count("dx_transpose_f32") == 2
+    """`for i l. sum for j. x*y` lowers to operand prologues + the tcgen05 GEMM
+    in f32 mode whatever the operands' storage order; f64 parity mode keeps
+    the generic loop kernel."""
+    for xk, yk in ((True, False), (False, True), (False, False), (True, True)):
+        p = dx.Program(P.contraction(200, 136, 68, xk, yk), ctx=None).plan
+        assert "tcgen05 gemm 200x136x68" in p and p.count("gemm operand") == 2, p
+    p = dx.Program(P.contraction(64, 64, 6), ctx=None).plan      # K padded to 8 in the operands
+    assert "tcgen05 gemm 64x64x6" in p
+    assert "tcgen05" not in dx.Program(P.contraction(64, 64, 64), ctx=None, float64=True).plan
     src = dx.Program(P.contraction(64, 64, 64), ctx=None).source
     sass = _sass(src)
     assert "UTCHMMA" in sass and "UTMALDG.2D" in sass and "LDTM" in sass  # tcgen05.mma, TMA, tcgen05.ld
-    assert "tcgen05" not in dx.Program(P.contraction(64, 64, 64), ctx=None, float64=True).plan
-    assert "tcgen05" not in dx.Program(P.contraction(64, 64, 6), ctx=None).plan
+
+
+def test_mlp_and_matmul_grad_on_tensor_cores():
+    """The AD programs: every contraction of the forward tape and of the
+    transposed loops is a GEMM (MLP: Z = XW1, Y = HW2, dH, dW2, dW1); the AoS
+    tapes are split, never materialized whole."""
+    p = dx.Program(P.mlp_grad(8192, 1024, 1024, 1024), ctx=None).plan
+    assert p.count("tcgen05 gemm") == 5, p
+    assert p.count("(+=)") == 3
+    assert "8589934592" not in p  # no B*H*I tape
+    p = dx.Program(P.matmul_grad(256), ctx=None).plan
+    assert p.count("tcgen05 gemm") == 2, p
