@@ -117,6 +117,23 @@ _sig("dxl_program_enable_kernel_timing", ctypes.c_int, _vp, ctypes.c_int)
 _sig("dxl_program_kernel_times", ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int, _ip)
 _sig("dxl_program_kernel_names", ctypes.c_char_p, _vp)
 _sig("dxc_l2_flush", ctypes.c_int, _vp, ctypes.c_size_t)
+_f32p = ctypes.POINTER(ctypes.c_float)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_sig("dxg_gmm_create", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+     ctypes.POINTER(_vp))
+_sig("dxg_gmm_destroy", ctypes.c_int, _vp)
+_sig("dxg_gmm_set_params", ctypes.c_int, _vp, _vp, _vp, _vp)
+_sig("dxg_gmm_set_points", ctypes.c_int, _vp, _vp)
+_sig("dxg_gmm_input_device_ptrs", ctypes.c_int, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+     ctypes.POINTER(_vp), ctypes.POINTER(_vp))
+_sig("dxg_gmm_run", ctypes.c_int, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int)
+_sig("dxg_gmm_get", ctypes.c_int, _vp, _vp, _vp, _vp, _vp)
+_sig("dxg_gmm_objective", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, _vp,
+     ctypes.c_double, ctypes.c_int, _vp)
+_sig("dxg_gmm_objective_grad", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp,
+     _vp, ctypes.c_double, ctypes.c_int, _vp, _vp)
+_sig("dxg_gmm_enable_timing", ctypes.c_int, _vp, ctypes.c_int)
+_sig("dxg_gmm_kernel_times", ctypes.c_int, _vp, _f32p, ctypes.c_int, _ip)
 
 #: every symbol declared in include/dexlet_cuda.h
 ABI_SYMBOLS = [
@@ -133,6 +150,14 @@ ABI_SYMBOLS = [
     "dxc_desc_reverse", "dxc_chunk_range", "dxc_l2_flush", "dxl_program_enable_kernel_timing",
     "dxl_program_kernel_times", "dxl_program_kernel_names",
 ]
+#: every symbol declared in include/dexlet_gmm.h
+GMM_ABI_SYMBOLS = [
+    "dxg_gmm_create", "dxg_gmm_destroy", "dxg_gmm_set_params", "dxg_gmm_set_points",
+    "dxg_gmm_input_device_ptrs", "dxg_gmm_run", "dxg_gmm_get", "dxg_gmm_objective",
+    "dxg_gmm_objective_grad", "dxg_gmm_enable_timing", "dxg_gmm_kernel_times",
+]
+GMM_KERNELS = ["dx_gmm_absmax", "dx_gmm_prep_q", "dx_gmm_prep_x", "dx_gmm_fwd", "dx_gmm_lse", "dx_gmm_sum", "dx_gmm_bwd",
+               "dx_gmm_moments", "dx_gmm_finish"]
 
 
 def _check(rc: int):
@@ -343,3 +368,71 @@ class Program:
         for l, (k, c) in enumerate(self.output_leaves()):
             res.append(self.get_output(l, DXC_F64 if k == LEAF_FLOAT else DXC_I64))
         return res
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+class GMM:
+    """Fused GMM objective + gradient on the device (include/dexlet_gmm.h):
+    ADBench's ``gmm_objective(d, k, n, alphas, means, icf, x, wishart, err)``
+    and its gradient, d = 64, fp32 inputs, fp64 results.  ``n_global`` is the
+    total point count when this rank holds a contiguous shard of the points."""
+
+    def __init__(self, ctx: Context, d: int, k: int, n: int, n_global: Optional[int] = None):
+        h = _vp()
+        _check(_lib.dxg_gmm_create(ctx.handle, d, k, n, n if n_global is None else n_global, ctypes.byref(h)))
+        self.handle, self.ctx, self.d, self.k, self.n = h, ctx, d, k, n
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _lib.dxg_gmm_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def set_params(self, alphas, means, icf):
+        self._keep = [np.ascontiguousarray(a, dtype=np.float32) for a in (alphas, means, icf)]
+        _check(_lib.dxg_gmm_set_params(self.handle, *(_ptr(a) for a in self._keep)))
+
+    def set_points(self, x):
+        self._x = np.ascontiguousarray(x, dtype=np.float32)
+        _check(_lib.dxg_gmm_set_points(self.handle, _ptr(self._x)))
+
+    def set_params_ptr(self, alphas: int, means: int, icf: int):
+        _check(_lib.dxg_gmm_set_params(self.handle, _vp(alphas), _vp(means), _vp(icf)))
+
+    def set_points_ptr(self, x: int):
+        _check(_lib.dxg_gmm_set_points(self.handle, _vp(x)))
+
+    def run(self, gamma: float = 1.0, m: int = 0, grad: bool = True):
+        _check(_lib.dxg_gmm_run(self.handle, gamma, m, 1 if grad else 0))
+
+    def enable_timing(self, on: bool = True):
+        _check(_lib.dxg_gmm_enable_timing(self.handle, 1 if on else 0))
+
+    def kernel_times(self):
+        arr = (ctypes.c_float * 16)()
+        n = ctypes.c_int()
+        _check(_lib.dxg_gmm_kernel_times(self.handle, arr, 16, ctypes.byref(n)))
+        return [(GMM_KERNELS[i], arr[i]) for i in range(n.value)]
+
+    def get(self, grad: bool = True):
+        err = np.zeros(1)
+        if not grad:
+            _check(_lib.dxg_gmm_get(self.handle, _ptr(err), None, None, None))
+            return float(err[0])
+        icf_sz = self.d * (self.d + 1) // 2
+        da = np.empty(self.k)
+        dm = np.empty((self.k, self.d))
+        di = np.empty((self.k, icf_sz))
+        _check(_lib.dxg_gmm_get(self.handle, _ptr(err), _ptr(da), _ptr(dm), _ptr(di)))
+        return float(err[0]), da, dm, di
+
+    def __call__(self, alphas, means, icf, x, gamma: float = 1.0, m: int = 0, grad: bool = True):
+        self.set_params(alphas, means, icf)
+        self.set_points(x)
+        self.run(gamma, m, grad)
+        return self.get(grad)

@@ -374,6 +374,77 @@ __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* 
   __syncthreads();
 }
 
+// Warp-private row table (WarpTab).  The warp's 32 rows were stored by
+// dx_tile_store4 at etile rows 32*warp .. 32*warp+31; they are added, lanes
+// over columns, G = 32/D rows per step, into a table of K+1 rows x 32 words
+// holding G interleaved copies (copy g in columns g*D .. g*D+D-1; row K takes
+// rows without a key).  Every step touches 32 distinct banks and each word has
+// one writer, so the adds are plain LDS/FADD/STS with no atomics, no
+// collisions and no block barrier.  Order is fixed: ascending row within the
+// warp, copies folded in order by dx_warp_tab_flush.
+template <int D, int K, int FWD = 1>
+__device__ __forceinline__ void dx_warp_tab(const float* etile, int key, float* tab) {
+  static_assert(D >= 4 && D <= 32 && (32 % D) == 0, "WarpTab row width");
+  constexpr int G = 32 / D, NB = D / 4;
+  const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
+  const int g = lane / D, c = lane % D;
+  const int k = key < 0 ? K : key;
+  __syncwarp();
+  if constexpr (!FWD) {
+  float* tl = tab + g * D + c;
+#pragma unroll
+  for (int s = 0; s < 32 / G; ++s) {
+    const int r = s * G + g;
+    const int t = wbase + r;
+    const float v = etile[t * D + ((((c >> 2) ^ ((t >> 1) & (NB - 1)))) << 2) + (c & 3)];
+    const int kr = __shfl_sync(DX_FULL, k, r);
+    tl[kr * 32] += v;
+  }
+  } else {
+  // Software-pipelined read-modify-write: the load of step s+1 is issued
+  // before the store of step s (ordered volatile shared accesses), and when
+  // both steps hit the same word the value just computed is forwarded.  Any
+  // older step's store precedes the load in program order.
+  constexpr int S = 32 / G;
+  const unsigned base = dx_smem_addr(tab + g * D + c);
+  float v[S];
+  unsigned a[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int r = s * G + g;
+    const int t = wbase + r;
+    v[s] = etile[t * D + ((((c >> 2) ^ ((t >> 1) & (NB - 1)))) << 2) + (c & 3)];
+    a[s] = base + (unsigned)__shfl_sync(DX_FULL, k, r) * 128u;
+  }
+  float cur;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(cur) : "r"(a[0]) : "memory");
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    float nxt = 0.f;
+    if (s + 1 < S) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nxt) : "r"(a[(s + 1) % S]) : "memory");
+    const float val = cur + v[s];
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a[s]), "f"(val) : "memory");
+    if (s + 1 < S) cur = a[(s + 1) % S] == a[s] ? val : nxt;
+  }
+  }
+}
+// Block partial of NW warp tables: entry (k, j) = sum over warps, then copies,
+// in that fixed order.
+template <int D, int K, int NW>
+__device__ __forceinline__ void dx_warp_tab_flush(const float* tabs, float* part) {
+  constexpr int G = 32 / D;
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * D; e += blockDim.x) {
+    const int k = e / D, j = e - (e / D) * D;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+#pragma unroll
+      for (int g = 0; g < G; ++g) s += tabs[(w * (K + 1) + k) * 32 + g * D + j];
+    part[e] = s;
+  }
+}
+
 // Block partial of a dx_tile_rows4 table: splits folded in fixed order.
 template <int D, int K, int NT>
 __device__ __forceinline__ void dx_tile_rows4_flush(float* scratch, const float4& acc, float* part) {

@@ -1,0 +1,859 @@
+// dx_gmm.cuh — fused GMM objective + gradient (BASELINE configs[2]; the
+// "fused GMM" kernel class of SURVEY.md §7, item 6) on sm_100a tensor cores.
+//
+// Objective (ADBench gmm_objective, restated in oracle/gmm.py):
+//   beta[k][i] = alpha_k + sum(q_k) - 0.5 || Q_k (x_i - mu_k) ||^2
+//   err = CONST + sum_i logsumexp_k beta[k][i] - n lse(alpha) + wishart prior
+// Gradient through the responsibilities g_ik = exp(beta[k][i] - lse_i):
+//   W_k = sum_i g_ik and the centred moments sum_i g_ik (x_i - mu_k) and
+//   sum_i g_ik (x_i - mu_k) x_i^T
+// from which the per-component d alpha, d mu, d Q follow in closed form
+// (dx_gmm_finish).  Both O(n K d^2) contractions run on tcgen05 (kind::f16,
+// FP16 operands, FP32 accumulators in TMEM) in "fp16x3": every fp32 operand
+// is a pair hi + lo of fp16 values (11-bit significands: the pair carries ~22
+// bits) and the MMA accumulates hi*hi + hi*lo + lo*hi, an error of ~2^-22
+// relative per product.  (bf16x3 carries only ~16 bits: its error in
+// ||Q (x - mu)||^2 moves beta by ~1e-3 and the responsibilities with it.)
+// fp16's range is handled by exact power-of-two scales: one for the points
+// (from their max |x|, dx_gmm_absmax) and one per component for Q_k.
+//
+//   dx_gmm_absmax  max |x| over the points (their power-of-two scale)
+//   dx_gmm_prep_q  per component: Q_k split into hi/lo SW128 K-major smem
+//                  images (B operand), b_k = Q_k mu_k, c_k = alpha_k + sum q_k
+//   dx_gmm_prep_x  points: X hi/lo images, 128-point tiles (forward A operand)
+//                  and X^T hi/lo images, 64-point chunks (backward B operand)
+//   dx_gmm_fwd     Y = X Q^T for 8 resident components per CTA; the epilogue
+//                  reduces each 64-column block to beta (never stores Y);
+//                  the MMAs carry the strictly lower L_k, the diagonal of Q_k
+//                  is applied in fp32 in the epilogue
+//   dx_gmm_lse     lse_i over the K betas of each point, sum_i lse_i
+//   dx_gmm_bwd     per component pair: D[(k,b)][a] = sum_i g_ik x_ib x_ia
+//                  (a < 64) and D[(k,b)][64] = m_kb, with the A operand
+//                  g * X^T produced in shared memory by SIMT warps; W_k by
+//                  warp reductions
+//   dx_gmm_finish  fp64 per component: moments -> gradients, prior, err
+// The whole objective+gradient is deterministic: every reduction has a fixed
+// order (per-CTA contiguous work ranges, partial slots folded in CTA order).
+//
+// Sizes: d = 64 is compiled in (DXG_D); n and K are runtime.
+
+#define DXG_D 64
+#define DXG_ICF (DXG_D * (DXG_D + 1) / 2)
+#define DXG_GC 8                 // components resident per forward CTA
+#define DXG_TM 128               // points per forward tile (MMA M)
+#define DXG_BC 64                // points per backward chunk (MMA K extent)
+#define DXG_BN 80                // backward MMA N: 64 dims + ones row + 15 zero rows
+#define DXG_PROMO 1              // backward chunks per TMEM promotion (fp32 registers)
+#define DXG_F64_EVERY 16         // promotions per fp64 spill (shared memory)
+#define DXG_FMAX 4               // backward partial slots per CTA
+#define DXG_FIN_SMEM (2 * DXG_D * (DXG_D + 1) * 8)
+
+// ---- shared helpers ----------------------------------------------------------
+// byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
+// rows are 128 bytes (64 bf16): 16-byte chunk index XOR (row & 7)
+__device__ __forceinline__ unsigned dxg_sw(unsigned row, unsigned col) {
+  return row * 128u + ((((col >> 3) ^ (row & 7u)) & 7u) << 4) + (col & 7u) * 2u;
+}
+// fp16 halves of a packed f16x2 word, as floats
+__device__ __forceinline__ float dxg_h_lo(unsigned w) {
+  float f;
+  asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; cvt.f32.f16 %0, l; }" : "=f"(f) : "r"(w));
+  return f;
+}
+__device__ __forceinline__ float dxg_h_hi(unsigned w) {
+  float f;
+  asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; cvt.f32.f16 %0, h; }" : "=f"(f) : "r"(w));
+  return f;
+}
+// split two floats into packed f16x2 hi and lo words (x0 in the low half)
+__device__ __forceinline__ void dxg_split2(float x0, float x1, unsigned& hi, unsigned& lo) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(x1 - dxg_h_hi(hi)), "f"(x0 - dxg_h_lo(hi)));
+}
+// exact power-of-two scale s with max_abs * s < 2^14 (fp16 max is 65504)
+__device__ __forceinline__ float dxg_scale_for(float max_abs) {
+  if (!(max_abs > 0.f)) return 1.f;
+  int e;
+  frexpf(max_abs, &e);  // max_abs < 2^e
+  return ldexpf(1.f, 14 - e);
+}
+
+template <int N>
+__device__ __forceinline__ unsigned dxg_idesc_f16() {
+  // c F32 (bit 4), a/b F16 (0 at bits 7, 10), both K-major, N>>3 at 17, M=128 (8 at 24)
+  return (1u << 4) | ((unsigned)(N >> 3) << 17) | (8u << 24);
+}
+__device__ __forceinline__ void dxg_umma_f16(unsigned tmem, unsigned long long da, unsigned long long db,
+                                              unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void dxg_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void dxg_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void dxg_named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+#define DXG_TMEM_LD16(taddr, v)                                                                              \
+  asm volatile(                                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),      \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) \
+      : "r"(taddr))
+
+// ---- max |x| (bit pattern of a non-negative float: atomicMax on u32 orders it)
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_absmax(const float* __restrict__ x, long long cnt,
+                                                                unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt / 4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(x)[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(DX_FULL, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// ---- prep: per-component Q images, b_k = Q_k mu_k, c_k = alpha_k + sum q_k ----
+// qimg layout: [Kpad/8 groups][split hi,lo][512 rows = 8 comps x 64][128 B];
+// row j*64 + r of group g holds row r of sq_k Q_{8g+j} (zero for k >= K);
+// bvec = sx sq_k Q_k mu_k, dvec = sq_k diag(Q_k), svec = (sx sq_k)^-2: the
+// forward forms sx sq_k Q_k (x - mu_k) = MMA(L) + dvec * (sx x) - bvec.
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_prep_q(const float* alphas, const float* means,
+                                                                const float* icf, int K, const unsigned* xmax,
+                                                                unsigned char* qimg, float* bvec, float* cvec,
+                                                                float* svec, float* dvec) {
+  __shared__ double Q[DXG_D][DXG_D + 1];
+  __shared__ float qmax[8];
+  const int k = blockIdx.x;
+  const bool live = k < K;
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
+    const int r = e / DXG_D, c = e % DXG_D;
+    double v = 0.0;
+    if (live) {
+      const float* q = icf + (long long)k * DXG_ICF;
+      if (r == c) v = exp((double)q[r]);
+      else if (r > c) v = (double)q[DXG_D + c * (DXG_D - 1) - c * (c - 1) / 2 + (r - c - 1)];
+    }
+    Q[r][c] = v;
+  }
+  __syncthreads();
+  float m = 0.f;
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) m = fmaxf(m, fabsf((float)Q[e / DXG_D][e % DXG_D]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(DX_FULL, m, o));
+  if ((threadIdx.x & 31) == 0) qmax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, qmax[w]);
+  const double sq = (double)dxg_scale_for(m), sx = (double)dxg_scale_for(__uint_as_float(*xmax));
+  const int g = k / DXG_GC, j = k % DXG_GC;
+  unsigned char* hi = qimg + (long long)g * 2 * (DXG_GC * 64 * 128);
+  unsigned char* lo = hi + DXG_GC * 64 * 128;
+  for (int e = threadIdx.x; e < DXG_D * DXG_D / 2; e += blockDim.x) {
+    const int r = e / (DXG_D / 2), c = 2 * (e % (DXG_D / 2));
+    unsigned h, l;
+    // the tensor cores see only the strictly lower L_k; the diagonal is
+    // applied exactly in the forward epilogue (dvec), which keeps the TMEM
+    // accumulation small (~|L x|) and beta accurate to fp32 level
+    dxg_split2(c == r ? 0.f : (float)(Q[r][c] * sq), c + 1 == r ? 0.f : (float)(Q[r][c + 1] * sq), h, l);
+    const unsigned off = dxg_sw((unsigned)(j * 64 + r), (unsigned)c);
+    *reinterpret_cast<unsigned*>(hi + off) = h;
+    *reinterpret_cast<unsigned*>(lo + off) = l;
+  }
+  if (threadIdx.x < DXG_D) {
+    const int r = threadIdx.x;
+    double s = 0.0;
+    if (live)
+      for (int c = 0; c <= r; ++c) s += Q[r][c] * (double)means[(long long)k * DXG_D + c];
+    bvec[(long long)k * DXG_D + r] = (float)(s * sq * sx);
+  }
+  if (threadIdx.x == 0) svec[k] = (float)(1.0 / (sq * sx * sq * sx));
+  if (threadIdx.x < DXG_D) dvec[(long long)k * DXG_D + threadIdx.x] = (float)(Q[threadIdx.x][threadIdx.x] * sq);
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    if (live) {
+      s = alphas[k];
+      for (int c = 0; c < DXG_D; ++c) s += (double)icf[(long long)k * DXG_ICF + c];
+    }
+    cvec[k] = (float)s;
+  }
+}
+
+// ---- prep: point images ----------------------------------------------------------
+// ximg:  [tiles of 128 points][hi 16 KB][lo 16 KB], row = point, col = dim
+// xtimg: [chunks of 64 points][hi 8 KB][lo 8 KB], row = dim, col = point
+// Rows past n are zero.  One block = one 128-point tile (two 64-point chunks).
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_prep_x(const float* x, long long n, const unsigned* xmax,
+                                                                unsigned char* ximg, unsigned char* xtimg) {
+  __shared__ float xs[DXG_TM][DXG_D + 1];
+  const long long t = blockIdx.x;
+  const float sx = dxg_scale_for(__uint_as_float(*xmax));
+  for (int e = threadIdx.x; e < DXG_TM * DXG_D / 4; e += blockDim.x) {
+    const int r = e / (DXG_D / 4), c4 = e % (DXG_D / 4);
+    const long long p = t * DXG_TM + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p < n) v = *reinterpret_cast<const float4*>(x + p * DXG_D + 4 * c4);
+    v.x *= sx; v.y *= sx; v.z *= sx; v.w *= sx;  // exact (power of two)
+    xs[r][4 * c4] = v.x;
+    xs[r][4 * c4 + 1] = v.y;
+    xs[r][4 * c4 + 2] = v.z;
+    xs[r][4 * c4 + 3] = v.w;
+  }
+  __syncthreads();
+  unsigned char* xh = ximg + t * 2 * (DXG_TM * 128);
+  unsigned char* xl = xh + DXG_TM * 128;
+  for (int e = threadIdx.x; e < DXG_TM * DXG_D / 2; e += blockDim.x) {
+    const int r = e / (DXG_D / 2), c = 2 * (e % (DXG_D / 2));
+    unsigned h, l;
+    dxg_split2(xs[r][c], xs[r][c + 1], h, l);
+    const unsigned off = dxg_sw((unsigned)r, (unsigned)c);
+    *reinterpret_cast<unsigned*>(xh + off) = h;
+    *reinterpret_cast<unsigned*>(xl + off) = l;
+  }
+  for (int e = threadIdx.x; e < 2 * DXG_D * (DXG_BC / 2); e += blockDim.x) {
+    const int ch = e / (DXG_D * (DXG_BC / 2));
+    const int rem = e % (DXG_D * (DXG_BC / 2));
+    const int a = rem / (DXG_BC / 2), p = 2 * (rem % (DXG_BC / 2));
+    unsigned h, l;
+    dxg_split2(xs[ch * DXG_BC + p][a], xs[ch * DXG_BC + p + 1][a], h, l);
+    unsigned char* th = xtimg + (t * 2 + ch) * 2 * (DXG_D * 128);
+    const unsigned off = dxg_sw((unsigned)a, (unsigned)p);
+    *reinterpret_cast<unsigned*>(th + off) = h;
+    *reinterpret_cast<unsigned*>(th + DXG_D * 128 + off) = l;
+  }
+}
+
+// ---- forward: beta[k][i] for every point and component ---------------------------
+// Work unit = (component group g of 8, contiguous tile range p of the points);
+// CTA c takes units c, c + grid, ...  Warp 0: bulk-copy producer (Q group once
+// per unit, X tiles through a 2-stage ring); warp 1: MMA issuer; warps 2-5:
+// epilogue (warp w drains TMEM lanes 32*(w%4)..+31 = tile rows).  TMEM: 512
+// columns = 8 components x 64, in two halves of 4 components that alternate
+// between MMA and epilogue.
+#define DXG_FWD_SMEM (2 * DXG_GC * 64 * 128 + 2 * 2 * DXG_TM * 128 + 1024)
+extern "C" __global__ void __launch_bounds__(192, 1)
+    dx_gmm_fwd(const unsigned char* __restrict__ qimg, const unsigned char* __restrict__ ximg,
+               const float* __restrict__ bvec, const float* __restrict__ cvec, const float* __restrict__ svec,
+               const float* __restrict__ dvec, int K, long long n,
+               long long npad, int P, float* __restrict__ beta) {
+  extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
+  unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
+  unsigned char* qs = smem;                                // 128 KB: hi (64 KB) then lo
+  unsigned char* xsm = smem + 2 * DXG_GC * 64 * 128;       // 2 stages x 32 KB
+  __shared__ __align__(8) unsigned long long xfull[2], xempty[2], tfull[2], tempty[2], qfull, qempty;
+  __shared__ float bsm[DXG_GC][DXG_D], dsm[DXG_GC][DXG_D];
+  __shared__ float csm[DXG_GC], ssm[DXG_GC];
+  __shared__ unsigned tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NG = (K + DXG_GC - 1) / DXG_GC;
+  const long long T = npad / DXG_TM;
+  const int units = NG * P;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      dx_mbar_init(&xfull[s], 1);
+      dx_mbar_init(&xempty[s], 5);  // MMA commit + the 4 epilogue warps (they read x)
+      dx_mbar_init(&tfull[s], 1);
+      dx_mbar_init(&tempty[s], 4);
+    }
+    dx_mbar_init(&qfull, 1);
+    dx_mbar_init(&qempty, 1);
+    dx_fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  dxg_fence_before();
+  __syncthreads();
+  dxg_fence_after();
+  const unsigned tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0, qn = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
+        const int g = u / P, p = u % P;
+        const long long t0 = (long long)p * T / P, t1 = (long long)(p + 1) * T / P;
+        if (qn > 0) dx_mbar_wait_bounded(&qempty, (unsigned)((qn - 1) & 1));
+        dx_mbar_expect_tx(&qfull, 2 * DXG_GC * 64 * 128);
+        dx_bulk_g2s(qs, qimg + (long long)g * 2 * DXG_GC * 64 * 128, 2 * DXG_GC * 64 * 128, &qfull);
+        for (long long t = t0; t < t1; ++t, ++it) {
+          const int s = it & 1;
+          if (it >= 2) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it >> 1) - 1) & 1));
+          dx_mbar_expect_tx(&xfull[s], 2 * DXG_TM * 128);
+          dx_bulk_g2s(xsm + s * 2 * DXG_TM * 128, ximg + t * 2 * DXG_TM * 128, 2 * DXG_TM * 128, &xfull[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const unsigned idesc = dxg_idesc_f16<256>();
+      const unsigned qaddr = dx_smem_addr(qs), xaddr = dx_smem_addr(xsm);
+      int it = 0, qn = 0, tt = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
+        const int p = u % P;
+        const long long t0 = (long long)p * T / P, t1 = (long long)(p + 1) * T / P;
+        dx_mbar_wait_bounded(&qfull, (unsigned)(qn & 1));
+        dxg_fence_after();
+        for (long long t = t0; t < t1; ++t, ++it) {
+          const int s = it & 1;
+          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+          dxg_fence_after();
+          const unsigned xa = xaddr + (unsigned)(s * 2 * DXG_TM * 128);
+          for (int h = 0; h < 2; ++h, ++tt) {
+            if (tt >= 2) dx_mbar_wait_bounded(&tempty[h], (unsigned)(((tt >> 1) - 1) & 1));
+            dxg_fence_after();
+            const unsigned td = tmem + (unsigned)(h * 256);
+            const unsigned qh = qaddr + (unsigned)(h * 256 * 128), ql = qh + DXG_GC * 64 * 128;
+#pragma unroll
+            for (int kk = 0; kk < DXG_D / 16; ++kk) {
+              const unsigned long long ah = dx_umma_desc_sw128(xa + kk * 32);
+              const unsigned long long al = dx_umma_desc_sw128(xa + DXG_TM * 128 + kk * 32);
+              const unsigned long long bh = dx_umma_desc_sw128(qh + kk * 32);
+              const unsigned long long bl = dx_umma_desc_sw128(ql + kk * 32);
+              dxg_umma_f16(td, ah, bh, idesc, kk > 0);
+              dxg_umma_f16(td, ah, bl, idesc, 1u);
+              dxg_umma_f16(td, al, bh, idesc, 1u);
+            }
+            dx_umma_commit(&tfull[h]);
+          }
+          dx_umma_commit(&xempty[s]);
+        }
+        dx_umma_commit(&qempty);  // Q group free once every MMA of this unit retired
+      }
+    }
+  } else {
+    // epilogue: warps 2..5
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    const unsigned lanebase = tmem + ((unsigned)(q * 32) << 16);
+    int tt = 0, it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int g = u / P, p = u % P;
+      const long long t0 = (long long)p * T / P, t1 = (long long)(p + 1) * T / P;
+      dxg_named_sync(1, 128);  // previous unit's epilogue is done with bsm/csm
+      for (int e = et; e < DXG_GC * DXG_D; e += 128) {
+        const int j = e / DXG_D, c = e % DXG_D;
+        const int k = g * DXG_GC + j;
+        bsm[j][c] = k < K ? bvec[(long long)k * DXG_D + c] : 0.f;
+        dsm[j][c] = k < K ? dvec[(long long)k * DXG_D + c] : 0.f;
+      }
+      if (et < DXG_GC) {
+        csm[et] = g * DXG_GC + et < K ? cvec[g * DXG_GC + et] : 0.f;
+        ssm[et] = g * DXG_GC + et < K ? svec[g * DXG_GC + et] : 0.f;
+      }
+      dxg_named_sync(1, 128);
+      for (long long t = t0; t < t1; ++t, ++it) {
+        const long long i = t * DXG_TM + row;
+        // this row's scaled point sx*x from the A stage (fp16 hi + lo)
+        float xr[DXG_D];
+        {
+          const int s = it & 1;
+          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+          const unsigned char* xh = xsm + s * 2 * DXG_TM * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const unsigned off = dxg_sw((unsigned)row, (unsigned)(ch * 8));
+            const uint4 hv = *reinterpret_cast<const uint4*>(xh + off);
+            const uint4 lv = *reinterpret_cast<const uint4*>(xh + DXG_TM * 128 + off);
+            const unsigned hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              xr[ch * 8 + 2 * w] = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]);
+              xr[ch * 8 + 2 * w + 1] = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) dx_mbar_arrive(&xempty[s]);
+        }
+        for (int h = 0; h < 2; ++h, ++tt) {
+          dx_mbar_wait_bounded(&tfull[h], (unsigned)((tt >> 1) & 1));
+          dxg_fence_after();
+#pragma unroll 1
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = h * 4 + jj;
+            unsigned v0[16], v1[16], v2[16], v3[16];
+            const unsigned ta = lanebase + (unsigned)(h * 256 + jj * 64);
+            DXG_TMEM_LD16(ta, v0);
+            DXG_TMEM_LD16(ta + 16, v1);
+            DXG_TMEM_LD16(ta + 32, v2);
+            DXG_TMEM_LD16(ta + 48, v3);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float s0 = 0.f, s1 = 0.f;
+            // y~_c = MMA_c - bvec_c + dvec_c * x~_c  (= sx sq Q (x - mu))
+#define DXG_Y(V, c0)                                                                                        \
+  {                                                                                                         \
+    const float y0 = fmaf(dsm[j][c0 + c], xr[c0 + c], __uint_as_float(V[c]) - bsm[j][c0 + c]);             \
+    const float y1 = fmaf(dsm[j][c0 + c + 1], xr[c0 + c + 1], __uint_as_float(V[c + 1]) - bsm[j][c0 + c + 1]); \
+    s0 = fmaf(y0, y0, s0);                                                                                  \
+    s1 = fmaf(y1, y1, s1);                                                                                  \
+  }
+#pragma unroll
+            for (int c = 0; c < 16; c += 2) {
+              DXG_Y(v0, 0)
+              DXG_Y(v1, 16)
+              DXG_Y(v2, 32)
+              DXG_Y(v3, 48)
+            }
+#undef DXG_Y
+            const int k = g * DXG_GC + j;
+            if (k < K && i < n) beta[(long long)k * npad + i] = csm[j] - 0.5f * ssm[j] * (s0 + s1);
+          }
+          dxg_fence_before();
+          __syncwarp();
+          if (lane == 0) dx_mbar_arrive(&tempty[h]);
+        }
+      }
+    }
+  }
+  dxg_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+// ---- log-sum-exp over components per point; block partials of sum_i lse_i -------
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __restrict__ beta, int K, long long n,
+                                                             long long npad, float* __restrict__ lse,
+                                                             double* __restrict__ part) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    // one pass, online max: s = sum exp(beta - m) rescaled when m grows
+    float m = -3.0e38f, s = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      const float v = beta[(long long)k * npad + i];
+      if (v > m) {
+        s = s * __expf(m - v) + 1.f;
+        m = v;
+      } else {
+        s += __expf(v - m);
+      }
+    }
+    const float l = m + __logf(s);
+    lse[i] = l;
+    acc += (double)l;
+  }
+  __shared__ double scr[32];
+  const double tot = dx_block_sum(acc, scr);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// ---- backward moments -------------------------------------------------------------
+// Work unit = (component pair pr, contiguous chunk range p); CTA c takes the
+// contiguous unit range [c*U/grid, (c+1)*U/grid) and accumulates consecutive
+// units of the same pair in registers, flushing a partial slot at every pair
+// change.  Warp 0: X^T chunk producer (bulk copies, 2-stage ring); warp 1: MMA
+// issuer; warps 2-9: A-operand producers (g * (X - mu)^T, fp16x3 split, W sums);
+// warps 10-13: TMEM promotion epilogue.  D (128 lanes x 80 columns, hi*hi and
+// the small cross products in separate accumulators) is double buffered in
+// TMEM and promoted every DXG_PROMO chunks into fp32 registers, which spill
+// every DXG_F64_EVERY promotions into fp64 accumulators in shared memory
+// (column-major, conflict-free).
+#define DXG_XT_BYTES (2 * DXG_D * 128)          // hi + lo image of one chunk
+#define DXG_XB_BYTES (DXG_BN * 128)             // one split of the B operand (+ ones rows)
+#define DXG_Z_BYTES (2 * 128 * 128)             // hi + lo A operand of one chunk
+#define DXG_BWD_SMEM (2 * 2 * DXG_XB_BYTES + 2 * DXG_Z_BYTES + DXG_BN * 128 * 8 + 1024)
+extern "C" __global__ void __launch_bounds__(448, 1)
+    dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
+               const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
+               int K, long long n, long long npad, int P2,
+               double* __restrict__ dpart, float* __restrict__ wpart, int* __restrict__ ppart) {
+  extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
+  unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
+  unsigned char* bs = smem;                           // 2 stages x (hi 10 KB, lo 10 KB)
+  unsigned char* zs = smem + 2 * 2 * DXG_XB_BYTES;    // 2 stages x (hi 16 KB, lo 16 KB)
+  double* dacc = reinterpret_cast<double*>(zs + 2 * DXG_Z_BYTES);  // [80][128] fp64
+  // per stage: beta of the pair's two components and lse over the chunk's 64
+  // points (bulk-copied with X^T, so the producers never wait on HBM)
+  __shared__ __align__(16) float gin[2][3][DXG_BC];
+  __shared__ __align__(8) unsigned long long xfull[2], xempty[2], zfull[2], zempty[2], tfull[2], tempty[2];
+  __shared__ unsigned tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NP = (K + 1) / 2;
+  const long long C = npad / DXG_BC;  // chunks
+  const long long units = (long long)NP * P2;
+  const long long u0 = (long long)blockIdx.x * units / gridDim.x, u1 = (long long)(blockIdx.x + 1) * units / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      dx_mbar_init(&xfull[s], 1);
+      dx_mbar_init(&xempty[s], 1);
+      dx_mbar_init(&zfull[s], 8);
+      dx_mbar_init(&zempty[s], 1);
+      dx_mbar_init(&tfull[s], 1);
+      dx_mbar_init(&tempty[s], 4);
+    }
+    dx_fence_mbar_init();
+  }
+  // constant B rows 64..79 of every stage: row 64 = 1.0 (hi) / 0 (lo), others 0
+  for (int e = threadIdx.x; e < 2 * 2 * 16 * 32; e += blockDim.x) {
+    const int st = e / (2 * 16 * 32), sp = (e / (16 * 32)) % 2, rr = (e / 32) % 16, w = e % 32;
+    const unsigned val = (sp == 0 && rr == 0) ? 0x3c003c00u : 0u;  // fp16 1.0
+    *reinterpret_cast<unsigned*>(bs + (st * 2 + sp) * DXG_XB_BYTES + (64 + rr) * 128 + w * 4) = val;
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  dx_fence_proxy_async();
+  dxg_fence_before();
+  __syncthreads();
+  dxg_fence_after();
+  const unsigned tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const long long pr = u / P2, p = u % P2;
+        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+        const long long k0 = pr * 2, k1 = (pr * 2 + 1 < K) ? pr * 2 + 1 : pr * 2;
+        for (long long c = c0; c < c1; ++c, ++it) {
+          const int s = it & 1;
+          if (it >= 2) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it >> 1) - 1) & 1));
+          dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES + 3 * DXG_BC * 4);
+          const unsigned char* src = xtimg + c * DXG_XT_BYTES;
+          dx_bulk_g2s(bs + (s * 2) * DXG_XB_BYTES, src, DXG_D * 128, &xfull[s]);
+          dx_bulk_g2s(bs + (s * 2 + 1) * DXG_XB_BYTES, src + DXG_D * 128, DXG_D * 128, &xfull[s]);
+          dx_bulk_g2s(gin[s][0], beta + k0 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
+          dx_bulk_g2s(gin[s][1], beta + k1 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
+          dx_bulk_g2s(gin[s][2], lse + c * DXG_BC, DXG_BC * 4, &xfull[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const unsigned idesc = dxg_idesc_f16<DXG_BN>();
+      const unsigned baddr = dx_smem_addr(bs), zaddr = dx_smem_addr(zs);
+      int it = 0, pc = 0;
+      long long prevPair = -1;
+      int inb = 0;  // chunks accumulated into the current TMEM buffer
+      for (long long u = u0; u < u1; ++u) {
+        const long long pr = u / P2, p = u % P2;
+        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+        if (pr != prevPair && inb > 0) {  // flush at pair change
+          dx_umma_commit(&tfull[pc & 1]);
+          ++pc;
+          inb = 0;
+        }
+        prevPair = pr;
+        for (long long c = c0; c < c1; ++c, ++it) {
+          const int s = it & 1;
+          if (inb == 0 && pc >= 2) dx_mbar_wait_bounded(&tempty[pc & 1], (unsigned)(((pc >> 1) - 1) & 1));
+          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+          dx_mbar_wait_bounded(&zfull[s], (unsigned)((it >> 1) & 1));
+          dxg_fence_after();
+          // buffer (pc & 1): columns [256 b, 256 b + 80) take hi*hi, [+128, +208)
+          // the small hi*lo + lo*hi products (fewer truncating adds on the big sum)
+          const unsigned td = tmem + (unsigned)((pc & 1) * 256), ts = td + 128;
+          const unsigned bh = baddr + (unsigned)(s * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
+          const unsigned zh = zaddr + (unsigned)(s * DXG_Z_BYTES), zl = zh + 128 * 128;
+#pragma unroll
+          for (int kk = 0; kk < DXG_BC / 16; ++kk) {
+            const unsigned long long ah = dx_umma_desc_sw128(zh + kk * 32);
+            const unsigned long long al = dx_umma_desc_sw128(zl + kk * 32);
+            const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
+            const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
+            const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
+            dxg_umma_f16(td, ah, dbh, idesc, acc);
+            dxg_umma_f16(ts, ah, dbl, idesc, acc);
+            dxg_umma_f16(ts, al, dbh, idesc, 1u);
+          }
+          dx_umma_commit(&xempty[s]);
+          dx_umma_commit(&zempty[s]);
+          if (++inb == DXG_PROMO) {
+            dx_umma_commit(&tfull[pc & 1]);
+            ++pc;
+            inb = 0;
+          }
+        }
+      }
+      if (inb > 0) {
+        dx_umma_commit(&tfull[pc & 1]);
+        ++pc;
+      }
+    }
+  } else if (warp < 10) {
+    // A-operand producers: thread (row r = (k_local, b), half hh of the chunk's
+    // points).  Z[(k,b)][i] = g_ik (x_ib - mu_kb), centred on the component's
+    // mean so the moments need no cancelling correction (M = D - m~ mu^T).
+    // g is computed once per (component, point): lane q of a warp evaluates
+    // point hh*32+q and the warp shares the 32 values through shared memory.
+    const int pt = threadIdx.x - 64;       // 0..255
+    const int r = pt & 127, hh = pt >> 7;  // row of Z, point half
+    const int kl = r >> 6, b = r & 63;
+    const int pw = pt >> 5;                // producer warp 0..7
+    const bool wrow = (pw & 1) == 0;       // warps holding rows b < 32 accumulate W
+    __shared__ __align__(16) float gw[8][32];
+    __shared__ float wred[8];
+    const float sx = dxg_scale_for(__uint_as_float(*xmax));
+    int it = 0;
+    float wacc = 0.f, mub = 0.f;
+    long long prevPair = -1;
+    int slot = 0;
+    auto flushW = [&]() {  // W of the finished pair: fixed-order reduction over points
+      const float w = dx_warp_sum(wacc);
+      dxg_named_sync(2, 256);
+      if (lane == 0) wred[pw] = w;
+      dxg_named_sync(2, 256);
+      if (pt < 2) wpart[((long long)blockIdx.x * DXG_FMAX + slot) * 2 + pt] = wred[2 * pt] + wred[2 * pt + 4];
+      ++slot;
+    };
+    for (long long u = u0; u < u1; ++u) {
+      const long long pr = u / P2, p = u % P2;
+      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+      const int k = (int)(pr * 2 + kl);
+      const bool live = k < K;
+      if (pr != prevPair) {
+        if (prevPair >= 0) flushW();
+        prevPair = pr;
+        wacc = 0.f;
+        mub = live ? means[(long long)k * DXG_D + b] * sx : 0.f;
+      }
+      for (long long c = c0; c < c1; ++c, ++it) {
+        const int s = it & 1;
+        if (it >= 2) dx_mbar_wait_bounded(&zempty[s], (unsigned)(((it >> 1) - 1) & 1));
+        dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+        {
+          const int q = hh * 32 + lane;
+          const float gg = __expf(gin[s][kl][q] - gin[s][2][q]);
+          const float gq = (live && c * DXG_BC + q < n) ? gg : 0.f;
+          if (wrow) wacc += gq;
+          gw[pw][lane] = gq;
+          __syncwarp();
+        }
+        const unsigned char* xh = bs + (s * 2) * DXG_XB_BYTES;
+        const unsigned char* xl = xh + DXG_XB_BYTES;
+        unsigned char* zh = zs + s * DXG_Z_BYTES;
+        unsigned char* zl = zh + 128 * 128;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {  // 4 x 8 points = 16-byte chunks
+          const int pcol = hh * 32 + cc * 8;
+          const unsigned off_x = dxg_sw((unsigned)b, (unsigned)pcol);
+          const uint4 h4 = *reinterpret_cast<const uint4*>(xh + off_x);
+          const uint4 l4 = *reinterpret_cast<const uint4*>(xl + off_x);
+          const float4 ga = *reinterpret_cast<const float4*>(&gw[pw][cc * 8]);
+          const float4 gb = *reinterpret_cast<const float4*>(&gw[pw][cc * 8 + 4]);
+          const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+          const unsigned hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
+          unsigned oh[4], ol[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float x0 = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]) - mub;
+            const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
+            dxg_split2(gv[2 * w] * x0, gv[2 * w + 1] * x1, oh[w], ol[w]);
+          }
+          const unsigned off_z = dxg_sw((unsigned)r, (unsigned)pcol);
+          *reinterpret_cast<uint4*>(zh + off_z) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+          *reinterpret_cast<uint4*>(zl + off_z) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+        }
+        dx_fence_proxy_async();  // generic-proxy writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) dx_mbar_arrive(&zfull[s]);
+      }
+    }
+    if (prevPair >= 0) flushW();
+  } else {
+    // promotion epilogue: warps 10..13 -> TMEM lane quarter (warp & 3)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const unsigned lanebase = tmem + ((unsigned)(q * 32) << 16);
+#pragma unroll 4
+    for (int j = 0; j < DXG_BN; ++j) dacc[j * 128 + row] = 0.0;
+    float acc[DXG_BN];
+#pragma unroll
+    for (int j = 0; j < DXG_BN; ++j) acc[j] = 0.f;
+    int pc = 0, inb = 0, slot = 0, nacc = 0;
+    long long prevPair = -1;
+    auto spill = [&]() {  // fp32 partial of <= DXG_F64_EVERY chunks -> fp64
+#pragma unroll
+      for (int j = 0; j < DXG_BN; ++j) {
+        dacc[j * 128 + row] += (double)acc[j];
+        acc[j] = 0.f;
+      }
+      nacc = 0;
+    };
+    auto drain = [&]() {
+      const int b = pc & 1;
+      dx_mbar_wait_bounded(&tfull[b], (unsigned)((pc >> 1) & 1));
+      dxg_fence_after();
+#pragma unroll
+      for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
+        unsigned v[16], w[16];
+        DXG_TMEM_LD16(lanebase + (unsigned)(b * 256 + j0), v);
+        DXG_TMEM_LD16(lanebase + (unsigned)(b * 256 + 128 + j0), w);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+      }
+      dxg_fence_before();
+      __syncwarp();
+      if (lane == 0) dx_mbar_arrive(&tempty[b]);
+      ++pc;
+      if (++nacc == DXG_F64_EVERY) spill();
+    };
+    auto flush = [&](long long pair) {
+      spill();
+      double* dst = dpart + (((long long)blockIdx.x * DXG_FMAX + slot) * 128 + row) * DXG_BN;
+#pragma unroll 4
+      for (int j = 0; j < DXG_BN; ++j) {
+        dst[j] = dacc[j * 128 + row];
+        dacc[j * 128 + row] = 0.0;
+      }
+      if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)pair;
+      ++slot;
+    };
+    for (long long u = u0; u < u1; ++u) {
+      const long long pr = u / P2, p = u % P2;
+      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+      if (pr != prevPair && prevPair >= 0) {
+        if (inb > 0) { drain(); inb = 0; }
+        flush(prevPair);
+      }
+      prevPair = pr;
+      for (long long c = c0; c < c1; ++c)
+        if (++inb == DXG_PROMO) { drain(); inb = 0; }
+    }
+    if (prevPair >= 0) {
+      if (inb > 0) drain();
+      flush(prevPair);
+    }
+  }
+  dxg_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+// ---- moments: fold the backward partial slots of each component's pair in CTA
+// order into fp64 mom[k] = (P [64][64], m~ [64], W) with the centred moments
+// P[b][a] = sum_i g (x - mu)_b x_a and m~ = sum_i g (x - mu) ----------------------
+#define DXG_MOM (DXG_D * DXG_D + DXG_D + 1)
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* dpart, const float* wpart,
+                                                                 const int* ppart, int nslot, const unsigned* xmax,
+                                                                 double* mom) {
+  // D accumulated sx^2 P and sx m~ (operands scaled by the points' scale sx)
+  const double isx = 1.0 / (double)dxg_scale_for(__uint_as_float(*xmax));
+  __shared__ int slots[1024];  // host guarantees nslot <= 1024
+  __shared__ int nsl;
+  const int k = blockIdx.x, pr = k / 2, kl = k % 2;
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int e = 0; e < nslot && ns < 1024; ++e)
+      if (ppart[e] == pr) slots[ns++] = e;
+    nsl = ns;
+  }
+  __syncthreads();
+  double* out = mom + (long long)k * DXG_MOM;
+  for (int e = threadIdx.x; e < DXG_D * (DXG_D + 1); e += blockDim.x) {
+    const int b = e / (DXG_D + 1), a = e % (DXG_D + 1);  // a == 64: first moment
+    double s = 0.0;
+    for (int sl = 0; sl < nsl; ++sl) s += dpart[((long long)slots[sl] * 128 + kl * 64 + b) * DXG_BN + a];
+    if (a < DXG_D) out[b * DXG_D + a] = s * isx * isx;
+    else out[DXG_D * DXG_D + b] = s * isx;
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int sl = 0; sl < nsl; ++sl) s += (double)wpart[(long long)slots[sl] * 2 + kl];
+    out[DXG_D * DXG_D + DXG_D] = s;
+  }
+}
+
+// fixed-order sum of the lse block partials
+extern "C" __global__ void dx_gmm_sum(const double* part, int n, double* out) {
+  __shared__ double scr[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  const double t = dx_block_sum(s, scr);
+  if (threadIdx.x == 0) *out = t;
+}
+
+// ---- finish: per component, fp64 --------------------------------------------------
+// From the fp64 moments of dx_gmm_moments (summed over ranks when sharded):
+//   M   = P - m~ mu^T                              (= sum_i g (x-mu)(x-mu)^T)
+//   dQ  = -Q M (lower triangle), v = Q m~, d mu = Q^T v
+//   d alpha = W - n softmax(alpha), d icf = (diag: dQ_jj e^q_j + W + gamma^2 e^{2 q_j} - m;
+//   L: dQ + gamma^2 L), and the prior term of the objective.
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_finish(
+    const float* alphas, const float* means, const float* icf, int K, long long n, const double* mom,
+    double gamma, int wm, double* d_alphas, double* d_means, double* d_icf, double* prior_k) {
+  extern __shared__ double dxg_fin_smem[];  // Q, M: 2 x 64 x 65 doubles (dynamic)
+  double(*Q)[DXG_D + 1] = reinterpret_cast<double(*)[DXG_D + 1]>(dxg_fin_smem);
+  double(*M)[DXG_D + 1] = reinterpret_cast<double(*)[DXG_D + 1]>(dxg_fin_smem + DXG_D * (DXG_D + 1));
+  __shared__ double mu[DXG_D], mm[DXG_D], v[DXG_D];
+  __shared__ double Wk, lse_a;
+  const int k = blockIdx.x;
+  const float* q = icf + (long long)k * DXG_ICF;
+  const double* mk = mom + (long long)k * DXG_MOM;
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
+    const int r = e / DXG_D, c = e % DXG_D;
+    double val = 0.0;
+    if (r == c) val = exp((double)q[r]);
+    else if (r > c) val = (double)q[DXG_D + c * (DXG_D - 1) - c * (c - 1) / 2 + (r - c - 1)];
+    Q[r][c] = val;
+    M[r][c] = mk[r * DXG_D + c];
+  }
+  if (threadIdx.x < DXG_D) {
+    const int b = threadIdx.x;
+    mu[b] = (double)means[(long long)k * DXG_D + b];
+    mm[b] = mk[DXG_D * DXG_D + b];
+  }
+  if (threadIdx.x == 0) {
+    Wk = mk[DXG_D * DXG_D + DXG_D];
+    double m0 = -1e300;
+    for (int j = 0; j < K; ++j) m0 = fmax(m0, (double)alphas[j]);
+    double se = 0.0;
+    for (int j = 0; j < K; ++j) se += exp((double)alphas[j] - m0);
+    lse_a = m0 + log(se);
+  }
+  __syncthreads();
+  // M <- P - m~ mu^T
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
+    const int r = e / DXG_D, c = e % DXG_D;
+    M[r][c] = M[r][c] - mm[r] * mu[c];
+  }
+  if (threadIdx.x < DXG_D) {
+    const int r = threadIdx.x;
+    double s = 0.0;
+    for (int c = 0; c <= r; ++c) s += Q[r][c] * mm[c];
+    v[r] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < DXG_D) {
+    const int a = threadIdx.x;
+    double s = 0.0;
+    for (int r = a; r < DXG_D; ++r) s += Q[r][a] * v[r];
+    d_means[(long long)k * DXG_D + a] = s;
+  }
+  const double g2 = gamma * gamma;
+  double* di = d_icf + (long long)k * DXG_ICF;
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
+    const int r = e / DXG_D, c = e % DXG_D;
+    if (c > r) continue;
+    double s = 0.0;
+    for (int j = 0; j <= r; ++j) s += Q[r][j] * M[j][c];  // Q lower triangular
+    const double dq = -s;
+    if (r == c) di[r] = dq * Q[r][r] + Wk + g2 * Q[r][r] * Q[r][r] - (double)wm;
+    else di[DXG_D + c * (DXG_D - 1) - c * (c - 1) / 2 + (r - c - 1)] = dq + g2 * Q[r][c];
+  }
+  if (threadIdx.x == 0) {
+    d_alphas[k] = Wk - (double)n * exp((double)alphas[k] - lse_a);
+    double frob = 0.0, sq = 0.0;
+    for (int c = 0; c < DXG_D; ++c) {
+      frob += Q[c][c] * Q[c][c];
+      sq += (double)q[c];
+    }
+    for (int e = DXG_D; e < DXG_ICF; ++e) frob += (double)q[e] * (double)q[e];
+    prior_k[k] = 0.5 * g2 * frob - (double)wm * sq;
+  }
+}

@@ -412,6 +412,7 @@ struct CellUse {
   long long rowD = 0;
   int rowSitesN = 0;     // row-eligible accumulation sites (pass 0)
   bool vec4 = false;     // TileRow with float4 column blocks (f32, D % 4 == 0)
+  bool warpTab = false;  // TileRow realised as warp-private tables (dx_warp_tab)
   int aliasStage = -1;   // TMA-staged stream buffer whose stage doubles as the row tile
   long long width = 0;
   int partialBuf = -1;
@@ -2751,8 +2752,17 @@ void Lowering::decideStrategies(KGen& g) {
     for (auto& cu : g.cells) {
       if (cu.strat != CellUse::TileRow) continue;
       long long Kr = cu.width / cu.rowD;
-      cu.vec4 = !opt.f64 && cu.rowD % 4 == 0 && Kr * (cu.rowD / 4) <= NT;
       cu.smemOff = (off + 15) / 16 * 16;
+      // WarpTab: warp-private interleaved tables, no sort and no block
+      // barrier per tile (dx_warp_tab); needs (K+1) x 128 B per warp.
+      long long wt = (long long)(NT / 32) * (Kr + 1) * 128;
+      cu.warpTab = !opt.f64 && cu.rowD % 4 == 0 && 32 % cu.rowD == 0 &&
+                   cu.smemOff + wt + (long long)NT * cu.rowD * 4 <= 150 * 1024 && !std::getenv("DEXLET_NO_WARPTAB");
+      cu.vec4 = cu.warpTab || (!opt.f64 && cu.rowD % 4 == 0 && Kr * (cu.rowD / 4) <= NT);
+      if (cu.warpTab) {
+        off = cu.smemOff + (int)(wt + (long long)NT * cu.rowD * 4);
+        continue;
+      }
       off = cu.smemOff + (int)(NT * (cu.rowD + 1) * esize + (NT / 32) * Kr * 4 + (Kr + 1) * 4 + NT * 4 + 64);
     }
     return;
@@ -3097,7 +3107,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       smem = std::max<int>(smem, cu.smemOff + (int)(warps * cu.width * esize));
       maxRowD = std::max(maxRowD, cu.rowD);
     }
-    if (cu.strat == CellUse::TileRow) {
+    if (cu.strat == CellUse::TileRow && cu.warpTab) {
+      long long Kr = cu.width / cu.rowD;
+      long long wt = (long long)(g.threads / 32) * (Kr + 1) * 128;
+      long long etB = cu.aliasStage >= 0 ? 0 : (long long)g.threads * cu.rowD * 4;
+      smem = std::max<int>(smem, cu.smemOff + (int)(wt + etB));
+    } else if (cu.strat == CellUse::TileRow) {
       long long Kr = cu.width / cu.rowD;
       long long etB = cu.aliasStage >= 0 ? 0 : (long long)g.threads * (cu.rowD + 1) * esize;
       smem = std::max<int>(smem, cu.smemOff + (int)(etB + (g.threads / 32) * Kr * 4 + (Kr + 1) * 4 + g.threads * 4 + 64));
@@ -3195,58 +3210,6 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "  unsigned char* dx_smem = dx_smem_raw + ((1024u - (dx_smem_addr(dx_smem_raw) & 1023u)) & 1023u);\n";
     }
     bool needSync = false;
-    for (size_t i = 0; i < g.cells.size(); ++i) {
-      CellUse& cu = g.cells[i];
-      std::string I = std::to_string(i);
-      switch (cu.strat) {
-        case CellUse::Reg: src << "  dx_f rp" << I << " = 0;\n"; break;
-        case CellUse::Smem:
-          src << "  dx_f* sm" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
-          src << "  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) sm" << I << "[t] = 0;\n";
-          needSync = true;
-          break;
-        case CellUse::Count:
-          src << "  unsigned* sm" << I << " = (unsigned*)(dx_smem + " << cu.smemOff << ");\n";
-          src << "  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) sm" << I << "[t] = 0u;\n";
-          needSync = true;
-          break;
-        case CellUse::TileRow: {
-          long long Kr = cu.width / cu.rowD;
-          int nacc = (int)((cu.width + g.threads - 1) / g.threads);
-          long long et = cu.aliasStage >= 0 ? 0 : (long long)g.threads * (cu.rowD + 1) * esize;
-          if (cu.vec4) src << "  float4 acc" << I << " = make_float4(0.f, 0.f, 0.f, 0.f);\n";
-          else {
-            src << "  dx_f acc" << I << "[" << nacc << "];\n";
-            src << "#pragma unroll\n  for (int t = 0; t < " << nacc << "; ++t) acc" << I << "[t] = 0;\n";
-          }
-          src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
-          src << "  int* wc" << I << " = (int*)(dx_smem + " << cu.smemOff + et << ");\n";
-          src << "  int* st" << I << " = wc" << I << " + " << (g.threads / 32) * Kr << ";\n";
-          src << "  int* pm" << I << " = st" << I << " + " << Kr + 1 << ";\n";
-          if (cu.vec4) {
-            src << "  for (int t = threadIdx.x; t < " << (g.threads / 32) * Kr << "; t += blockDim.x) wc" << I << "[t] = 0;\n";
-            needSync = true;
-          }
-          break;
-        }
-        case CellUse::Row:
-          src << "  dx_f* rt" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
-          src << "  for (int t = threadIdx.x; t < " << warps * cu.width << "; t += blockDim.x) rt" << I << "[t] = 0;\n";
-          needSync = true;
-          break;
-        default: break;
-      }
-    }
-    if (maxRowD > 0)
-      src << "  dx_f* dx_stage = (dx_f*)(dx_smem + " << stageOff << ") + dx_warp * " << 32 * (maxRowD + 1) + 32 << ";\n";
-    for (int b : g.wholeStaged) {
-      std::string ct = ctype(plan.bufs[b].kind);
-      src << "  " << ct << "* wt" << b << " = (" << ct << "*)(dx_smem + " << wholeAt[b] << ");\n";
-      src << "  for (int t = threadIdx.x; t < " << plan.bufs[b].elems << "; t += blockDim.x) *(" << ct
-          << "*)((char*)wt" << b << " + dx_swz((unsigned)(t * " << storageBytesOf(plan.bufs[b].kind, opt.f64)
-          << "), 3)) = p" << b << "[t];\n";
-      needSync = true;
-    }
     if (!g.staged.empty()) {
       src << "  __shared__ __align__(8) unsigned long long dx_bar[2];\n";
       for (int b : g.staged) {
@@ -3284,6 +3247,69 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
             << ", (unsigned)n" << B << ", &dx_bar[stg]);\n";
       }
       src << "  };\n";
+      // first tile in flight before the shared-memory set-up below
+      if (tileCell >= 0 || g.tile)
+        src << "  if (threadIdx.x == 0 && (long long)blockIdx.x * blockDim.x < (dx_hi - dx_lo + " << (U - 1) << ") / " << U << ") dx_issue(0, (long long)blockIdx.x * blockDim.x);\n";
+      needSync = true;
+    }
+    for (size_t i = 0; i < g.cells.size(); ++i) {
+      CellUse& cu = g.cells[i];
+      std::string I = std::to_string(i);
+      switch (cu.strat) {
+        case CellUse::Reg: src << "  dx_f rp" << I << " = 0;\n"; break;
+        case CellUse::Smem:
+          src << "  dx_f* sm" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
+          src << "  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) sm" << I << "[t] = 0;\n";
+          needSync = true;
+          break;
+        case CellUse::Count:
+          src << "  unsigned* sm" << I << " = (unsigned*)(dx_smem + " << cu.smemOff << ");\n";
+          src << "  for (int t = threadIdx.x; t < " << cu.width << "; t += blockDim.x) sm" << I << "[t] = 0u;\n";
+          needSync = true;
+          break;
+        case CellUse::TileRow: {
+          long long Kr = cu.width / cu.rowD;
+          int nacc = (int)((cu.width + g.threads - 1) / g.threads);
+          long long et = cu.aliasStage >= 0 ? 0 : (long long)g.threads * (cu.rowD + 1) * esize;
+          if (cu.warpTab) {
+            long long wt = (long long)(g.threads / 32) * (Kr + 1) * 32;
+            src << "  float* wtab" << I << " = (float*)(dx_smem + " << cu.smemOff << ");\n";
+            src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff + wt * 4 << ");\n";
+            src << "  for (int t = threadIdx.x; t < " << wt << "; t += blockDim.x) wtab" << I << "[t] = 0.f;\n";
+            needSync = true;
+            break;
+          }
+          if (cu.vec4) src << "  float4 acc" << I << " = make_float4(0.f, 0.f, 0.f, 0.f);\n";
+          else {
+            src << "  dx_f acc" << I << "[" << nacc << "];\n";
+            src << "#pragma unroll\n  for (int t = 0; t < " << nacc << "; ++t) acc" << I << "[t] = 0;\n";
+          }
+          src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
+          src << "  int* wc" << I << " = (int*)(dx_smem + " << cu.smemOff + et << ");\n";
+          src << "  int* st" << I << " = wc" << I << " + " << (g.threads / 32) * Kr << ";\n";
+          src << "  int* pm" << I << " = st" << I << " + " << Kr + 1 << ";\n";
+          if (cu.vec4) {
+            src << "  for (int t = threadIdx.x; t < " << (g.threads / 32) * Kr << "; t += blockDim.x) wc" << I << "[t] = 0;\n";
+            needSync = true;
+          }
+          break;
+        }
+        case CellUse::Row:
+          src << "  dx_f* rt" << I << " = (dx_f*)(dx_smem + " << cu.smemOff << ");\n";
+          src << "  for (int t = threadIdx.x; t < " << warps * cu.width << "; t += blockDim.x) rt" << I << "[t] = 0;\n";
+          needSync = true;
+          break;
+        default: break;
+      }
+    }
+    if (maxRowD > 0)
+      src << "  dx_f* dx_stage = (dx_f*)(dx_smem + " << stageOff << ") + dx_warp * " << 32 * (maxRowD + 1) + 32 << ";\n";
+    for (int b : g.wholeStaged) {
+      std::string ct = ctype(plan.bufs[b].kind);
+      src << "  " << ct << "* wt" << b << " = (" << ct << "*)(dx_smem + " << wholeAt[b] << ");\n";
+      src << "  for (int t = threadIdx.x; t < " << plan.bufs[b].elems << "; t += blockDim.x) *(" << ct
+          << "*)((char*)wt" << b << " + dx_swz((unsigned)(t * " << storageBytesOf(plan.bufs[b].kind, opt.f64)
+          << "), 3)) = p" << b << "[t];\n";
       needSync = true;
     }
     if (needSync) src << "  __syncthreads();\n";
@@ -3292,7 +3318,6 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     src << "  const long long dx_stride = (long long)gridDim.x * blockDim.x;\n";
     if ((tileCell >= 0 || g.tile) && !g.staged.empty()) {
       // TMA pipeline: tile t+1 is in flight while tile t is computed
-      src << "  if (threadIdx.x == 0 && (long long)blockIdx.x * blockDim.x < dx_n) dx_issue(0, (long long)blockIdx.x * blockDim.x);\n";
       src << "  int dx_it = 0;\n";
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride, ++dx_it) {\n";
       src << "    const int dx_stg = dx_it & 1;\n";
@@ -3356,6 +3381,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           if (cu.aliasStage >= 0)
             etp = "(sb" + std::to_string(cu.aliasStage) + " + dx_sh" + std::to_string(cu.aliasStage) + ")";
           src << "    dx_tile_store4<" << rs.D << ">(" << etp << ", threadIdx.x, rowv" << rs.id << ");\n";
+          if (cu.warpTab) {
+            src << "    dx_warp_tab<" << rs.D << ", " << Kr << ", " << (std::getenv("DEXLET_WT_SIMPLE") ? 0 : 1) << ">(" << etp << ", rowk" << rs.id << ", wtab" << I
+                << " + dx_warp * " << (Kr + 1) * 32 << ");\n";
+            src << "    __syncthreads();  // every warp is done with this TMA stage\n";
+            continue;
+          }
           src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(" << etp << ", rowk" << rs.id
               << ", wc" << I << ", st" << I << ", pm" << I << ", acc" << I << ");\n";
           continue;
@@ -3389,6 +3420,11 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           break;
         case CellUse::TileRow: {
           int nacc = (int)((cu.width + g.threads - 1) / g.threads);
+          if (cu.warpTab) {
+            src << "  dx_warp_tab_flush<" << cu.rowD << ", " << cu.width / cu.rowD << ", " << g.threads / 32 << ">(wtab" << I
+                << ", part" << I << " + (long long)blockIdx.x * " << cu.width << ");\n";
+            break;
+          }
           if (cu.vec4) {
             std::string scratch = cu.aliasStage >= 0 ? "sb" + std::to_string(cu.aliasStage) : "et" + I;
             src << "  dx_tile_rows4_flush<" << cu.rowD << ", " << cu.width / cu.rowD << ", " << g.threads << ">(" << scratch

@@ -28,6 +28,7 @@
 
 #include "dx_device_src.inc"  // kDxDeviceSource: hand-written device runtime
 #include "dx_gemm_src.inc"    // kDxGemmSource: tcgen05 GEMM for contraction nests
+#include "dx_gmm_src.inc"     // kDxGmmSource: fused GMM objective + gradient
 
 namespace dxrt {
 
@@ -38,6 +39,7 @@ const std::string& lastError() { return g_lastError; }
 
 const char* deviceRuntimeSource() { return kDxDeviceSource; }
 const char* gemmSource() { return kDxGemmSource; }
+const char* gmmSource() { return kDxGmmSource; }
 
 static bool g_cuInit = false;
 static std::mutex g_mu;
@@ -289,7 +291,6 @@ int Ctx::loadModule(const std::string& source, CUmodule* out) {
 
 using namespace dxrt;
 
-struct dxc_ctx : dxrt::Ctx {};
 struct dxc_buf {
   dxrt::Ctx* ctx;
   CUdeviceptr ptr;

@@ -18,6 +18,7 @@ int ensureInit();
 int compileCubin(const std::string& source, std::string& cubin);
 const char* deviceRuntimeSource();
 const char* gemmSource();  // dx_gemm.cuh: tcgen05 contraction kernels
+const char* gmmSource();   // dx_gmm.cuh: fused GMM objective + gradient
 int loadNccl();
 
 struct Ctx {
@@ -42,3 +43,6 @@ struct Ctx {
 };
 
 }  // namespace dxrt
+
+// The C-ABI context handle is the runtime context itself.
+struct dxc_ctx : dxrt::Ctx {};

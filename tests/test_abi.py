@@ -116,3 +116,39 @@ def test_no_device_calls_fail_loudly():
     prog = dx.Program(P.histogram(10, 3), ctx=None)
     with pytest.raises(dx.DexError):
         prog.run()
+
+
+def test_gmm_header_symbols_exported():
+    """include/dexlet_gmm.h: every declared entry point is exported."""
+    with open(os.path.join(ROOT, "include", "dexlet_gmm.h")) as f:
+        syms = sorted(set(re.findall(r"\b(dxg_[a-z0-9_]+)\s*\(", f.read())))
+    assert len(syms) >= 10
+    lib = ctypes.CDLL(dx.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(dx.GMM_ABI_SYMBOLS) == syms
+
+
+def test_gmm_module_compiles_for_sm100a():
+    """The fused GMM kernels NVRTC-compile for sm_100a (no GPU needed) and the
+    contractions are tcgen05 MMAs (UTCHMMA in the SASS)."""
+    from paper_2104_05372_b200.csrc_sources import gmm_module_source  # noqa: F401
+    src = gmm_module_source()
+    lib = dx.lib()
+    lib.dxc_module_cubin.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    n = ctypes.c_size_t()
+    assert lib.dxc_module_cubin(src.encode(), None, 0, ctypes.byref(n)) == 0, lib.dxc_last_error()
+    buf = ctypes.create_string_buffer(n.value)
+    assert lib.dxc_module_cubin(src.encode(), buf, n.value, ctypes.byref(n)) == 0
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump unavailable")
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+        f.write(buf.raw)
+        f.flush()
+        sass = subprocess.run([cuobjdump, "-sass", f.name], capture_output=True, text=True).stdout
+    for k in dx.GMM_KERNELS:
+        assert f"Function : {k}" in sass, k
+    assert "UTCHMMA" in sass
+    assert "UBLKCP" in sass

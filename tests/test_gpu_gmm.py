@@ -1,0 +1,70 @@
+"""GPU parity of the fused GMM kernel class (include/dexlet_gmm.h) against the
+fp64 ADBench restatement in oracle/gmm.py (itself pinned by a closed form,
+finite differences and a loop transcription in tests/test_gmm_oracle.py).
+
+Tolerance: the reference's rtMaxRelDiff metric |a-b| / (1 + max(|a|,|b|))
+(eval.cpp:758-763) <= 1e-4 on the objective and on every gradient entry
+(fp32 inputs, bf16x3 tensor-core contractions, fp64 moments)."""
+import numpy as np
+import pytest
+
+from oracle import gmm as G
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / (1.0 + np.maximum(np.abs(a), np.abs(b))))) if a.size else 0.0
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2104_05372_b200 as dx
+    return dx.Context(0)
+
+
+@pytest.mark.parametrize("n,k", [(1000, 3), (4999, 10), (8192, 17), (20000, 24)])
+def test_gmm_objective_grad(ctx, n, k):
+    import paper_2104_05372_b200 as dx
+    a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=100 + k)
+    g = dx.GMM(ctx, 64, k, n)
+    err, da, dm, di = g(a, mu, icf, x)
+    werr, wda, wdm, wdi = G.gmm_objective_grad(a, mu, icf, x)
+    assert rel(err, werr) <= TOL, (err, werr)
+    assert rel(da, wda) <= TOL
+    assert rel(dm, wdm) <= TOL
+    assert rel(di, wdi) <= TOL
+
+
+def test_gmm_objective_only_and_wishart(ctx):
+    import paper_2104_05372_b200 as dx
+    n, k = 3000, 5
+    a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=7)
+    g = dx.GMM(ctx, 64, k, n)
+    err = g(a, mu, icf, x, gamma=0.7, m=2, grad=False)
+    assert rel(err, G.gmm_objective(a, mu, icf, x, 0.7, 2)) <= TOL
+    err2, da, dm, di = g(a, mu, icf, x, gamma=0.7, m=2, grad=True)
+    w = G.gmm_objective_grad(a, mu, icf, x, 0.7, 2)
+    assert rel(err2, w[0]) <= TOL and rel(di, w[3]) <= TOL and rel(da, w[1]) <= TOL
+
+
+def test_gmm_repeat_deterministic(ctx):
+    import paper_2104_05372_b200 as dx
+    n, k = 6000, 9
+    a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=3)
+    g = dx.GMM(ctx, 64, k, n)
+    r1 = g(a, mu, icf, x)
+    r2 = g(a, mu, icf, x)
+    assert r1[0] == r2[0]
+    for u, v in zip(r1[1:], r2[1:]):
+        assert np.array_equal(u, v)
+
+
+def test_gmm_bad_dimension(ctx):
+    import paper_2104_05372_b200 as dx
+    with pytest.raises(dx.DexError):
+        dx.GMM(ctx, 32, 4, 100)
