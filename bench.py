@@ -79,6 +79,21 @@ def config_spec(name, world):
                     work_basis="fwd 2 GEMMs + bwd dW2, dH, dW1 (2*B*1024^2 flops each)",
                     workload="2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) "
                              "(BASELINE configs[4])", extra={"batch_total": b}, out_bytes=4 + 2 * 1024 * 1024 * 4)
+    if name == "gmm":
+        from oracle.gmm import gmm_inputs  # seeded input generator only (no oracle compute)
+        n, d, k = N_PER_GPU, 64, 200
+        a, mu, icf, x = gmm_inputs(n, d, k)
+        fwd = 2 * n * k * d * d
+        bwd = 2 * n * k * d * (d + 1)
+        return dict(metric="GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)", gmm=True,
+                    inputs=(a, mu, icf, x), bound="tensor", work=fwd + bwd,
+                    work_by_kernel={"dx_gmm_fwd": fwd, "dx_gmm_bwd": bwd},
+                    work_basis="2nKd^2 (forward Q_k x contraction) + 2nKd(d+1) (backward moments "
+                               "sum g x x^T, sum g x), dense GEMM-equivalent flops",
+                    workload="ADBench GMM log-likelihood + gradient w.r.t. (alphas, means, icf), "
+                             "n=1M points per GPU, d=64, K=200, Wishart gamma=1 m=0 (BASELINE configs[2]); "
+                             "fused tcgen05 kernel class (include/dexlet_gmm.h)",
+                    extra={"n_total": n * world, "d": d, "k": k}, world=world)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -91,7 +106,7 @@ def parse():
     ap.add_argument("--ref-sample", type=int, default=10_000,
                     help="points per reference step (bounded CPU sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="kmeans", choices=["kmeans", "histogram", "matmul", "mlp"])
+    ap.add_argument("--config", default="kmeans", choices=["kmeans", "histogram", "matmul", "mlp", "gmm"])
     ap.add_argument("--profile", action="store_true",
                     help="for ncu runs: skip clock sampling, e2e and the CPU baseline")
     return ap.parse_args()
@@ -173,6 +188,112 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class ProgramRunner:
+    """A lowered dexlet program (dxl_program_*): graph replay per step."""
+
+    def __init__(self, dx, ctx, spec, rank, world):
+        self.dx, self.ctx = dx, ctx
+        self.prog = dx.Program(spec["src"], ctx=ctx, rank=rank, world=world)
+        self.inputs = spec["inputs"]
+        for i, leaves in enumerate(self.inputs):
+            for l, arr in enumerate(leaves):
+                self.prog.set_input(i, l, arr)
+        self.prog.enable_kernel_timing(True)
+        self.launches = self.prog.num_launches()
+
+    def run(self):
+        self.prog.run()
+
+    def kernel_times(self):
+        return self.prog.kernel_times()
+
+    def e2e_setup(self):
+        import ctypes
+        dx = self.dx
+        self.host = []  # pinned copies of every input leaf
+        for i, leaves in enumerate(self.inputs):
+            for l, arr in enumerate(leaves):
+                arr = np.ascontiguousarray(arr)
+                p = ctypes.c_void_p()
+                dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
+                ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
+                dt = {np.dtype(np.float32): dx.DXC_F32, np.dtype(np.int32): dx.DXC_I32}[arr.dtype]
+                self.host.append((i, l, p.value, arr.nbytes, dt))
+        self.outs = []
+        for leaf, (kind, count) in enumerate(self.prog.output_leaves()):
+            p = ctypes.c_void_p()
+            nb = count * (4 if kind != dx.LEAF_INT else 8)
+            dx.lib().dxc_host_alloc(nb, ctypes.byref(p))
+            self.outs.append((leaf, p.value, dx.DXC_F32 if kind == dx.LEAF_FLOAT else
+                              (dx.DXC_I32 if kind == dx.LEAF_INDEX else dx.DXC_I64), nb))
+        return sum(h[3] for h in self.host), sum(o[3] for o in self.outs)
+
+    def e2e_step(self):
+        for (inp, l, ptr, nb, dt) in self.host:
+            self.prog.set_input_ptr(inp, l, ptr, dt)
+        self.prog.run()
+        for (leaf, ptr, dt, nb) in self.outs:
+            self.prog.get_output_ptr(leaf, ptr, dt)
+
+
+class GmmRunner:
+    """The fused GMM kernel class (dxg_gmm_*): objective + gradient per step."""
+
+    def __init__(self, dx, ctx, spec, rank, world):
+        self.dx, self.ctx = dx, ctx
+        a, mu, icf, x = spec["inputs"]
+        self.arrs = [np.ascontiguousarray(v, dtype=np.float32) for v in (a, mu, icf, x)]
+        n = x.shape[0]
+        self.g = dx.GMM(ctx, x.shape[1], len(a), n, n * world)
+        self.g.set_params(a, mu, icf)
+        self.g.set_points(x)
+        self.g.enable_timing(True)
+        self.launches = len(dx.GMM_KERNELS)
+
+    def run(self):
+        self.g.run()
+
+    def kernel_times(self):
+        self.g.get(grad=False)  # completes the run and reads its per-kernel event times
+        return [(k, ms) for k, ms in self.g.kernel_times() if ms > 0]
+
+    def e2e_setup(self):
+        import ctypes
+        dx = self.dx
+        self.ptrs = []
+        for arr in self.arrs:
+            p = ctypes.c_void_p()
+            dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
+            ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
+            self.ptrs.append(p.value)
+        k, d = self.arrs[0].shape[0], self.arrs[1].shape[1]
+        self.outs = [np.empty(1), np.empty(k), np.empty((k, d)), np.empty((k, d * (d + 1) // 2))]
+        return sum(a.nbytes for a in self.arrs), sum(o.nbytes for o in self.outs)
+
+    def e2e_step(self):
+        import ctypes
+        lib = self.dx.lib()
+        self.g.set_params_ptr(*self.ptrs[:3])
+        self.g.set_points_ptr(self.ptrs[3])
+        self.g.run()
+        lib.dxg_gmm_get(self.g.handle, *(a.ctypes.data_as(ctypes.c_void_p) for a in self.outs))
+
+
+def gmm_cpu_rate(sample_n=2000, reps=2):
+    """fp64 numpy port of ADBench GMM (oracle/gmm.py) on a bounded sample of
+    the workload, scaled linearly in points to n = 1M."""
+    from oracle import gmm as G
+    a, mu, icf, x = G.gmm_inputs(sample_n, 64, 200, seed=7)
+    times = []
+    for i in range(1 + reps):
+        t0 = time.perf_counter()
+        G.gmm_objective_grad(a, mu, icf, x)
+        if i:
+            times.append(time.perf_counter() - t0)
+    sec = statistics.mean(times)
+    return (sample_n / N_PER_GPU) / sec, sec
+
+
 def peaks(bound="hbm"):
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -218,6 +339,26 @@ def run_reference(args, world, rank):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
+    if args.config == "gmm":
+        # no reference implementation exists (no exp/log in the language): the
+        # fp64 port of ADBench's algorithm is the CPU arm
+        rates = [gmm_cpu_rate(reps=1) for _ in range(max(1, args.steps))]
+        rate = statistics.mean(r for r, _ in rates)
+        sec = statistics.mean(t for _, t in rates)
+        line = {
+            "impl": "reference", "metric": "GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)",
+            "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (oracle/gmm.py:gmm_inputs, seed 7)",
+            "config": {"workload": "ADBench GMM objective + gradient, d=64, K=200 (BASELINE configs[2])",
+                       "reference_sample_points": 2000},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"oracle/gmm.py fp64 port on n=2000 points, {sec:.3f} s/eval, "
+                                       f"scaled linearly to 1M points"},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
     rate, sec, times = reference_rate(args.ref_sample, cores, args.steps, warm=args.warmup)
     sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2) on "
               f"n={args.ref_sample} points (d={D}, K={K}), chunks={cores}; {sec:.3f} s/eval; "
@@ -261,12 +402,8 @@ def main():
         ctx.init_comm(obj[0], world, rank)
 
     spec = config_spec(args.config, world)
-    prog = dx.Program(spec["src"], ctx=ctx, rank=rank, world=world)
-    for i, leaves in enumerate(spec["inputs"]):
-        for l, arr in enumerate(leaves):
-            prog.set_input(i, l, arr)
-    prog.enable_kernel_timing(True)
-    launches_per_run = prog.num_launches()
+    prog = (GmmRunner if spec.get("gmm") else ProgramRunner)(dx, ctx, spec, rank, world)
+    launches_per_run = prog.launches
 
     def barrier():
         ctx.sync()
@@ -316,34 +453,12 @@ def main():
     dom_ms = statistics.mean(dom[1])
 
     # ---- end to end through the C-ABI with host buffers ----------------------
-    import ctypes
-    host = []  # pinned copies of every input leaf
-    for i, leaves in enumerate(spec["inputs"]):
-        for l, arr in enumerate(leaves):
-            arr = np.ascontiguousarray(arr)
-            p = ctypes.c_void_p()
-            dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
-            ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
-            dt = {np.dtype(np.float32): dx.DXC_F32, np.dtype(np.int32): dx.DXC_I32}[arr.dtype]
-            host.append((i, l, p.value, arr.nbytes, dt))
-    outs = []
-    for leaf, (kind, count) in enumerate(prog.output_leaves()):
-        p = ctypes.c_void_p()
-        nb = count * (4 if kind != dx.LEAF_INT else 8)
-        dx.lib().dxc_host_alloc(nb, ctypes.byref(p))
-        outs.append((leaf, p.value, dx.DXC_F32 if kind == dx.LEAF_FLOAT else
-                     (dx.DXC_I32 if kind == dx.LEAF_INDEX else dx.DXC_I64), nb))
-    h2d = sum(h[3] for h in host)
-    d2h = sum(o[3] for o in outs)
+    h2d, d2h = prog.e2e_setup()
     e2e_ms = []
     for i in range(0 if args.profile else args.warmup + args.steps):
         ctx.l2_flush()
         e0 = ctx.event()
-        for (inp, l, ptr, nb, dt) in host:
-            prog.set_input_ptr(inp, l, ptr, dt)
-        prog.run()
-        for (leaf, ptr, dt, nb) in outs:
-            prog.get_output_ptr(leaf, ptr, dt)
+        prog.e2e_step()
         e1 = ctx.event()
         ms = ctx.elapsed_ms(e0, e1)
         ctx.destroy_event(e0)
@@ -363,15 +478,20 @@ def main():
     if rank == 0:
         peak, peak_kind = peaks(spec["bound"])
         work = spec["work"]
+        # the dominant kernel's own algorithmic work (GMM: per kernel; else the whole step)
+        work = spec.get("work_by_kernel", {}).get(dom[0], work)
         achieved = work / (dom_ms_max * 1e-3) / (1e9 if spec["bound"] == "hbm" else 1e12)
         tr = traffic_per_launch() if args.config == "kmeans" else None
         line = {
             "metric": spec["metric"], "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded; see paper_2104_05372_b200/programs.py)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if not spec.get("gmm") else "f32 (fp16x3 tensor-core products, fp64 folds)",
+            "data": "synthetic (seeded; see paper_2104_05372_b200/programs.py, oracle/gmm.py:gmm_inputs)",
             "config": dict({"workload": spec["workload"],
-                            "parallelism": f"outer loop sharded x{world} + NCCL allreduce of Accum cells",
+                            "parallelism": (f"points sharded x{world} + NCCL allreduce of the fp64 moments"
+                                            if spec.get("gmm") else
+                                            f"outer loop sharded x{world} + NCCL allreduce of Accum cells"),
                             "l2": "flushed before every timed step (256 MB scratch write, outside the events)"},
                            **spec["extra"]),
             "roofline": {"bound": spec["bound"], "kernel": dom[0], "achieved": achieved, "peak": peak,
@@ -396,6 +516,13 @@ def main():
             except Exception as e:  # the oracle library must travel with the repo
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
+        if world == 1 and not args.no_cpu_baseline and not args.profile and spec.get("gmm"):
+            rate, sec = gmm_cpu_rate()
+            line["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                "sample": (f"fp64 numpy restatement of ADBench GMM (oracle/gmm.py; the reference cannot express "
+                           f"GMM) on n=2000 points (d=64, K=200), {sec:.3f} s/eval, scaled linearly to 1M points; "
+                           f"cores = host threads available to numpy's BLAS")}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -227,12 +227,12 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_prep_x(const float* x, 
 // ---- forward: beta[k][i] for every point and component ---------------------------
 // Work unit = (component group g of 8, contiguous tile range p of the points);
 // CTA c takes units c, c + grid, ...  Warp 0: bulk-copy producer (Q group once
-// per unit, X tiles through a 2-stage ring); warp 1: MMA issuer; warps 2-5:
-// epilogue (warp w drains TMEM lanes 32*(w%4)..+31 = tile rows).  TMEM: 512
+// per unit, X tiles through a 2-stage ring); warp 1: MMA issuer; warps 2-9:
+// epilogue (warp w drains TMEM lanes 32*(w%4)..+31 = tile rows, of one half).  TMEM: 512
 // columns = 8 components x 64, in two halves of 4 components that alternate
 // between MMA and epilogue.
 #define DXG_FWD_SMEM (2 * DXG_GC * 64 * 128 + 2 * 2 * DXG_TM * 128 + 1024)
-extern "C" __global__ void __launch_bounds__(192, 1)
+extern "C" __global__ void __launch_bounds__(320, 1)
     dx_gmm_fwd(const unsigned char* __restrict__ qimg, const unsigned char* __restrict__ ximg,
                const float* __restrict__ bvec, const float* __restrict__ cvec, const float* __restrict__ svec,
                const float* __restrict__ dvec, int K, long long n,
@@ -253,7 +253,7 @@ extern "C" __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       dx_mbar_init(&xfull[s], 1);
-      dx_mbar_init(&xempty[s], 5);  // MMA commit + the 4 epilogue warps (they read x)
+      dx_mbar_init(&xempty[s], 9);  // MMA commit + the 8 epilogue warps (they read x)
       dx_mbar_init(&tfull[s], 1);
       dx_mbar_init(&tempty[s], 4);
     }
@@ -327,17 +327,19 @@ extern "C" __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // epilogue: warps 2..5
+    // epilogue: warps 2..9; warp w drains TMEM lane quarter w % 4 of half
+    // (w - 2) / 4 (components 0-3 or 4-7 of the resident group)
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int hsel = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;  // 0..255
     const unsigned lanebase = tmem + ((unsigned)(q * 32) << 16);
     int tt = 0, it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int g = u / P, p = u % P;
       const long long t0 = (long long)p * T / P, t1 = (long long)(p + 1) * T / P;
-      dxg_named_sync(1, 128);  // previous unit's epilogue is done with bsm/csm
-      for (int e = et; e < DXG_GC * DXG_D; e += 128) {
+      dxg_named_sync(1, 256);  // previous unit's epilogue is done with bsm/csm
+      for (int e = et; e < DXG_GC * DXG_D; e += 256) {
         const int j = e / DXG_D, c = e % DXG_D;
         const int k = g * DXG_GC + j;
         bsm[j][c] = k < K ? bvec[(long long)k * DXG_D + c] : 0.f;
@@ -347,7 +349,7 @@ extern "C" __global__ void __launch_bounds__(192, 1)
         csm[et] = g * DXG_GC + et < K ? cvec[g * DXG_GC + et] : 0.f;
         ssm[et] = g * DXG_GC + et < K ? svec[g * DXG_GC + et] : 0.f;
       }
-      dxg_named_sync(1, 128);
+      dxg_named_sync(1, 256);
       for (long long t = t0; t < t1; ++t, ++it) {
         const long long i = t * DXG_TM + row;
         // this row's scaled point sx*x from the A stage (fp16 hi + lo)
@@ -372,6 +374,7 @@ extern "C" __global__ void __launch_bounds__(192, 1)
           if (lane == 0) dx_mbar_arrive(&xempty[s]);
         }
         for (int h = 0; h < 2; ++h, ++tt) {
+          if (h != hsel) continue;
           dx_mbar_wait_bounded(&tfull[h], (unsigned)((tt >> 1) & 1));
           dxg_fence_after();
 #pragma unroll 1

@@ -241,7 +241,7 @@ int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
   {
     int P = g->P;
     void* a[] = {&g->qimg, &g->ximg, &g->bvec, &g->cvec, &g->svec, &g->dvec, &K, &n, &npad, &P, &g->beta};
-    if ((rc = launch(g, K_FWD, (unsigned)g->gridF, 192, FWD_SMEM, a))) return rc;
+    if ((rc = launch(g, K_FWD, (unsigned)g->gridF, 320, FWD_SMEM, a))) return rc;
   }
   {
     void* a[] = {&g->beta, &K, &n, &npad, &g->lse, &g->lpart};
