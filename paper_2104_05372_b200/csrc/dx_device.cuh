@@ -518,7 +518,8 @@ __device__ __forceinline__ void dx_grid_barrier(unsigned* counter) {
 // owns columns [8b, 8b+8); thread (c, g) sums rows g, g+R, ... in order, then a
 // fixed tree over the R row groups.  Deterministic for a fixed grid.
 template <class T, class P>
-__device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T scale, T* cell, bool counts) {
+__device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T scale, T* cell, bool counts,
+                                             bool store) {
   constexpr int C = 8;
   const int R = (blockDim.x / C) < 32 ? (blockDim.x / C) : 32;
   __shared__ T red[32][C];
@@ -542,7 +543,11 @@ __device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T s
       if (ty < h && ty + h < R) red[ty][tx] += red[ty + h][tx];
       __syncthreads();
     }
-    if (ty == 0 && c < width) cell[c] += counts ? red[0][tx] * scale : red[0][tx];
+    if (ty == 0 && c < width) {
+      const T v = counts ? red[0][tx] * scale : red[0][tx];
+      if (store) cell[c] = v;  // the cell's zero-fill was folded into this kernel
+      else cell[c] += v;
+    }
     __syncthreads();
   }
 }

@@ -43,10 +43,32 @@
 #define DXG_TM 128               // points per forward tile (MMA M)
 #define DXG_BC 64                // points per backward chunk (MMA K extent)
 #define DXG_BN 80                // backward MMA N: 64 dims + ones row + 15 zero rows
+#ifndef DXG_PROMO
 #define DXG_PROMO 1              // backward chunks per TMEM promotion (fp32 registers)
+#endif
 #define DXG_F64_EVERY 16         // promotions per fp64 spill (shared memory)
 #define DXG_FMAX 4               // backward partial slots per CTA
 #define DXG_FIN_SMEM (2 * DXG_D * (DXG_D + 1) * 8)
+// Backward A operand (g * (x - mu)^T) in tensor memory (written by the SIMT
+// producers with tcgen05.st, read by the MMA as [a-tmem]) instead of shared
+// memory: takes its 32 KB/chunk of writes and 48 KB/chunk of MMA reads off
+// the shared-memory pipe, which bounds the kernel otherwise.
+#ifndef DXG_TMEM_A
+#define DXG_TMEM_A 1
+#endif
+// TMEM columns of the backward kernel: D buffer b at 160 b (hi*hi at +0,
+// cross products at +80, 80 columns each); A stage s (hi 32 columns, lo 32)
+// at 320 + 64 s.  Three A stages (the producers run up to two chunks ahead
+// of the tensor core).
+#define DXG_NXS 5                // X^T (+ beta, lse) stages of the backward TMA ring
+#define DXG_TB_SMALL 80
+#define DXG_TD(b) ((b) * 160)
+#define DXG_TA(s) (320 + 64 * (s))
+#if DXG_TMEM_A
+#define DXG_NZS 3
+#else
+#define DXG_NZS 2
+#endif
 
 // ---- shared helpers ----------------------------------------------------------
 // byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
@@ -90,6 +112,19 @@ __device__ __forceinline__ void dxg_umma_f16(unsigned tmem, unsigned long long d
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void dxg_umma_f16_ta(unsigned tmem, unsigned ta, unsigned long long db, unsigned idesc,
+                                                unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
+      "r"(ta), "l"(db), "r"(idesc), "r"(accumulate));
+}
+#define DXG_TMEM_ST16(taddr, v)                                                                                \
+  asm volatile(                                                                                                \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])              \
+      : "memory")
 __device__ __forceinline__ void dxg_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void dxg_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void dxg_named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -462,7 +497,11 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
 #define DXG_XT_BYTES (2 * DXG_D * 128)          // hi + lo image of one chunk
 #define DXG_XB_BYTES (DXG_BN * 128)             // one split of the B operand (+ ones rows)
 #define DXG_Z_BYTES (2 * 128 * 128)             // hi + lo A operand of one chunk
-#define DXG_BWD_SMEM (2 * 2 * DXG_XB_BYTES + 2 * DXG_Z_BYTES + DXG_BN * 128 * 8 + 1024)
+#if DXG_TMEM_A
+#define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + DXG_BN * 128 * 8 + 1024)
+#else
+#define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_Z_BYTES + DXG_BN * 128 * 8 + 1024)
+#endif
 extern "C" __global__ void __launch_bounds__(448, 1)
     dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
@@ -471,12 +510,16 @@ extern "C" __global__ void __launch_bounds__(448, 1)
   extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
   unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
   unsigned char* bs = smem;                           // 2 stages x (hi 10 KB, lo 10 KB)
-  unsigned char* zs = smem + 2 * 2 * DXG_XB_BYTES;    // 2 stages x (hi 16 KB, lo 16 KB)
+  unsigned char* zs = smem + DXG_NXS * 2 * DXG_XB_BYTES;  // 2 stages x (hi 16 KB, lo 16 KB)
+#if DXG_TMEM_A
+  double* dacc = reinterpret_cast<double*>(zs);  // [80][128] fp64
+#else
   double* dacc = reinterpret_cast<double*>(zs + 2 * DXG_Z_BYTES);  // [80][128] fp64
+#endif
   // per stage: beta of the pair's two components and lse over the chunk's 64
   // points (bulk-copied with X^T, so the producers never wait on HBM)
-  __shared__ __align__(16) float gin[2][3][DXG_BC];
-  __shared__ __align__(8) unsigned long long xfull[2], xempty[2], zfull[2], zempty[2], tfull[2], tempty[2];
+  __shared__ __align__(16) float gin[DXG_NXS][3][DXG_BC];
+  __shared__ __align__(8) unsigned long long xfull[DXG_NXS], xempty[DXG_NXS], zfull[DXG_NZS], zempty[DXG_NZS], tfull[2], tempty[2];
   __shared__ unsigned tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NP = (K + 1) / 2;
@@ -486,17 +529,23 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      dx_mbar_init(&xfull[s], 1);
-      dx_mbar_init(&xempty[s], 1);
+      if (s < DXG_NZS - 2) {  // (third A stage)
+        dx_mbar_init(&zfull[2 + s], 8);
+        dx_mbar_init(&zempty[2 + s], 1);
+      }
       dx_mbar_init(&zfull[s], 8);
       dx_mbar_init(&zempty[s], 1);
       dx_mbar_init(&tfull[s], 1);
       dx_mbar_init(&tempty[s], 4);
     }
+    for (int s = 0; s < DXG_NXS; ++s) {
+      dx_mbar_init(&xfull[s], 1);
+      dx_mbar_init(&xempty[s], 1);
+    }
     dx_fence_mbar_init();
   }
   // constant B rows 64..79 of every stage: row 64 = 1.0 (hi) / 0 (lo), others 0
-  for (int e = threadIdx.x; e < 2 * 2 * 16 * 32; e += blockDim.x) {
+  for (int e = threadIdx.x; e < DXG_NXS * 2 * 16 * 32; e += blockDim.x) {
     const int st = e / (2 * 16 * 32), sp = (e / (16 * 32)) % 2, rr = (e / 32) % 16, w = e % 32;
     const unsigned val = (sp == 0 && rr == 0) ? 0x3c003c00u : 0u;  // fp16 1.0
     *reinterpret_cast<unsigned*>(bs + (st * 2 + sp) * DXG_XB_BYTES + (64 + rr) * 128 + w * 4) = val;
@@ -521,8 +570,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
         const long long k0 = pr * 2, k1 = (pr * 2 + 1 < K) ? pr * 2 + 1 : pr * 2;
         for (long long c = c0; c < c1; ++c, ++it) {
-          const int s = it & 1;
-          if (it >= 2) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it >> 1) - 1) & 1));
+          const int s = it % DXG_NXS;
+          if (it >= DXG_NXS) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it / DXG_NXS) - 1) & 1));
           dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES + 3 * DXG_BC * 4);
           const unsigned char* src = xtimg + c * DXG_XT_BYTES;
           dx_bulk_g2s(bs + (s * 2) * DXG_XB_BYTES, src, DXG_D * 128, &xfull[s]);
@@ -550,15 +599,29 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         }
         prevPair = pr;
         for (long long c = c0; c < c1; ++c, ++it) {
-          const int s = it & 1;
+          const int s = it % DXG_NZS;
           if (inb == 0 && pc >= 2) dx_mbar_wait_bounded(&tempty[pc & 1], (unsigned)(((pc >> 1) - 1) & 1));
-          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
-          dx_mbar_wait_bounded(&zfull[s], (unsigned)((it >> 1) & 1));
+          const int xs = it % DXG_NXS;
+          dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
+          dx_mbar_wait_bounded(&zfull[s], (unsigned)((it / DXG_NZS) & 1));
           dxg_fence_after();
           // buffer (pc & 1): columns [256 b, 256 b + 80) take hi*hi, [+128, +208)
           // the small hi*lo + lo*hi products (fewer truncating adds on the big sum)
-          const unsigned td = tmem + (unsigned)((pc & 1) * 256), ts = td + 128;
-          const unsigned bh = baddr + (unsigned)(s * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
+          const unsigned td = tmem + (unsigned)DXG_TD(pc & 1), ts = td + DXG_TB_SMALL;
+          const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
+#if DXG_TMEM_A
+          (void)zaddr;
+          const unsigned tah = tmem + (unsigned)DXG_TA(s), tal = tah + 32;
+#pragma unroll
+          for (int kk = 0; kk < DXG_BC / 16; ++kk) {
+            const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
+            const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
+            const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
+            dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
+            dxg_umma_f16_ta(ts, tah + kk * 8, dbl, idesc, acc);
+            dxg_umma_f16_ta(ts, tal + kk * 8, dbh, idesc, 1u);
+          }
+#else
           const unsigned zh = zaddr + (unsigned)(s * DXG_Z_BYTES), zl = zh + 128 * 128;
 #pragma unroll
           for (int kk = 0; kk < DXG_BC / 16; ++kk) {
@@ -571,7 +634,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             dxg_umma_f16(ts, ah, dbl, idesc, acc);
             dxg_umma_f16(ts, al, dbh, idesc, 1u);
           }
-          dx_umma_commit(&xempty[s]);
+#endif
+          dx_umma_commit(&xempty[xs]);
           dx_umma_commit(&zempty[s]);
           if (++inb == DXG_PROMO) {
             dx_umma_commit(&tfull[pc & 1]);
@@ -592,10 +656,18 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     // g is computed once per (component, point): lane q of a warp evaluates
     // point hh*32+q and the warp shares the 32 values through shared memory.
     const int pt = threadIdx.x - 64;       // 0..255
-    const int r = pt & 127, hh = pt >> 7;  // row of Z, point half
-    const int kl = r >> 6, b = r & 63;
     const int pw = pt >> 5;                // producer warp 0..7
+#if DXG_TMEM_A
+    // TMEM lane access: warp w owns lanes 32 (w % 4) .. +31 = rows of A
+    const int r = (warp & 3) * 32 + lane, hh = pw >> 2;
+    const bool wrow = (r & 32) == 0;       // warps holding rows b < 32 accumulate W
+    const int wk0a = 2, wk0b = 6, wk1a = 0, wk1b = 4;  // producer warps of the b<32 rows of k_local 0 / 1
+#else
+    const int r = pt & 127, hh = pt >> 7;  // row of Z, point half
     const bool wrow = (pw & 1) == 0;       // warps holding rows b < 32 accumulate W
+    const int wk0a = 0, wk0b = 4, wk1a = 2, wk1b = 6;
+#endif
+    const int kl = r >> 6, b = r & 63;
     __shared__ __align__(16) float gw[8][32];
     __shared__ float wred[8];
     const float sx = dxg_scale_for(__uint_as_float(*xmax));
@@ -608,7 +680,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       dxg_named_sync(2, 256);
       if (lane == 0) wred[pw] = w;
       dxg_named_sync(2, 256);
-      if (pt < 2) wpart[((long long)blockIdx.x * DXG_FMAX + slot) * 2 + pt] = wred[2 * pt] + wred[2 * pt + 4];
+      if (pt < 2)
+        wpart[((long long)blockIdx.x * DXG_FMAX + slot) * 2 + pt] = pt == 0 ? wred[wk0a] + wred[wk0b] : wred[wk1a] + wred[wk1b];
       ++slot;
     };
     for (long long u = u0; u < u1; ++u) {
@@ -623,21 +696,26 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         mub = live ? means[(long long)k * DXG_D + b] * sx : 0.f;
       }
       for (long long c = c0; c < c1; ++c, ++it) {
-        const int s = it & 1;
-        if (it >= 2) dx_mbar_wait_bounded(&zempty[s], (unsigned)(((it >> 1) - 1) & 1));
-        dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+        const int s = it % DXG_NZS;
+        const int xs = it % DXG_NXS;
+        if (it >= DXG_NZS) dx_mbar_wait_bounded(&zempty[s], (unsigned)(((it / DXG_NZS) - 1) & 1));
+        dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
         {
           const int q = hh * 32 + lane;
-          const float gg = __expf(gin[s][kl][q] - gin[s][2][q]);
+          const float gg = __expf(gin[xs][kl][q] - gin[xs][2][q]);
           const float gq = (live && c * DXG_BC + q < n) ? gg : 0.f;
           if (wrow) wacc += gq;
           gw[pw][lane] = gq;
           __syncwarp();
         }
-        const unsigned char* xh = bs + (s * 2) * DXG_XB_BYTES;
+        const unsigned char* xh = bs + (xs * 2) * DXG_XB_BYTES;
         const unsigned char* xl = xh + DXG_XB_BYTES;
+#if DXG_TMEM_A
+        unsigned th[16], tl[16];
+#else
         unsigned char* zh = zs + s * DXG_Z_BYTES;
         unsigned char* zl = zh + 128 * 128;
+#endif
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {  // 4 x 8 points = 16-byte chunks
           const int pcol = hh * 32 + cc * 8;
@@ -655,11 +733,29 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
             dxg_split2(gv[2 * w] * x0, gv[2 * w + 1] * x1, oh[w], ol[w]);
           }
+#if DXG_TMEM_A
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            th[cc * 4 + w] = oh[w];
+            tl[cc * 4 + w] = ol[w];
+          }
+#else
           const unsigned off_z = dxg_sw((unsigned)r, (unsigned)pcol);
           *reinterpret_cast<uint4*>(zh + off_z) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
           *reinterpret_cast<uint4*>(zl + off_z) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+#endif
         }
+#if DXG_TMEM_A
+        {
+          const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(DXG_TA(s) + hh * 16);
+          DXG_TMEM_ST16(ta, th);
+          DXG_TMEM_ST16(ta + 32, tl);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          dxg_fence_before();
+        }
+#else
         dx_fence_proxy_async();  // generic-proxy writes -> tensor-core reads
+#endif
         __syncwarp();
         if (lane == 0) dx_mbar_arrive(&zfull[s]);
       }
@@ -692,8 +788,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 #pragma unroll
       for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
         unsigned v[16], w[16];
-        DXG_TMEM_LD16(lanebase + (unsigned)(b * 256 + j0), v);
-        DXG_TMEM_LD16(lanebase + (unsigned)(b * 256 + 128 + j0), w);
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + DXG_TB_SMALL + j0), w);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);

@@ -7,6 +7,7 @@
 // sum between moments and finish when the points are sharded over ranks.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -26,9 +27,12 @@ constexpr int TM = 128;
 constexpr int BC = 64;
 constexpr int BN = 80;
 constexpr int FMAX = 4;
+constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
 constexpr int FWD_SMEM = 2 * GC * 64 * 128 + 2 * 2 * TM * 128 + 1024;
-constexpr int BWD_SMEM = 2 * 2 * (BN * 128) + 2 * (2 * 128 * 128) + BN * 128 * 8 + 1024;
+inline int bwdSmem() {
+  return NXS * 2 * (BN * 128) + (std::getenv("DEXLET_GMM_SMEM_A") ? 2 * (2 * 128 * 128) : 0) + BN * 128 * 8 + 1024;
+}
 constexpr int FIN_SMEM = 2 * D * (D + 1) * 8;
 enum { K_ABSMAX, K_PREPQ, K_PREPX, K_FWD, K_LSE, K_SUM, K_BWD, K_MOM, K_FIN, K_N };
 const char* kNames[K_N] = {"dx_gmm_absmax", "dx_gmm_prep_q", "dx_gmm_prep_x", "dx_gmm_fwd", "dx_gmm_lse",
@@ -138,12 +142,15 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   g->P2 = pickP2(g->NP, g->C, sms);
   g->gridB = (int)std::min<long long>(sms, (long long)g->NP * g->P2);
   g->gridL = (int)std::min<long long>(4 * sms, (g->n + 255) / 256);
-  std::string src = std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
+  // DEXLET_GMM_SMEM_A=1: backward A operand staged in shared memory (A/B)
+  std::string src = std::string(std::getenv("DEXLET_GMM_SMEM_A") ? "#define DXG_TMEM_A 0\n" : "");
+  if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
+  src += std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
   if ((rc = ctx->loadModule(src, &g->mod))) { delete g; return rc; }
   for (int i = 0; i < K_N; ++i)
     if ((rc = check(cuModuleGetFunction(&g->fn[i], g->mod, kNames[i]), kNames[i]))) { delete g; return rc; }
   if ((rc = check(cuFuncSetAttribute(g->fn[K_FWD], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, FWD_SMEM), "smem fwd")) ||
-      (rc = check(cuFuncSetAttribute(g->fn[K_BWD], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, BWD_SMEM), "smem bwd")) ||
+      (rc = check(cuFuncSetAttribute(g->fn[K_BWD], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bwdSmem()), "smem bwd")) ||
       (rc = check(cuFuncSetAttribute(g->fn[K_FIN], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, FIN_SMEM), "smem fin"))) {
     delete g;
     return rc;
@@ -254,7 +261,7 @@ int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
     if ((rc = check(cuMemsetD8Async(g->ppart, 0xff, (size_t)g->gridB * FMAX * 4, s), "memset ppart"))) return rc;
     int P2 = g->P2;
     void* a[] = {&g->xtimg, &g->beta, &g->lse, &g->means, &g->xmax, &K, &n, &npad, &P2, &g->dpart, &g->wpart, &g->ppart};
-    if ((rc = launch(g, K_BWD, (unsigned)g->gridB, 448, BWD_SMEM, a))) return rc;
+    if ((rc = launch(g, K_BWD, (unsigned)g->gridB, 448, bwdSmem(), a))) return rc;
     int nslot = g->gridB * FMAX;
     void* b[] = {&g->dpart, &g->wpart, &g->ppart, &nslot, &g->xmax, &g->mom};
     if ((rc = launch(g, K_MOM, (unsigned)K, 256, 0, b))) return rc;

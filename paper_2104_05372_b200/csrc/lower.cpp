@@ -2650,6 +2650,24 @@ class Lowering {
   std::vector<KernelBody> pending;
   bool flushing = false;
 
+  // The buffer's pending zero-fill, if the last step touching it is one: the
+  // next kernel can overwrite the buffer instead (the step is dropped).
+  bool takeZero(int b) {
+    for (size_t i = plan.steps.size(); i-- > 0;) {
+      Step& st = plan.steps[i];
+      bool refs = st.buf == b || st.buf2 == b;
+      for (auto& a : st.args) refs |= (a.k == KArg::Buf || a.k == KArg::TMap) && a.buf == b;
+      if (!refs) continue;
+      if (st.k == Step::Zero && st.buf == b && st.off == 0 && !st.dead &&
+          (st.elems <= 0 || st.elems >= plan.bufs[b].elems)) {
+        st.dead = true;
+        return true;
+      }
+      return false;
+    }
+    return false;
+  }
+
   void addStep(const Step& st) {
     if (st.k != Step::Zero && !pending.empty() && !flushing) flushPending();
     plan.steps.push_back(st);
@@ -3403,7 +3421,10 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     if (tileCell < 0 && g.tile && !g.staged.empty())
       src << "    __syncthreads();  // every thread is done with this TMA stage\n";
     src << "  }\n";
-    src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
+    // cooperative kernels that are the first writer of the error flag reset
+    // it themselves (block 0, before the grid barrier; flags are raised after it)
+    const bool coopErr = coop && takeZero(plan.errFlagBuf);
+    if (!coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
     // epilogue: block partials
     for (size_t i = 0; i < g.cells.size(); ++i) {
       CellUse& cu = g.cells[i];
@@ -3445,15 +3466,19 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       }
     }
     if (coop) {
+      if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
       src << "  dx_grid_barrier(p" << syncBuf << ");\n";
+      if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
       for (size_t i = 0; i < g.cells.size(); ++i) {
         CellUse& cu = g.cells[i];
         if (cu.partialBuf < 0) continue;
         std::string ct = ctype(plan.bufs[cu.targetBuf].kind);
         bool counts = cu.strat == CellUse::Count;
+        // a cell whose only pending step is its zero-fill is overwritten
+        const bool store = takeZero(cu.targetBuf);
         src << "  dx_coop_fold<" << ct << ", " << (counts ? "unsigned" : "dx_f") << ">(part" << i << ", "
             << cu.width << "LL, (" << ct << ")" << litF(counts ? cu.constVal : 1.0, true) << ", " << cu.pname
-            << ", " << (counts ? "true" : "false") << ");\n";
+            << ", " << (counts ? "true" : "false") << ", " << (store ? "true" : "false") << ");\n";
       }
     }
     src << "}\n\n";
@@ -3934,14 +3959,14 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
   }
   std::vector<Step> kept;
   for (auto& st : L.plan.steps) {
-    if (st.k == Step::Zero && !live[st.buf]) continue;
+    if ((st.k == Step::Zero && !live[st.buf]) || st.dead) continue;
     kept.push_back(st);
   }
   // kernel step indices referenced by partial buffers / finalize steps moved
   std::vector<int> remap(L.plan.steps.size(), -1);
   for (size_t i = 0, j = 0; i < L.plan.steps.size(); ++i) {
     const Step& st = L.plan.steps[i];
-    if (st.k == Step::Zero && !live[st.buf]) continue;
+    if ((st.k == Step::Zero && !live[st.buf]) || st.dead) continue;
     remap[i] = (int)j++;
   }
   for (auto& st : kept)

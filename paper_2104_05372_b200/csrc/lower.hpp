@@ -77,6 +77,7 @@ struct Step {
   int smem = 0;           // dynamic shared memory bytes
   int minGrid = 0;        // ordinals per thread (U)
   bool coop = false;      // cooperative launch (in-kernel grid barrier + finalize)
+  bool dead = false;      // Zero step taken over by the first kernel writing the buffer
   long long fixedGrid = 0;  // >0: launch exactly this many blocks (tile kernels: GEMM, transpose)
   // Finalize: partial buf -> cell (buf, off, elems = width)
   enum FinK { Seq, Tree, Count } fin = Seq;

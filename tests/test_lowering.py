@@ -42,12 +42,16 @@ def _sass(source):
 def test_kmeans_value_and_grad_is_one_fused_kernel():
     """Forward tape inlined into both consumers (no HBM tape), the cotangent
     broadcast folded (accum-to-map), cost and gradient loops fused
-    horizontally: one kernel + two finalizes."""
+    horizontally: one cooperative kernel that also folds the partials and
+    owns the zero-fills (the plan is that single launch)."""
     prog = dx.Program(P.kmeans_cost_grad(100_000, 16, 64), ctx=None)
     ks = _kernels(prog.plan)
     assert len(ks) == 1, prog.plan
+    assert "zero b" not in prog.plan.split("---")[0], prog.plan
     src = prog.source
-    assert "dx_tile_rows4<16, 64" in src          # tile-sorted row reduction for dC
+    assert "dx_warp_tab<16, 64" in src            # warp-private row tables for dC
+    assert "dx_warp_tab_flush<16, 64" in src
+    assert ", true);" in src                      # fold overwrites the (never zeroed) cell
     assert "dx_block_sum(rp" in src               # register partial for the cost
     assert "dx_tma_2d(" in src                    # TMA tensor tiles of the points
     sass = _sass(src)
