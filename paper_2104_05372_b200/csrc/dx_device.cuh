@@ -434,14 +434,18 @@ template <int D, int K, int NW>
 __device__ __forceinline__ void dx_warp_tab_flush(const float* tabs, float* part) {
   constexpr int G = 32 / D;
   __syncthreads();
-  for (int e = threadIdx.x; e < K * D; e += blockDim.x) {
-    const int k = e / D, j = e - (e / D) * D;
-    float s = 0.f;
+  // float4 columns: entry quad (k, 4q..4q+3)
+  for (int e = threadIdx.x; e < K * D / 4; e += blockDim.x) {
+    const int k = e / (D / 4), j = 4 * (e - k * (D / 4));
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int w = 0; w < NW; ++w)
 #pragma unroll
-      for (int g = 0; g < G; ++g) s += tabs[(w * (K + 1) + k) * 32 + g * D + j];
-    part[e] = s;
+      for (int g = 0; g < G; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(tabs + (w * (K + 1) + k) * 32 + g * D + j);
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      }
+    *reinterpret_cast<float4*>(part + k * D + j) = s;
   }
 }
 

@@ -3293,7 +3293,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
             long long wt = (long long)(g.threads / 32) * (Kr + 1) * 32;
             src << "  float* wtab" << I << " = (float*)(dx_smem + " << cu.smemOff << ");\n";
             src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff + wt * 4 << ");\n";
-            src << "  for (int t = threadIdx.x; t < " << wt << "; t += blockDim.x) wtab" << I << "[t] = 0.f;\n";
+            src << "  for (int t = threadIdx.x; t < " << wt / 4 << "; t += blockDim.x) reinterpret_cast<float4*>(wtab" << I
+                << ")[t] = make_float4(0.f, 0.f, 0.f, 0.f);\n";
             needSync = true;
             break;
           }
