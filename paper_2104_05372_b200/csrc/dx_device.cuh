@@ -86,6 +86,9 @@ __device__ __forceinline__ void dx_mbar_expect_tx(unsigned long long* bar, unsig
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dx_smem_addr(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void dx_mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dx_smem_addr(bar)) : "memory");
+}
 // global -> shared bulk copy (TMA, 1-D), completion counted on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void dx_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {

@@ -69,9 +69,6 @@ __device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
   lo = dx_tf32_rn((float)(v - (double)hi));
 }
 
-__device__ __forceinline__ void dx_mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dx_smem_addr(bar)) : "memory");
-}
 
 #define DX_TMEM_LD32(taddr, v)                                                                                    \
   asm volatile(                                                                                                   \

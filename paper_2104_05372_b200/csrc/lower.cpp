@@ -3139,6 +3139,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   int tileCell = -1;
   for (size_t i = 0; i < g.cells.size(); ++i)
     if (g.cells[i].strat == CellUse::TileRow) tileCell = (int)i;
+  // WarpTab kernels fed by the TMA ring: warps share nothing but the stages
+  const bool warpTabRing = tileCell >= 0 && g.cells[tileCell].warpTab && !g.staged.empty() &&
+                           std::getenv("DEXLET_WT_RING") != nullptr;  // opt-in: measured no faster
   int stageOff = (smem + 15) / 16 * 16;
   if (maxRowD > 0) smem = stageOff + warps * (32 * (int)(maxRowD + 1) + 32) * esize;
   // TMA staging areas
@@ -3229,12 +3232,13 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     bool needSync = false;
     if (!g.staged.empty()) {
-      src << "  __shared__ __align__(8) unsigned long long dx_bar[2];\n";
+      src << "  __shared__ __align__(8) unsigned long long dx_bar[2], dx_empty[2];\n";
       for (int b : g.staged) {
         std::string ct = ctype(plan.bufs[b].kind);
         src << "  " << ct << "* sb" << b << " = (" << ct << "*)(dx_smem + " << stageAt[b] << ");\n";
       }
-      src << "  if (threadIdx.x == 0) { dx_mbar_init(&dx_bar[0], 1); dx_mbar_init(&dx_bar[1], 1); dx_fence_mbar_init(); }\n";
+      src << "  if (threadIdx.x == 0) { dx_mbar_init(&dx_bar[0], 1); dx_mbar_init(&dx_bar[1], 1); dx_mbar_init(&dx_empty[0], "
+          << g.threads / 32 << "); dx_mbar_init(&dx_empty[1], " << g.threads / 32 << "); dx_fence_mbar_init(); }\n";
       // thread 0 streams the rows of tile `tb` into stage `stg` (16-byte
       // aligned superset of the byte range; readers add the shift)
       src << "  auto dx_issue = [&](int stg, long long tb) {\n";
@@ -3340,7 +3344,14 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "  int dx_it = 0;\n";
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride, ++dx_it) {\n";
       src << "    const int dx_stg = dx_it & 1;\n";
-      src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
+      if (warpTabRing) {
+        // the stage of tile it-1 is reused once every warp has arrived on its
+        // empty barrier: only the issuing thread waits, the other warps go on
+        src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { if (dx_it >= 1) dx_mbar_wait(&dx_empty[dx_stg ^ 1], "
+               "(unsigned)(((dx_it - 1) >> 1) & 1)); dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
+      } else {
+        src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
+      }
       for (int b : g.staged) {
         int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
         auto lb = g.streamUse[b];
@@ -3403,7 +3414,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
           if (cu.warpTab) {
             src << "    dx_warp_tab<" << rs.D << ", " << Kr << ", " << (std::getenv("DEXLET_WT_SIMPLE") ? 0 : 1) << ">(" << etp << ", rowk" << rs.id << ", wtab" << I
                 << " + dx_warp * " << (Kr + 1) * 32 << ");\n";
-            src << "    __syncthreads();  // every warp is done with this TMA stage\n";
+            if (warpTabRing) src << "    __syncwarp();\n    if (dx_lane == 0) dx_mbar_arrive(&dx_empty[dx_stg]);  // this warp is done with the stage\n";
+            else src << "    __syncthreads();  // every warp is done with this TMA stage\n";
             continue;
           }
           src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(" << etp << ", rowk" << rs.id

@@ -1,5 +1,5 @@
 # A/B of lowering strategies on the k-means hot kernel (env knobs of lower.cpp)
-python -m pytest tests -m gpu -x -q -k "kmeans or parity or kat" 2>&1 | tail -2
-for env in "" "DEXLET_NO_TMA=1" "DEXLET_TILE_NT=128" "DEXLET_WT_SIMPLE=1" $EXTRA_AB; do
+python -m pytest tests -m gpu -x -q -k "kmeans or parity or kat or gemm or full" 2>&1 | tail -2
+for env in "" "DEXLET_WT_BARRIER=1" "DEXLET_TILE_NT=128" $EXTRA_AB; do
   echo "== $env"; env $env timeout 120 python scripts/quick_perf.py kmeans 2>&1 | grep -E "kmeans cost"
 done
