@@ -1487,6 +1487,7 @@ class Lowering {
 
   // Kernel drivers (defined after KGen helpers).
   HV loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool serial, Span sp);
+  HV flattenEffectNest(const HEnvP& env, const EFor& f, const DescPtr& d);
   HV loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs);
   HV splitMaterialize(const HV& lz);
   ValuePtr typeValue(const DTy& t);
@@ -2403,10 +2404,113 @@ class Lowering {
     return k;
   }
 
+  // In-kernel accum-to-map (the kernel twin of tryAccumToMap): the action
+  //   <lets not touching r>; let t = for j. (<pure lets>; sl = r!j' ; sl += v); t
+  // with j' = j or reverse j and v independent of r makes the final value the
+  // table `for j'. v`, kept lazy (inlined at its uses) instead of a local
+  // array filled by a loop.  This is the per-row cotangent broadcast of every
+  // transposed `sum` inside a kernel (autodiff.cpp:760-772).
+  KV accumToMapK(KGen& g, const KScope& s0, const ERunAccum& r, const DTy& payload) {
+    if (opt.noFusion || payload->k != DType::Table || payload->a->k != DType::Float) return nullptr;
+    const Name rref = r.action.ref;
+    std::vector<const ELet*> pre;
+    ExprPtr cur = r.action.body;
+    const EFor* f = nullptr;
+    while (const auto* l = as<ELet>(cur)) {
+      if (const auto* ff = as<EFor>(l->bound)) {
+        const auto* ret = as<ERet>(l->body);
+        const auto* rv = ret ? as<VVar>(ret->value) : nullptr;
+        if (!rv || rv->name != l->binder) return nullptr;
+        f = ff;
+        break;
+      }
+      for (const Name& n : freeVars(l->bound))
+        if (n == rref) return nullptr;
+      pre.push_back(l);
+      cur = l->body;
+    }
+    if (!f) return nullptr;
+    // the loop body: lets ending in `sl += v`, then a trivial return
+    std::vector<const ELet*> lets;
+    ExprPtr b = f->body;
+    while (const auto* l = as<ELet>(b)) {
+      lets.push_back(l);
+      b = l->body;
+    }
+    int accIdx = -1;
+    for (size_t i = 0; i < lets.size(); ++i)
+      if (as<EAccum>(lets[i]->bound)) {
+        if (accIdx >= 0) return nullptr;
+        accIdx = (int)i;
+      }
+    if (accIdx < 0) return nullptr;
+    const auto* acc = as<EAccum>(lets[accIdx]->bound);
+    const auto* refVar = as<VVar>(acc->ref);
+    if (!refVar) return nullptr;
+    const ESlice* sl = nullptr;
+    for (int i = 0; i < accIdx; ++i)
+      if (lets[i]->binder == refVar->name) sl = as<ESlice>(lets[i]->bound);
+    const auto* root = sl ? as<VVar>(sl->ref) : nullptr;
+    if (!root || root->name != rref) return nullptr;
+    const auto* ix = as<VVar>(sl->idx);
+    if (!ix) return nullptr;
+    bool reversed = false;
+    if (ix->name != f->binder) {
+      const ELet* rl = nullptr;
+      for (int i = 0; i < accIdx; ++i)
+        if (lets[i]->binder == ix->name) rl = lets[i];
+      const auto* u = rl ? as<EUnOp>(rl->bound) : nullptr;
+      const auto* uv = u && u->op == UnOp::ReverseIndex ? as<VVar>(u->v) : nullptr;
+      if (!uv || uv->name != f->binder) return nullptr;
+      reversed = true;
+    }
+    for (const Name& n : freeVars(acc->value))
+      if (n == rref || n == refVar->name) return nullptr;
+    for (size_t i = accIdx + 1; i < lets.size(); ++i)
+      if (!as<ERet>(lets[i]->bound)) return nullptr;
+    if (!as<ERet>(b)) return nullptr;
+    ExprPtr body = eRet(acc->value);
+    for (int i = accIdx - 1; i >= 0; --i) {
+      if (lets[i]->binder == refVar->name) continue;
+      for (const Name& n : freeVars(lets[i]->bound))
+        if (n == rref || n == refVar->name) return nullptr;
+      if (!pureBody(lets[i]->bound)) return nullptr;
+      body = eLet(lets[i]->binder, lets[i]->annot, lets[i]->bound, body);
+    }
+    DescPtr d = resolveDesc(f->annot, kernelLook(g, s0));
+    if (!descEq(d, payload->desc)) return nullptr;
+    // evaluate the prefix lets, then the map
+    KScope s = s0;
+    for (const ELet* l : pre) s = kbind(s, l->binder, kexpr(g, s, l->bound, l->annot));
+    Name m = f->binder;
+    if (reversed) {
+      m = NameSupply::fresh("m");
+      body = eLet(f->binder, f->annot, eUn(UnOp::ReverseIndex, vVar(m)), body);
+    }
+    auto k = std::make_shared<KVal>();
+    k->k = KVal::Lazy;
+    auto lz = std::make_shared<LazyK>();
+    lz->binder = m;
+    lz->desc = d;
+    lz->body = body;
+    lz->scope = s;
+    lz->covered = s.covered;
+    lz->cheap = cheapBody(body);
+    lz->key = m.uid;
+    k->ty = payload;
+    k->lz = lz;
+    auto unitTab = std::make_shared<KVal>();
+    unitTab->k = KVal::Table;
+    unitTab->ty = tTable(d, tUnit());
+    return kPair(unitTab, k);
+  }
+
   KV runAccumK(KGen& g, const KScope& s, const ERunAccum& r, const ExprPtr& e) {
     const auto* ra = as<VRefType>(r.action.refAnnot);
     if (!ra) fail(ErrCode::Internal, "runAccum reached the lowering unannotated", e->span);
     DTy payload = resolveType(ra->payload, kernelLook(g, s));
+    if (!std::getenv("DEXLET_NO_KMAP"))
+      if (KV m = accumToMapK(g, s, r, payload)) return m;
     std::vector<Slot> slots = localArrays(g, payload, true);
     std::vector<LeafInfo> plv = leaves(payload);
     for (size_t l = 0; l < slots.size(); ++l)
@@ -3574,6 +3678,7 @@ HV Lowering::loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool 
     return requestKernel(kb, true, nullptr, nullptr);
   }
   if (HV gm = contractNest(env, f, d)) return gm;
+  if (HV fl = flattenEffectNest(env, f, d)) return fl;
   KernelBody kb;
   kb.desc = d;
   kb.dims = {d};
@@ -3584,6 +3689,105 @@ HV Lowering::loopKernel(const HEnvP& env, const EFor& f, const DescPtr& d, bool 
   kb.env = env;
   kb.note = "parallel for " + printName(f.binder);
   return requestKernel(kb, false, nullptr, nullptr);
+}
+
+// Effectful nests `for i. <pure lets>; (let t = for j. B; t)` whose outer loop
+// alone cannot fill the GPU (the MLP's dY rows: 8192 x 1024) run over the
+// flattened (i, j) space, j fastest: the pure lets are recomputed per element
+// (they are per-row scalars), and per-row writes r!i!j become coalesced
+// owner writes instead of one 4 KB-strided row per thread.
+static bool hasLoop(const ExprPtr& e) {
+  bool found = false;
+  std::function<void(const ExprPtr&)> scan = [&](const ExprPtr& x) {
+    if (found) return;
+    std::visit(
+        [&](const auto& n) {
+          using T = std::decay_t<decltype(n)>;
+          if constexpr (std::is_same_v<T, EFor>) found = true;
+          else if constexpr (std::is_same_v<T, ELet>) { scan(n.bound); scan(n.body); }
+          else if constexpr (std::is_same_v<T, ECase>) { scan(n.leftBody); scan(n.rightBody); }
+          else if constexpr (std::is_same_v<T, ERunState> || std::is_same_v<T, ERunAccum>) scan(n.action.body);
+        },
+        x->node);
+  };
+  scan(e);
+  return found;
+}
+
+// A runAccum whose action is loop-free lets followed by the broadcast loop
+// `for j. r!j' += v` (what accumToMapK turns into a lazy map): cheap to
+// recompute per element once lowered.
+static bool mapLikeRunAccum(const ERunAccum& r) {
+  ExprPtr cur = r.action.body;
+  while (const auto* l = as<ELet>(cur)) {
+    if (const auto* f = as<EFor>(l->bound)) {
+      const auto* ret = as<ERet>(l->body);
+      const auto* rv = ret ? as<VVar>(ret->value) : nullptr;
+      if (!rv || rv->name != l->binder || hasLoop(f->body)) return false;
+      int accs = 0;
+      for (ExprPtr b = f->body; const auto* bl = as<ELet>(b); b = bl->body) accs += as<EAccum>(bl->bound) != nullptr;
+      return accs == 1;
+    }
+    if (hasLoop(l->bound)) return false;
+    cur = l->body;
+  }
+  return false;
+}
+
+HV Lowering::flattenEffectNest(const HEnvP& env, const EFor& f, const DescPtr& d) {
+  if (opt.noFusion || std::getenv("DEXLET_NO_FLATTEN_EFFECT")) return nullptr;
+  const long long n = size(d);
+  if (n >= 148LL * 1024) return nullptr;  // the outer loop fills the GPU already
+  std::vector<const ELet*> pre;
+  ExprPtr cur = f.body;
+  const EFor* inner = nullptr;
+  const ELet* innerLet = nullptr;
+  while (const auto* l = as<ELet>(cur)) {
+    if (const auto* ff = as<EFor>(l->bound)) {
+      const auto* ret = as<ERet>(l->body);
+      const auto* rv = ret ? as<VVar>(ret->value) : nullptr;
+      if (!rv || rv->name != l->binder) return nullptr;
+      inner = ff;
+      innerLet = l;
+      break;
+    }
+    if (!pureBody(l->bound) || as<ERunState>(l->bound) || as<EFor>(l->bound)) return nullptr;
+    // recomputed per element: only loop-free lets, or runAccums that are a
+    // loop-free chain ending in the accum-to-map broadcast
+    if (const auto* ra = as<ERunAccum>(l->bound)) {
+      if (!mapLikeRunAccum(*ra)) return nullptr;
+    } else if (hasLoop(l->bound)) {
+      return nullptr;
+    }
+    pre.push_back(l);
+    cur = l->body;
+  }
+  if (!inner || pureBody(inner->body)) return nullptr;
+  DescPtr d2;
+  try {
+    d2 = resolveDesc(inner->annot, hostLook(env));
+  } catch (const DexError&) {
+    return nullptr;
+  }
+  if (size(d2) < 32) return nullptr;
+  (void)innerLet;
+  ExprPtr body = inner->body;
+  for (size_t i = pre.size(); i-- > 0;) body = eLet(pre[i]->binder, pre[i]->annot, pre[i]->bound, body);
+  KernelBody kb;
+  kb.desc = descPair(d, d2);
+  kb.dims = {d, d2};
+  kb.dimBinders = {f.binder, inner->binder};
+  kb.dimReversed = {false, false};
+  kb.body = [this, body](KGen& g, const KScope& s) { return kexpr(g, s, body, nullptr); };
+  kb.env = env;
+  kb.note = "parallel for " + printName(f.binder) + " x " + printName(inner->binder) + " (flattened)";
+  HV r = requestKernel(kb, false, nullptr, nullptr);
+  // an effect-only nest: (Fin n) => (Fin m) => Unit
+  auto h = std::make_shared<HVal>();
+  h->k = HVal::Buf;
+  h->ty = tTable(d, tTable(d2, tUnit()));
+  (void)r;
+  return h;
 }
 
 HV Lowering::loopKernelLazy(const HV& lz, const std::vector<int>* intoBufs,
