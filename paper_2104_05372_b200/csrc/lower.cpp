@@ -2879,7 +2879,7 @@ void Lowering::decideStrategies(KGen& g) {
       // barrier per tile (dx_warp_tab); needs (K+1) x 128 B per warp.
       long long wt = (long long)(NT / 32) * (Kr + 1) * 128;
       cu.warpTab = !opt.f64 && cu.rowD % 4 == 0 && 32 % cu.rowD == 0 &&
-                   cu.smemOff + wt + (long long)NT * cu.rowD * 4 <= 150 * 1024 && !std::getenv("DEXLET_NO_WARPTAB");
+                   cu.smemOff + wt + (long long)NT * cu.rowD * 4 <= (NT > 256 ? 200 : 150) * 1024 && !std::getenv("DEXLET_NO_WARPTAB");
       cu.vec4 = cu.warpTab || (!opt.f64 && cu.rowD % 4 == 0 && Kr * (cu.rowD / 4) <= NT);
       if (cu.warpTab) {
         off = cu.smemOff + (int)(wt + (long long)NT * cu.rowD * 4);
@@ -3149,7 +3149,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       g.staged.insert(b);
       long long rowB = lb.first * eb;
       if (g.needAlign.count(b) && !opt.f64 && plan.bufs[b].kind == SK::F && aligned &&
-          (rowB == 32 || rowB == 64 || rowB == 128) && g.threads <= 256 && !std::getenv("DEXLET_NO_TMA_TENSOR"))
+          (rowB == 32 || rowB == 64 || rowB == 128) && g.threads % 256 == 0 && !std::getenv("DEXLET_NO_TMA_TENSOR"))
         g.tensorStaged[b] = rowB == 32 ? 1 : rowB == 64 ? 3 : 7;
     }
     for (int b : g.nonStream) {
@@ -3303,7 +3303,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     a.rowLen = g.streamUse[b].first;
     a.off = g.streamUse[b].second;
     a.rows = (plan.bufs[b].elems - a.off) / a.rowLen;
-    a.boxRows = g.threads;
+    a.boxRows = std::min(g.threads, 256);  // TMA box dims are <= 256: larger tiles take several boxes
     a.swizzle = (mask + 1) * 16;
     args.push_back(a);
   }
@@ -3366,7 +3366,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       for (int b : g.staged) {
         std::string B = std::to_string(b);
         if (g.tensorStaged.count(b)) {
-          src << "    dx_tma_2d(sb" << B << " + stg * " << stageElems[b] << "LL, &tm" << B << ", 0, (int)r0, &dx_bar[stg]);\n";
+          for (int bx = 0; bx < std::max(1, g.threads / 256); ++bx)
+            src << "    dx_tma_2d(sb" << B << " + stg * " << stageElems[b] << "LL + " << (long long)bx * 256 * g.streamUse[b].first
+                << "LL, &tm" << B << ", 0, (int)r0 + " << bx * 256 << ", &dx_bar[stg]);\n";
           continue;
         }
         src << "    dx_bulk_g2s(sb" << B << " + stg * " << stageElems[b] << "LL, (const char*)p" << B << " + a" << B

@@ -16,7 +16,7 @@ def timeit(prog, iters=20, warm=3):
 ctx = dx.Context(0)
 which = sys.argv[1] if len(sys.argv) > 1 else "kmeans"
 if which == "kmeans":
-    n, d, k = 1_000_000, 16, 64
+    n, d, k = (int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000), 16, 64
     pts, asg, cs = P.kmeans_inputs(n, d, k)
     t = time.time(); prog = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx); print("compile", time.time()-t)
     print(prog.plan.split("--- optimized")[0])
