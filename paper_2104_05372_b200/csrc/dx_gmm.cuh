@@ -60,7 +60,11 @@
 // cross products at +80, 80 columns each); A stage s (hi 32 columns, lo 32)
 // at 320 + 64 s.  Three A stages (the producers run up to two chunks ahead
 // of the tensor core).
+#if DXG_TMEM_A
 #define DXG_NXS 5                // X^T (+ beta, lse) stages of the backward TMA ring
+#else
+#define DXG_NXS 2                // (shared memory holds the A stages instead)
+#endif
 #define DXG_TB_SMALL 80
 #define DXG_TD(b) ((b) * 160)
 #define DXG_TA(s) (320 + 64 * (s))
@@ -716,6 +720,10 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         unsigned char* zh = zs + s * DXG_Z_BYTES;
         unsigned char* zl = zh + 128 * 128;
 #endif
+#ifdef DXG_DBG_NOPROD  // (timing experiment: tensor-core pipeline without the SIMT producers)
+#pragma unroll
+        for (int w = 0; w < 16; ++w) th[w] = tl[w] = 0u;
+#else
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {  // 4 x 8 points = 16-byte chunks
           const int pcol = hh * 32 + cc * 8;
@@ -745,6 +753,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
           *reinterpret_cast<uint4*>(zl + off_z) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
 #endif
         }
+#endif
 #if DXG_TMEM_A
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(DXG_TA(s) + hh * 16);

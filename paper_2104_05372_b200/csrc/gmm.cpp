@@ -31,7 +31,8 @@ constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
 constexpr int FWD_SMEM = 2 * GC * 64 * 128 + 2 * 2 * TM * 128 + 1024;
 inline int bwdSmem() {
-  return NXS * 2 * (BN * 128) + (std::getenv("DEXLET_GMM_SMEM_A") ? 2 * (2 * 128 * 128) : 0) + BN * 128 * 8 + 1024;
+  const bool smemA = std::getenv("DEXLET_GMM_SMEM_A") != nullptr;
+  return (smemA ? 2 : NXS) * 2 * (BN * 128) + (smemA ? 2 * (2 * 128 * 128) : 0) + BN * 128 * 8 + 1024;
 }
 constexpr int FIN_SMEM = 2 * D * (D + 1) * 8;
 enum { K_ABSMAX, K_PREPQ, K_PREPX, K_FWD, K_LSE, K_SUM, K_BWD, K_MOM, K_FIN, K_N };
@@ -145,6 +146,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   // DEXLET_GMM_SMEM_A=1: backward A operand staged in shared memory (A/B)
   std::string src = std::string(std::getenv("DEXLET_GMM_SMEM_A") ? "#define DXG_TMEM_A 0\n" : "");
   if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
+  if (std::getenv("DEXLET_GMM_DBG_NOPROD")) src += "#define DXG_DBG_NOPROD 1\n";
   src += std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
   if ((rc = ctx->loadModule(src, &g->mod))) { delete g; return rc; }
   for (int i = 0; i < K_N; ++i)
