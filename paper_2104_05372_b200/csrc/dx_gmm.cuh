@@ -27,10 +27,10 @@
 //                  the MMAs carry the strictly lower L_k, the diagonal of Q_k
 //                  is applied in fp32 in the epilogue
 //   dx_gmm_lse     lse_i over the K betas of each point, sum_i lse_i
-//   dx_gmm_bwd     per component pair: D[(k,b)][a] = sum_i g_ik x_ib x_ia
-//                  (a < 64) and D[(k,b)][64] = m_kb, with the A operand
-//                  g * X^T produced in shared memory by SIMT warps; W_k by
-//                  warp reductions
+//   dx_gmm_bwd     per component pair: D[(k,b)][a] = sum_i z_ikb x_ia with
+//                  z = g (x - mu_k), the A operand z^T produced by SIMT warps
+//                  straight into tensor memory; W_k and m~_kb = sum_i z_ikb
+//                  by the same warps in fp32/fp64
 //   dx_gmm_finish  fp64 per component: moments -> gradients, prior, err
 // The whole objective+gradient is deterministic: every reduction has a fixed
 // order (per-CTA contiguous work ranges, partial slots folded in CTA order).
@@ -42,7 +42,8 @@
 #define DXG_GC 8                 // components resident per forward CTA
 #define DXG_TM 128               // points per forward tile (MMA M)
 #define DXG_BC 64                // points per backward chunk (MMA K extent)
-#define DXG_BN 80                // backward MMA N: 64 dims + ones row + 15 zero rows
+#define DXG_BN 64                // backward MMA N: the 64 dims of X^T
+#define DXG_WP (2 * (1 + DXG_D))  // backward per-slot sums: per component W and the centred m~
 #ifndef DXG_PROMO
 #define DXG_PROMO 1              // backward chunks per TMEM promotion (fp32 registers)
 #endif
@@ -56,23 +57,18 @@
 #ifndef DXG_TMEM_A
 #define DXG_TMEM_A 1
 #endif
-// TMEM columns of the backward kernel: D buffer b at 160 b (hi*hi at +0,
-// cross products at +80, 80 columns each); A stage s (hi 32 columns, lo 32)
-// at 320 + 64 s.  Three A stages (the producers run up to two chunks ahead
-// of the tensor core).
+// TMEM columns of the backward kernel: D buffer b at 192 b with three
+// independent accumulators (hi*hi, hi*lo, lo*hi at +0, +64, +128: the MMAs of
+// a k-step do not wait on each other); A stage s (hi 32 columns, lo 32) at
+// 384 + 64 s.
 #if DXG_TMEM_A
 #define DXG_NXS 5                // X^T (+ beta, lse) stages of the backward TMA ring
 #else
 #define DXG_NXS 2                // (shared memory holds the A stages instead)
 #endif
-#define DXG_TB_SMALL 80
-#define DXG_TD(b) ((b) * 160)
-#define DXG_TA(s) (320 + 64 * (s))
-#if DXG_TMEM_A
-#define DXG_NZS 3
-#else
+#define DXG_TD(b) ((b) * 192)
+#define DXG_TA(s) (384 + 64 * (s))
 #define DXG_NZS 2
-#endif
 
 // ---- shared helpers ----------------------------------------------------------
 // byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
@@ -499,7 +495,7 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
 // every DXG_F64_EVERY promotions into fp64 accumulators in shared memory
 // (column-major, conflict-free).
 #define DXG_XT_BYTES (2 * DXG_D * 128)          // hi + lo image of one chunk
-#define DXG_XB_BYTES (DXG_BN * 128)             // one split of the B operand (+ ones rows)
+#define DXG_XB_BYTES (DXG_BN * 128)             // one split of the B operand
 #define DXG_Z_BYTES (2 * 128 * 128)             // hi + lo A operand of one chunk
 #if DXG_TMEM_A
 #define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + DXG_BN * 128 * 8 + 1024)
@@ -510,7 +506,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
                int K, long long n, long long npad, int P2,
-               double* __restrict__ dpart, float* __restrict__ wpart, int* __restrict__ ppart) {
+               double* __restrict__ dpart, double* __restrict__ wpart, int* __restrict__ ppart) {
   extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
   unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
   unsigned char* bs = smem;                           // 2 stages x (hi 10 KB, lo 10 KB)
@@ -533,10 +529,6 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      if (s < DXG_NZS - 2) {  // (third A stage)
-        dx_mbar_init(&zfull[2 + s], 8);
-        dx_mbar_init(&zempty[2 + s], 1);
-      }
       dx_mbar_init(&zfull[s], 8);
       dx_mbar_init(&zempty[s], 1);
       dx_mbar_init(&tfull[s], 1);
@@ -547,12 +539,6 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       dx_mbar_init(&xempty[s], 1);
     }
     dx_fence_mbar_init();
-  }
-  // constant B rows 64..79 of every stage: row 64 = 1.0 (hi) / 0 (lo), others 0
-  for (int e = threadIdx.x; e < DXG_NXS * 2 * 16 * 32; e += blockDim.x) {
-    const int st = e / (2 * 16 * 32), sp = (e / (16 * 32)) % 2, rr = (e / 32) % 16, w = e % 32;
-    const unsigned val = (sp == 0 && rr == 0) ? 0x3c003c00u : 0u;  // fp16 1.0
-    *reinterpret_cast<unsigned*>(bs + (st * 2 + sp) * DXG_XB_BYTES + (64 + rr) * 128 + w * 4) = val;
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
@@ -611,7 +597,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
           dxg_fence_after();
           // buffer (pc & 1): columns [256 b, 256 b + 80) take hi*hi, [+128, +208)
           // the small hi*lo + lo*hi products (fewer truncating adds on the big sum)
-          const unsigned td = tmem + (unsigned)DXG_TD(pc & 1), ts = td + DXG_TB_SMALL;
+          const unsigned td = tmem + (unsigned)DXG_TD(pc & 1);
           const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
 #if DXG_TMEM_A
           (void)zaddr;
@@ -622,8 +608,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
             dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
-            dxg_umma_f16_ta(ts, tah + kk * 8, dbl, idesc, acc);
-            dxg_umma_f16_ta(ts, tal + kk * 8, dbh, idesc, 1u);
+            dxg_umma_f16_ta(td + 64, tah + kk * 8, dbl, idesc, acc);
+            dxg_umma_f16_ta(td + 128, tal + kk * 8, dbh, idesc, acc);
           }
 #else
           const unsigned zh = zaddr + (unsigned)(s * DXG_Z_BYTES), zl = zh + 128 * 128;
@@ -635,8 +621,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
             dxg_umma_f16(td, ah, dbh, idesc, acc);
-            dxg_umma_f16(ts, ah, dbl, idesc, acc);
-            dxg_umma_f16(ts, al, dbh, idesc, 1u);
+            dxg_umma_f16(td + 64, ah, dbl, idesc, acc);
+            dxg_umma_f16(td + 128, al, dbh, idesc, acc);
           }
 #endif
           dx_umma_commit(&xempty[xs]);
@@ -674,6 +660,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     const int kl = r >> 6, b = r & 63;
     __shared__ __align__(16) float gw[8][32];
     __shared__ float wred[8];
+    __shared__ double mred[2][128];
+    double msum = 0.0;  // sum of this thread's z = g (x - mu) over its points
     const float sx = dxg_scale_for(__uint_as_float(*xmax));
     int it = 0;
     float wacc = 0.f, mub = 0.f;
@@ -684,8 +672,12 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       dxg_named_sync(2, 256);
       if (lane == 0) wred[pw] = w;
       dxg_named_sync(2, 256);
-      if (pt < 2)
-        wpart[((long long)blockIdx.x * DXG_FMAX + slot) * 2 + pt] = pt == 0 ? wred[wk0a] + wred[wk0b] : wred[wk1a] + wred[wk1b];
+      mred[hh][r] = msum;
+      dxg_named_sync(2, 256);
+      double* wp = wpart + ((long long)blockIdx.x * DXG_FMAX + slot) * DXG_WP;
+      if (pt < 2) wp[pt * (1 + DXG_D)] = (double)(pt == 0 ? wred[wk0a] + wred[wk0b] : wred[wk1a] + wred[wk1b]);
+      if (hh == 0) wp[kl * (1 + DXG_D) + 1 + b] = mred[0][r] + mred[1][r];
+      msum = 0.0;
       ++slot;
     };
     for (long long u = u0; u < u1; ++u) {
@@ -714,6 +706,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         }
         const unsigned char* xh = bs + (xs * 2) * DXG_XB_BYTES;
         const unsigned char* xl = xh + DXG_XB_BYTES;
+        float mchunk = 0.f;  // this chunk's part of m~ (32 points)
 #if DXG_TMEM_A
         unsigned th[16], tl[16];
 #else
@@ -739,7 +732,9 @@ extern "C" __global__ void __launch_bounds__(448, 1)
           for (int w = 0; w < 4; ++w) {
             const float x0 = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]) - mub;
             const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
-            dxg_split2(gv[2 * w] * x0, gv[2 * w + 1] * x1, oh[w], ol[w]);
+            const float z0 = gv[2 * w] * x0, z1 = gv[2 * w + 1] * x1;
+            mchunk += z0 + z1;
+            dxg_split2(z0, z1, oh[w], ol[w]);
           }
 #if DXG_TMEM_A
 #pragma unroll
@@ -754,6 +749,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 #endif
         }
 #endif
+        msum += (double)mchunk;
 #if DXG_TMEM_A
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(DXG_TA(s) + hh * 16);
@@ -796,12 +792,13 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       dxg_fence_after();
 #pragma unroll
       for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
-        unsigned v[16], w[16];
+        unsigned v[16], w[16], x[16];
         DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + DXG_TB_SMALL + j0), w);
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + 64 + j0), w);
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + 128 + j0), x);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + (__uint_as_float(w[j]) + __uint_as_float(x[j]));
       }
       dxg_fence_before();
       __syncwarp();
@@ -847,10 +844,10 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 // order into fp64 mom[k] = (P [64][64], m~ [64], W) with the centred moments
 // P[b][a] = sum_i g (x - mu)_b x_a and m~ = sum_i g (x - mu) ----------------------
 #define DXG_MOM (DXG_D * DXG_D + DXG_D + 1)
-extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* dpart, const float* wpart,
+extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* dpart, const double* wpart,
                                                                  const int* ppart, int nslot, const unsigned* xmax,
                                                                  double* mom) {
-  // D accumulated sx^2 P and sx m~ (operands scaled by the points' scale sx)
+  // the operands were scaled by the points' scale sx: D = sx^2 P, m~ sums sx m~
   const double isx = 1.0 / (double)dxg_scale_for(__uint_as_float(*xmax));
   __shared__ int slots[1024];  // host guarantees nslot <= 1024
   __shared__ int nsl;
@@ -863,17 +860,17 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* d
   }
   __syncthreads();
   double* out = mom + (long long)k * DXG_MOM;
-  for (int e = threadIdx.x; e < DXG_D * (DXG_D + 1); e += blockDim.x) {
-    const int b = e / (DXG_D + 1), a = e % (DXG_D + 1);  // a == 64: first moment
+  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
+    const int b = e / DXG_D, a = e % DXG_D;
     double s = 0.0;
     for (int sl = 0; sl < nsl; ++sl) s += dpart[((long long)slots[sl] * 128 + kl * 64 + b) * DXG_BN + a];
-    if (a < DXG_D) out[b * DXG_D + a] = s * isx * isx;
-    else out[DXG_D * DXG_D + b] = s * isx;
+    out[b * DXG_D + a] = s * isx * isx;
   }
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int sl = 0; sl < nsl; ++sl) s += (double)wpart[(long long)slots[sl] * 2 + kl];
-    out[DXG_D * DXG_D + DXG_D] = s;
+  if (threadIdx.x <= DXG_D) {
+    double s = 0.0;  // threadIdx 0: W; 1 + b: m~_b
+    for (int sl = 0; sl < nsl; ++sl) s += wpart[(long long)slots[sl] * DXG_WP + kl * (1 + DXG_D) + threadIdx.x];
+    if (threadIdx.x == 0) out[DXG_D * DXG_D + DXG_D] = s;
+    else out[DXG_D * DXG_D + threadIdx.x - 1] = s * isx;
   }
 }
 

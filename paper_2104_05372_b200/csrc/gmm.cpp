@@ -25,7 +25,8 @@ constexpr int ICF = D * (D + 1) / 2;
 constexpr int GC = 8;
 constexpr int TM = 128;
 constexpr int BC = 64;
-constexpr int BN = 80;
+constexpr int BN = 64;
+constexpr int WP = 2 * (1 + 64);  // DXG_WP
 constexpr int FMAX = 4;
 constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
@@ -141,6 +142,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   g->P = pickP(g->NG, g->T, sms);
   g->gridF = (int)std::min<long long>(sms, (long long)g->NG * g->P);
   g->P2 = pickP2(g->NP, g->C, sms);
+  if (const char* e = std::getenv("DEXLET_GMM_P2")) g->P2 = std::max(1, std::atoi(e));  // (experiments)
   g->gridB = (int)std::min<long long>(sms, (long long)g->NP * g->P2);
   g->gridL = (int)std::min<long long>(4 * sms, (g->n + 255) / 256);
   // DEXLET_GMM_SMEM_A=1: backward A operand staged in shared memory (A/B)
@@ -176,7 +178,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
       {&g->lpart, (size_t)g->gridL * 8},
       {&g->lsum, 8},
       {&g->dpart, (size_t)g->gridB * FMAX * 128 * BN * 8},
-      {&g->wpart, (size_t)g->gridB * FMAX * 2 * 4},
+      {&g->wpart, (size_t)g->gridB * FMAX * WP * 8},
       {&g->ppart, (size_t)g->gridB * FMAX * 4},
       {&g->mom, (size_t)k * MOM * 8},
       {&g->dal, (size_t)k * 8},
