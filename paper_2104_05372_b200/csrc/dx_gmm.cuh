@@ -607,9 +607,13 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
             const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
+#ifndef DXG_DBG_NOMMA  // (timing experiment: the pipeline without tensor-core work)
             dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
             dxg_umma_f16_ta(td + 64, tah + kk * 8, dbl, idesc, acc);
             dxg_umma_f16_ta(td + 128, tal + kk * 8, dbh, idesc, acc);
+#else
+            (void)acc; (void)dbh; (void)dbl;
+#endif
           }
 #else
           const unsigned zh = zaddr + (unsigned)(s * DXG_Z_BYTES), zl = zh + 128 * 128;
