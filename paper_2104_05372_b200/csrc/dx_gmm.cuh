@@ -48,7 +48,7 @@
 #define DXG_PROMO 1              // backward chunks per TMEM promotion (fp32 registers)
 #endif
 #define DXG_F64_EVERY 16         // promotions per fp64 spill (shared memory)
-#define DXG_FMAX 4               // backward partial slots per CTA
+#define DXG_FMAX 8               // backward partial slots per CTA (= units per CTA)
 #define DXG_FIN_SMEM (2 * DXG_D * (DXG_D + 1) * 8)
 // Backward A operand (g * (x - mu)^T) in tensor memory (written by the SIMT
 // producers with tcgen05.st, read by the MMA as [a-tmem]) instead of shared
@@ -66,9 +66,13 @@
 #else
 #define DXG_NXS 2                // (shared memory holds the A stages instead)
 #endif
-#define DXG_TD(b) ((b) * 192)
-#define DXG_TA(s) (384 + 64 * (s))
-#define DXG_NZS 2
+#ifndef DXG_NACC
+#define DXG_NACC 1               // TMEM accumulators per D buffer (1: merged, 3: hh / hl / lh)
+#endif
+#define DXG_TD(b) ((b) * 64 * DXG_NACC)
+#define DXG_TACC(i) ((DXG_NACC == 3 ? (i) : 0) * 64)
+#define DXG_NZS ((512 - 128 * DXG_NACC) / 64)  // A stages filling the rest of TMEM
+#define DXG_TA(s) (128 * DXG_NACC + 64 * (s))
 
 // ---- shared helpers ----------------------------------------------------------
 // byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
@@ -484,10 +488,9 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
 }
 
 // ---- backward moments -------------------------------------------------------------
-// Work unit = (component pair pr, contiguous chunk range p); CTA c takes the
-// contiguous unit range [c*U/grid, (c+1)*U/grid) and accumulates consecutive
-// units of the same pair in registers, flushing a partial slot at every pair
-// change.  Warp 0: X^T chunk producer (bulk copies, 2-stage ring); warp 1: MMA
+// Work unit = (component pair pr, contiguous chunk range p); CTA c takes
+// units c, c + grid, ... (chunk-range-major order) and flushes a partial slot
+// per unit.  Warp 0: X^T chunk producer (bulk copies, 2-stage ring); warp 1: MMA
 // issuer; warps 2-9: A-operand producers (g * (X - mu)^T, fp16x3 split, W sums);
 // warps 10-13: TMEM promotion epilogue.  D (128 lanes x 80 columns, hi*hi and
 // the small cross products in separate accumulators) is double buffered in
@@ -525,12 +528,18 @@ extern "C" __global__ void __launch_bounds__(448, 1)
   const int NP = (K + 1) / 2;
   const long long C = npad / DXG_BC;  // chunks
   const long long units = (long long)NP * P2;
-  const long long u0 = (long long)blockIdx.x * units / gridDim.x, u1 = (long long)(blockIdx.x + 1) * units / gridDim.x;
+  // Units are enumerated chunk-range-major and dealt round-robin, so the CTAs
+  // running at the same time work on the same few chunk ranges (of different
+  // pairs) and each X^T chunk comes from HBM about once, then from L2.
+#define DXG_UNITS_LOOP for (long long u = blockIdx.x; u < units; u += gridDim.x)
+#define DXG_UNIT_SPLIT const long long pr = u % NP, p = u / NP
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < DXG_NZS; ++s) {
       dx_mbar_init(&zfull[s], 8);
       dx_mbar_init(&zempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       dx_mbar_init(&tfull[s], 1);
       dx_mbar_init(&tempty[s], 4);
     }
@@ -555,20 +564,26 @@ extern "C" __global__ void __launch_bounds__(448, 1)
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (long long u = u0; u < u1; ++u) {
-        const long long pr = u / P2, p = u % P2;
+      DXG_UNITS_LOOP {
+        DXG_UNIT_SPLIT;
         const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
         const long long k0 = pr * 2, k1 = (pr * 2 + 1 < K) ? pr * 2 + 1 : pr * 2;
         for (long long c = c0; c < c1; ++c, ++it) {
           const int s = it % DXG_NXS;
           if (it >= DXG_NXS) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it / DXG_NXS) - 1) & 1));
+#ifdef DXG_DBG_NOGIN  // (timing experiment: only the X^T images)
+          dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES);
+#else
           dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES + 3 * DXG_BC * 4);
+#endif
           const unsigned char* src = xtimg + c * DXG_XT_BYTES;
           dx_bulk_g2s(bs + (s * 2) * DXG_XB_BYTES, src, DXG_D * 128, &xfull[s]);
           dx_bulk_g2s(bs + (s * 2 + 1) * DXG_XB_BYTES, src + DXG_D * 128, DXG_D * 128, &xfull[s]);
+#ifndef DXG_DBG_NOGIN
           dx_bulk_g2s(gin[s][0], beta + k0 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
           dx_bulk_g2s(gin[s][1], beta + k1 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
           dx_bulk_g2s(gin[s][2], lse + c * DXG_BC, DXG_BC * 4, &xfull[s]);
+#endif
         }
       }
     }
@@ -579,8 +594,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       int it = 0, pc = 0;
       long long prevPair = -1;
       int inb = 0;  // chunks accumulated into the current TMEM buffer
-      for (long long u = u0; u < u1; ++u) {
-        const long long pr = u / P2, p = u % P2;
+      DXG_UNITS_LOOP {
+        DXG_UNIT_SPLIT;
         const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
         if (pr != prevPair && inb > 0) {  // flush at pair change
           dx_umma_commit(&tfull[pc & 1]);
@@ -609,8 +624,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
 #ifndef DXG_DBG_NOMMA  // (timing experiment: the pipeline without tensor-core work)
             dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
-            dxg_umma_f16_ta(td + 64, tah + kk * 8, dbl, idesc, acc);
-            dxg_umma_f16_ta(td + 128, tal + kk * 8, dbh, idesc, acc);
+            dxg_umma_f16_ta(td + DXG_TACC(1), tah + kk * 8, dbl, idesc, DXG_NACC == 3 ? acc : 1u);
+            dxg_umma_f16_ta(td + DXG_TACC(2), tal + kk * 8, dbh, idesc, DXG_NACC == 3 ? acc : 1u);
 #else
             (void)acc; (void)dbh; (void)dbl;
 #endif
@@ -625,8 +640,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
             dxg_umma_f16(td, ah, dbh, idesc, acc);
-            dxg_umma_f16(td + 64, ah, dbl, idesc, acc);
-            dxg_umma_f16(td + 128, al, dbh, idesc, acc);
+            dxg_umma_f16(td + DXG_TACC(1), ah, dbl, idesc, DXG_NACC == 3 ? acc : 1u);
+            dxg_umma_f16(td + DXG_TACC(2), al, dbh, idesc, DXG_NACC == 3 ? acc : 1u);
           }
 #endif
           dx_umma_commit(&xempty[xs]);
@@ -684,8 +699,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       msum = 0.0;
       ++slot;
     };
-    for (long long u = u0; u < u1; ++u) {
-      const long long pr = u / P2, p = u % P2;
+    DXG_UNITS_LOOP {
+      DXG_UNIT_SPLIT;
       const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
       const int k = (int)(pr * 2 + kl);
       const bool live = k < K;
@@ -757,9 +772,13 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 #if DXG_TMEM_A
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(DXG_TA(s) + hh * 16);
+#ifndef DXG_DBG_NOSTTM  // (timing experiment)
           DXG_TMEM_ST16(ta, th);
           DXG_TMEM_ST16(ta + 32, tl);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#else
+          (void)ta;
+#endif
           dxg_fence_before();
         }
 #else
@@ -796,6 +815,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       dxg_fence_after();
 #pragma unroll
       for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
+#if DXG_NACC == 3
         unsigned v[16], w[16], x[16];
         DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
         DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + 64 + j0), w);
@@ -803,6 +823,13 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + (__uint_as_float(w[j]) + __uint_as_float(x[j]));
+#else
+        unsigned v[16];
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]);
+#endif
       }
       dxg_fence_before();
       __syncwarp();
@@ -821,8 +848,8 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)pair;
       ++slot;
     };
-    for (long long u = u0; u < u1; ++u) {
-      const long long pr = u / P2, p = u % P2;
+    DXG_UNITS_LOOP {
+      DXG_UNIT_SPLIT;
       const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
       if (pr != prevPair && prevPair >= 0) {
         if (inb > 0) { drain(); inb = 0; }
@@ -853,12 +880,12 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* d
                                                                  double* mom) {
   // the operands were scaled by the points' scale sx: D = sx^2 P, m~ sums sx m~
   const double isx = 1.0 / (double)dxg_scale_for(__uint_as_float(*xmax));
-  __shared__ int slots[1024];  // host guarantees nslot <= 1024
+  __shared__ int slots[2048];  // host guarantees nslot <= 2048
   __shared__ int nsl;
   const int k = blockIdx.x, pr = k / 2, kl = k % 2;
   if (threadIdx.x == 0) {
     int ns = 0;
-    for (int e = 0; e < nslot && ns < 1024; ++e)
+    for (int e = 0; e < nslot && ns < 2048; ++e)
       if (ppart[e] == pr) slots[ns++] = e;
     nsl = ns;
   }

@@ -27,7 +27,7 @@ constexpr int TM = 128;
 constexpr int BC = 64;
 constexpr int BN = 64;
 constexpr int WP = 2 * (1 + 64);  // DXG_WP
-constexpr int FMAX = 4;
+constexpr int FMAX = 8;
 constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
 constexpr int FWD_SMEM = 2 * GC * 64 * 128 + 2 * 2 * TM * 128 + 1024;
@@ -56,18 +56,17 @@ int pickP(int NG, long long T, int grid) {
   }
   return best;
 }
-// Backward: units = NP pairs x P2 chunk ranges, contiguous ranges per CTA.
-// Each CTA may see at most FMAX distinct pairs (partial slots).
+// Backward: units = NP pairs x P2 chunk ranges dealt round-robin; each unit
+// is one partial slot, so a CTA may take at most FMAX units.
 int pickP2(int NP, long long C, int grid) {
   int best = 1;
   double bestEff = -1;
   for (int P2 = 1; P2 <= 4096 && P2 <= C; ++P2) {
     long long units = (long long)NP * P2;
     long long per = (units + grid - 1) / grid;
-    if ((per + P2 - 1) / P2 + 1 > FMAX) continue;
+    if (per > FMAX) break;
     double eff = (double)units / (double)(per * grid);
     if (eff > bestEff + 1e-9) { bestEff = eff; best = P2; }
-    if (eff > 0.995 && C / P2 >= 16) break;
   }
   return best;
 }
@@ -150,6 +149,9 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
   if (std::getenv("DEXLET_GMM_DBG_NOPROD")) src += "#define DXG_DBG_NOPROD 1\n";
   if (std::getenv("DEXLET_GMM_DBG_NOMMA")) src += "#define DXG_DBG_NOMMA 1\n";
+  if (std::getenv("DEXLET_GMM_DBG_NOGIN")) src += "#define DXG_DBG_NOGIN 1\n";
+  if (std::getenv("DEXLET_GMM_DBG_NOSTTM")) src += "#define DXG_DBG_NOSTTM 1\n";
+  if (const char* e = std::getenv("DEXLET_GMM_NACC")) src += std::string("#define DXG_NACC ") + e + "\n";
   src += std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
   if ((rc = ctx->loadModule(src, &g->mod))) { delete g; return rc; }
   for (int i = 0; i < K_N; ++i)
