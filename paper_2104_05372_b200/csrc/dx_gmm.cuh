@@ -871,18 +871,269 @@ extern "C" __global__ void __launch_bounds__(448, 1)
   }
 }
 
+// ---- backward, two pairs (four components) per unit ---------------------------------
+// Same math as dx_gmm_bwd, but each X^T chunk staged by the bulk-copy ring
+// feeds the MMAs of two component pairs (the single-pair kernel is bound by
+// re-streaming X^T once per pair).  TMEM: D[q][b] (pair q, buffer b, one merged
+// accumulator) at (2q + b) * 64, A[q][s] (pair q, stage s: hi 32 + lo 32
+// columns) at 256 + (2q + s) * 64.  Warps: 0 bulk copies, 1 MMA, 2-9
+// producers (warps 2-5 pair 0, 6-9 pair 1; each thread one row (k, b) over all
+// 64 points of the chunk), 10-13 epilogue (fp32 shared accumulators per unit,
+// flushed to fp64 partial slots, one slot per unit).
+#define DXG_QWP (4 * (1 + DXG_D))
+#define DXG_BWD4_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_BN * 128 * 4 + 1024)
+#ifndef DXG_PROMO4
+#define DXG_PROMO4 2
+#endif
+extern "C" __global__ void __launch_bounds__(448, 1)
+    dx_gmm_bwd4(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
+                const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
+                int K, long long n, long long npad, int P2, double* __restrict__ dpart, double* __restrict__ wpart,
+                int* __restrict__ ppart) {
+  extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
+  unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
+  unsigned char* bs = smem;                                                      // NXS x (hi 8 KB, lo 8 KB)
+  float* dacc = reinterpret_cast<float*>(smem + DXG_NXS * 2 * DXG_XB_BYTES);   // [2][64][128]
+  __shared__ __align__(16) float gin[DXG_NXS][5][DXG_BC];
+  __shared__ __align__(16) float gw[8][64];
+  __shared__ __align__(8) unsigned long long xfull[DXG_NXS], xempty[DXG_NXS], zfull[2][2], zempty[2][2],
+      tfull[2][2], tempty[2][2];
+  __shared__ unsigned tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NQ = (K + 3) / 4;
+  const long long C = npad / DXG_BC;
+  const long long units = (long long)NQ * P2;
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 2; ++q)
+      for (int b = 0; b < 2; ++b) {
+        dx_mbar_init(&zfull[q][b], 4);
+        dx_mbar_init(&zempty[q][b], 1);
+        dx_mbar_init(&tfull[q][b], 1);
+        dx_mbar_init(&tempty[q][b], 4);
+      }
+    for (int s = 0; s < DXG_NXS; ++s) {
+      dx_mbar_init(&xfull[s], 1);
+      dx_mbar_init(&xempty[s], 1);
+    }
+    dx_fence_mbar_init();
+  }
+  for (int e = threadIdx.x; e < 2 * DXG_BN * 128; e += blockDim.x) dacc[e] = 0.f;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  dxg_fence_before();
+  __syncthreads();
+  dxg_fence_after();
+  const unsigned tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long qd = u % NQ, p = u / NQ;
+        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+        long long kr[4];
+        for (int j = 0; j < 4; ++j) kr[j] = (4 * qd + j < K) ? 4 * qd + j : 0;
+        for (long long c = c0; c < c1; ++c, ++it) {
+          const int xs = it % DXG_NXS;
+          if (it >= DXG_NXS) dx_mbar_wait_bounded(&xempty[xs], (unsigned)(((it / DXG_NXS) - 1) & 1));
+          dx_mbar_expect_tx(&xfull[xs], DXG_XT_BYTES + 5 * DXG_BC * 4);
+          const unsigned char* src = xtimg + c * DXG_XT_BYTES;
+          dx_bulk_g2s(bs + (xs * 2) * DXG_XB_BYTES, src, DXG_D * 128, &xfull[xs]);
+          dx_bulk_g2s(bs + (xs * 2 + 1) * DXG_XB_BYTES, src + DXG_D * 128, DXG_D * 128, &xfull[xs]);
+          for (int j = 0; j < 4; ++j) dx_bulk_g2s(gin[xs][j], beta + kr[j] * npad + c * DXG_BC, DXG_BC * 4, &xfull[xs]);
+          dx_bulk_g2s(gin[xs][4], lse + c * DXG_BC, DXG_BC * 4, &xfull[xs]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const unsigned idesc = dxg_idesc_f16<DXG_BN>();
+      const unsigned baddr = dx_smem_addr(bs);
+      int it = 0, pc = 0, inb = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long p = u / NQ;
+        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+        for (long long c = c0; c < c1; ++c, ++it) {
+          const int xs = it % DXG_NXS, s = it & 1;
+          dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
+          const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
+          for (int q = 0; q < 2; ++q) {
+            if (inb == 0 && pc >= 2) dx_mbar_wait_bounded(&tempty[q][pc & 1], (unsigned)(((pc >> 1) - 1) & 1));
+            dx_mbar_wait_bounded(&zfull[q][s], (unsigned)((it >> 1) & 1));
+            dxg_fence_after();
+            const unsigned td = tmem + (unsigned)((2 * q + (pc & 1)) * 64);
+            const unsigned tah = tmem + (unsigned)(256 + (2 * q + s) * 64), tal = tah + 32;
+#pragma unroll
+            for (int kk = 0; kk < DXG_BC / 16; ++kk) {
+              const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
+              const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
+              dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, (inb > 0 || kk > 0) ? 1u : 0u);
+              dxg_umma_f16_ta(td, tah + kk * 8, dbl, idesc, 1u);
+              dxg_umma_f16_ta(td, tal + kk * 8, dbh, idesc, 1u);
+            }
+            dx_umma_commit(&zempty[q][s]);
+          }
+          dx_umma_commit(&xempty[xs]);
+          if (++inb == DXG_PROMO4 || c + 1 == c1) {  // every unit ends with a drain
+            dx_umma_commit(&tfull[0][pc & 1]);
+            dx_umma_commit(&tfull[1][pc & 1]);
+            ++pc;
+            inb = 0;
+          }
+        }
+      }
+    }
+  } else if (warp < 10) {
+    const int pw = warp - 2, q = pw >> 2;           // pair of this producer warp
+    const int r = (warp & 3) * 32 + lane;            // TMEM lane = row (k_local, b) of A[q]
+    const int kl = r >> 6, b = r & 63;
+    const bool wrow = (r & 32) == 0;                 // the warp with rows b < 32 sums W of comp kl
+    const float sx = dxg_scale_for(__uint_as_float(*xmax));
+    int it = 0, slot = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
+      const long long qd = u % NQ, p = u / NQ;
+      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+      const int kq = 2 * q + kl;                     // component within the quad
+      const int k = (int)(4 * qd) + kq;
+      const bool live = k < K;
+      const float mub = live ? means[(long long)k * DXG_D + b] * sx : 0.f;
+      float wacc = 0.f;
+      double msum = 0.0;
+      for (long long c = c0; c < c1; ++c, ++it) {
+        const int xs = it % DXG_NXS, s = it & 1;
+        if (it >= 2) dx_mbar_wait_bounded(&zempty[q][s], (unsigned)(((it >> 1) - 1) & 1));
+        dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
+        {
+          const long long i0 = c * DXG_BC + lane, i1 = i0 + 32;
+          const float g0 = __expf(gin[xs][kq][lane] - gin[xs][4][lane]);
+          const float g1 = __expf(gin[xs][kq][lane + 32] - gin[xs][4][lane + 32]);
+          const float q0 = (live && i0 < n) ? g0 : 0.f, q1 = (live && i1 < n) ? g1 : 0.f;
+          if (wrow) wacc += q0 + q1;
+          gw[pw][lane] = q0;
+          gw[pw][lane + 32] = q1;
+          __syncwarp();
+        }
+        const unsigned char* xh = bs + (xs * 2) * DXG_XB_BYTES;
+        const unsigned char* xl = xh + DXG_XB_BYTES;
+        unsigned th[32], tl[32];
+        float mchunk = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {  // 8 x 8 points
+          const unsigned off_x = dxg_sw((unsigned)b, (unsigned)(cc * 8));
+          const uint4 h4 = *reinterpret_cast<const uint4*>(xh + off_x);
+          const uint4 l4 = *reinterpret_cast<const uint4*>(xl + off_x);
+          const float4 ga = *reinterpret_cast<const float4*>(&gw[pw][cc * 8]);
+          const float4 gb = *reinterpret_cast<const float4*>(&gw[pw][cc * 8 + 4]);
+          const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+          const unsigned hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float x0 = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]) - mub;
+            const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
+            const float z0 = gv[2 * w] * x0, z1 = gv[2 * w + 1] * x1;
+            mchunk += z0 + z1;
+            dxg_split2(z0, z1, th[cc * 4 + w], tl[cc * 4 + w]);
+          }
+        }
+        msum += (double)mchunk;
+        {
+          const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(256 + (2 * q + s) * 64);
+          DXG_TMEM_ST16(ta, th);
+          DXG_TMEM_ST16(ta + 16, (th + 16));
+          DXG_TMEM_ST16(ta + 32, tl);
+          DXG_TMEM_ST16(ta + 48, (tl + 16));
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          dxg_fence_before();
+        }
+        __syncwarp();
+        if (lane == 0) dx_mbar_arrive(&zfull[q][s]);
+      }
+      // unit done: W (warp sum) and m~ (per row) of this thread's component
+      double* wp = wpart + ((long long)blockIdx.x * DXG_FMAX + slot) * DXG_QWP + kq * (1 + DXG_D);
+      const float wsum = dx_warp_sum(wacc);
+      if (wrow && lane == 0) wp[0] = (double)wsum;
+      wp[1 + b] = msum;
+    }
+  } else {
+    // epilogue: warps 10..13 -> TMEM lane quarter (warp & 3); fp32 shared accumulators
+    const int qr = warp & 3;
+    const int row = qr * 32 + lane;
+    const unsigned lanebase = tmem + ((unsigned)(qr * 32) << 16);
+    int pc = 0, slot = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
+      const long long qd = u % NQ, p = u / NQ;
+      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+      double* dst = dpart + ((long long)blockIdx.x * DXG_FMAX + slot) * 256 * DXG_BN;
+      // fp32 shared accumulators hold at most DXG_F64_EVERY promotions; then
+      // they are added into the unit's fp64 slot (global, L2-resident)
+      int npro = 0;
+      bool first = true;
+      auto spill = [&]() {
+        for (int q = 0; q < 2; ++q) {
+          double* dq = dst + ((long long)q * 128 + row) * DXG_BN;
+#pragma unroll 4
+          for (int j = 0; j < DXG_BN; ++j) {
+            const double v = (double)dacc[(q * DXG_BN + j) * 128 + row];
+            dq[j] = first ? v : dq[j] + v;
+            dacc[(q * DXG_BN + j) * 128 + row] = 0.f;
+          }
+        }
+        first = false;
+        npro = 0;
+      };
+      int inb = 0;
+      for (long long c = c0; c < c1; ++c) {
+        if (++inb == DXG_PROMO4 || c + 1 == c1) {
+          const int bb = pc & 1;
+          for (int q = 0; q < 2; ++q) {
+            dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
+            dxg_fence_after();
+#pragma unroll
+            for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
+              unsigned v[16];
+              DXG_TMEM_LD16(lanebase + (unsigned)((2 * q + bb) * 64 + j0), v);
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+              for (int j = 0; j < 16; ++j) dacc[(q * DXG_BN + j0 + j) * 128 + row] += __uint_as_float(v[j]);
+            }
+            dxg_fence_before();
+            __syncwarp();
+            if (lane == 0) dx_mbar_arrive(&tempty[q][bb]);
+          }
+          ++pc;
+          inb = 0;
+          if (++npro == DXG_F64_EVERY) spill();
+        }
+      }
+      if (npro > 0 || first) spill();  // the rest of this unit into its fp64 slot
+      if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)qd;
+    }
+  }
+  dxg_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
 // ---- moments: fold the backward partial slots of each component's pair in CTA
 // order into fp64 mom[k] = (P [64][64], m~ [64], W) with the centred moments
 // P[b][a] = sum_i g (x - mu)_b x_a and m~ = sum_i g (x - mu) ----------------------
 #define DXG_MOM (DXG_D * DXG_D + DXG_D + 1)
 extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* dpart, const double* wpart,
                                                                  const int* ppart, int nslot, const unsigned* xmax,
-                                                                 double* mom) {
+                                                                 int G, double* mom) {
+  // G components per partial slot (2: dx_gmm_bwd, 4: dx_gmm_bwd4)
   // the operands were scaled by the points' scale sx: D = sx^2 P, m~ sums sx m~
   const double isx = 1.0 / (double)dxg_scale_for(__uint_as_float(*xmax));
   __shared__ int slots[2048];  // host guarantees nslot <= 2048
   __shared__ int nsl;
-  const int k = blockIdx.x, pr = k / 2, kl = k % 2;
+  const int k = blockIdx.x, pr = k / G, kl = k % G;
   if (threadIdx.x == 0) {
     int ns = 0;
     for (int e = 0; e < nslot && ns < 2048; ++e)
@@ -894,12 +1145,12 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* d
   for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
     const int b = e / DXG_D, a = e % DXG_D;
     double s = 0.0;
-    for (int sl = 0; sl < nsl; ++sl) s += dpart[((long long)slots[sl] * 128 + kl * 64 + b) * DXG_BN + a];
+    for (int sl = 0; sl < nsl; ++sl) s += dpart[((long long)slots[sl] * (G * 64) + kl * 64 + b) * DXG_BN + a];
     out[b * DXG_D + a] = s * isx * isx;
   }
   if (threadIdx.x <= DXG_D) {
     double s = 0.0;  // threadIdx 0: W; 1 + b: m~_b
-    for (int sl = 0; sl < nsl; ++sl) s += wpart[(long long)slots[sl] * DXG_WP + kl * (1 + DXG_D) + threadIdx.x];
+    for (int sl = 0; sl < nsl; ++sl) s += wpart[(long long)slots[sl] * (G * (1 + DXG_D)) + kl * (1 + DXG_D) + threadIdx.x];
     if (threadIdx.x == 0) out[DXG_D * DXG_D + DXG_D] = s;
     else out[DXG_D * DXG_D + threadIdx.x - 1] = s * isx;
   }

@@ -1,0 +1,13 @@
+# round evidence (3): GPU tests, all bench configs, reference arm, smoke
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r3_pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/r3_pytest_gpu.log
+for c in kmeans gmm histogram matmul mlp; do
+  timeout 400 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/r3_bench_$c.log 2>&1
+done
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r3_bench_ref.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r3_smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/r3_smoke.log
+ncu --set full --clock-control none --import-source on -k regex:"dx_gmm_(fwd|bwd)" -s 2 -c 2 -o gpurun_out/r3_gmm_full python bench.py --config gmm --profile > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:dxk_0 -s 2 -c 1 -o gpurun_out/r3_kmeans_full python bench.py --config kmeans --profile > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r3_kmeans_launches.csv python bench.py --config kmeans --profile > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/r3_gmm_launches.csv python bench.py --config gmm --profile > /dev/null 2>&1
+tail -n 2 gpurun_out/r3_pytest_gpu.log gpurun_out/r3_smoke.log
