@@ -1068,24 +1068,6 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
       const long long qd = u % NQ, p = u / NQ;
       const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-      double* dst = dpart + ((long long)blockIdx.x * DXG_FMAX + slot) * 256 * DXG_BN;
-      // fp32 shared accumulators hold at most DXG_F64_EVERY promotions; then
-      // they are added into the unit's fp64 slot (global, L2-resident)
-      int npro = 0;
-      bool first = true;
-      auto spill = [&]() {
-        for (int q = 0; q < 2; ++q) {
-          double* dq = dst + ((long long)q * 128 + row) * DXG_BN;
-#pragma unroll 4
-          for (int j = 0; j < DXG_BN; ++j) {
-            const double v = (double)dacc[(q * DXG_BN + j) * 128 + row];
-            dq[j] = first ? v : dq[j] + v;
-            dacc[(q * DXG_BN + j) * 128 + row] = 0.f;
-          }
-        }
-        first = false;
-        npro = 0;
-      };
       int inb = 0;
       for (long long c = c0; c < c1; ++c) {
         if (++inb == DXG_PROMO4 || c + 1 == c1) {
@@ -1107,10 +1089,18 @@ extern "C" __global__ void __launch_bounds__(448, 1)
           }
           ++pc;
           inb = 0;
-          if (++npro == DXG_F64_EVERY) spill();
         }
       }
-      if (npro > 0 || first) spill();  // the rest of this unit into its fp64 slot
+      // flush this unit: rows (q, row) of the quad's D to an fp64 slot
+      double* dst = dpart + ((long long)blockIdx.x * DXG_FMAX + slot) * 256 * DXG_BN;
+      for (int q = 0; q < 2; ++q) {
+        double* dq = dst + ((long long)q * 128 + row) * DXG_BN;
+#pragma unroll 4
+        for (int j = 0; j < DXG_BN; ++j) {
+          dq[j] = (double)dacc[(q * DXG_BN + j) * 128 + row];
+          dacc[(q * DXG_BN + j) * 128 + row] = 0.f;
+        }
+      }
       if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)qd;
     }
   }
