@@ -311,12 +311,22 @@ def peaks(bound="hbm"):
     return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s bf16)"
 
 
-def traffic_per_launch():
-    p = os.path.join(ROOT, "profiles", "kmeans_ncu_summary.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            j = json.load(f)
-        return j.get("dram_bytes_per_launch")
+def traffic_per_launch(config="kmeans"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from
+    the committed ncu --set full capture (profiles/r01c_<config>_ncu_summary.json)."""
+    p = os.path.join(ROOT, "profiles", f"r01c_{config}_ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for k in j.get("kernels", []):
+        m = k["metrics"]
+        try:
+            rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
+            return float(rd["value"]) * scale[rd["unit"]] + float(wr["value"]) * scale[wr["unit"]]
+        except (KeyError, ValueError):
+            continue
     return None
 
 
@@ -485,7 +495,7 @@ def main():
         # the dominant kernel's own algorithmic work (GMM: per kernel; else the whole step)
         work = spec.get("work_by_kernel", {}).get(dom[0], work)
         achieved = work / (dom_ms_max * 1e-3) / (1e9 if spec["bound"] == "hbm" else 1e12)
-        tr = traffic_per_launch() if args.config == "kmeans" else None
+        tr = traffic_per_launch(args.config) if args.config in ("kmeans", "histogram") else None
         line = {
             "metric": spec["metric"], "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
