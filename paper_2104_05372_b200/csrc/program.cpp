@@ -137,6 +137,7 @@ int Program::prepare() {
     if ((rc = dxrt::check(cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, s.threads, s.smem), "occupancy")))
       return rc;
     if (nb < 1) nb = 1;
+    if (const char* e = std::getenv("DEXLET_BLOCKS_PER_SM")) nb = std::max(1, std::min(nb, std::atoi(e)));  // (experiments)
     long long U = s.minGrid > 0 ? s.minGrid : 1;  // ordinals per thread
     long long need = ((hi - lo + U - 1) / U + s.threads - 1) / s.threads;
     long long cap = (long long)ctx->smCount * nb;
