@@ -95,7 +95,8 @@ __device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
 template <int BN, int STAGES, class CT>
 __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap* tal, const dx_tmap* tb,
                                                const dx_tmap* tbl, long long M, long long N, long long K, CT* C,
-                                               long long ldc, long long mode) {
+                                               long long ldc, long long mode, long long ksplit,
+                                               unsigned* tickets) {
   constexpr unsigned A_BYTES = DX_GEMM_BM * 128, B_BYTES = BN * 128;
   constexpr unsigned STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   constexpr unsigned TMEM_COLS = 4 * BN;
@@ -106,8 +107,15 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
   __shared__ unsigned tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = (int)((N + BN - 1) / BN);
-  const int m0 = (int)(blockIdx.x / NT) * DX_GEMM_BM, n0 = (int)(blockIdx.x % NT) * BN;
-  const int KB = (int)((K + DX_GEMM_BK - 1) / DX_GEMM_BK);
+  // split-K: CTA (tile, part) takes k-blocks [kb0, kb0 + KB); the parts of a
+  // tile add into C one after another, in part order (ticket per tile), so the
+  // result is deterministic
+  const int S = (int)(ksplit > 1 ? ksplit : 1);
+  const int tile = (int)(blockIdx.x / S), part = (int)(blockIdx.x % S);
+  const int m0 = (int)(tile / NT) * DX_GEMM_BM, n0 = (int)(tile % NT) * BN;
+  const int KBT = (int)((K + DX_GEMM_BK - 1) / DX_GEMM_BK);
+  const int kb0 = (int)((long long)part * KBT / S);
+  const int KB = (int)((long long)(part + 1) * KBT / S) - kb0;
   const int NC = (KB + DX_GEMM_CHUNK - 1) / DX_GEMM_CHUNK;
 
   if (threadIdx.x == 0) {
@@ -139,10 +147,11 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         if (kb >= STAGES) dx_mbar_wait_bounded(&empty[s], (unsigned)(((kb / STAGES) - 1) & 1));
         unsigned char* st = smem + s * STAGE_BYTES;
         dx_mbar_expect_tx(&full[s], STAGE_BYTES);
-        dx_tma_2d(st, ta, kb * DX_GEMM_BK, m0, &full[s]);
-        dx_tma_2d(st + A_BYTES, tal, kb * DX_GEMM_BK, m0, &full[s]);
-        dx_tma_2d(st + 2 * A_BYTES, tb, kb * DX_GEMM_BK, n0, &full[s]);
-        dx_tma_2d(st + 2 * A_BYTES + B_BYTES, tbl, kb * DX_GEMM_BK, n0, &full[s]);
+        const int kc = (kb0 + kb) * DX_GEMM_BK;
+        dx_tma_2d(st, ta, kc, m0, &full[s]);
+        dx_tma_2d(st + A_BYTES, tal, kc, m0, &full[s]);
+        dx_tma_2d(st + 2 * A_BYTES, tb, kc, n0, &full[s]);
+        dx_tma_2d(st + 2 * A_BYTES + B_BYTES, tbl, kc, n0, &full[s]);
       }
     }
   } else if (warp == 5) {
@@ -199,6 +208,18 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
       __syncwarp();
       if (lane == 0) dx_mbar_arrive(&tempty[b]);
     }
+    if (S > 1) {  // wait for the previous parts of this tile
+      if (threadIdx.x == 0) {
+        while (true) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(tickets + tile) : "memory");
+          if ((int)(v % (unsigned)S) == part) break;
+          __nanosleep(64);
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (part > 0) mode = 1;
+    }
     const long long row = m0 + warp * 32 + lane;
     if (row < M) {
       CT* out = C + row * ldc + n0;
@@ -218,6 +239,11 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         }
       }
     }
+    if (S > 1) {  // release the next part
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) atomicAdd(tickets + tile, 1u);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -231,12 +257,14 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
 extern "C" __global__ void __launch_bounds__(192, 1)
     dx_gemm_tf32x3_n128(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
                         const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
-                        long long N, long long K, float* C, long long ldc, long long mode) {
-  dx_gemm_tf32x3<128, 3, float>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode);
+                        long long N, long long K, float* C, long long ldc, long long mode, long long ksplit,
+                        unsigned* tickets) {
+  dx_gemm_tf32x3<128, 3, float>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
 }
 extern "C" __global__ void __launch_bounds__(192, 1)
     dx_gemm_tf32x3_n128_d(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
                           const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
-                          long long N, long long K, double* C, long long ldc, long long mode) {
-  dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode);
+                          long long N, long long K, double* C, long long ldc, long long mode, long long ksplit,
+                          unsigned* tickets) {
+  dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
 }
