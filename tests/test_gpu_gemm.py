@@ -21,7 +21,8 @@ SHAPES = [
     (130, 260, 32, False, True),     # both operands transposed relative to the natural order
     (128, 128, 4, True, True),       # K below one k-block
     (1000, 520, 1024, False, False),
-    (384, 128, 4096, True, True),    # long K: many pipeline wraps
+    (384, 128, 4096, True, True),    # long K: many pipeline wraps; split-K 4
+    (256, 256, 8192, True, False),   # split-K 8 (4 tiles would leave 144 SMs idle)
     (1, 1, 8, True, False),          # single element
 ]
 
@@ -66,3 +67,18 @@ def test_matmul_fwd_uses_gemm(ctx):
     assert "tcgen05 gemm 256x256x256" in prog.plan
     (z,) = prog(x, y)
     assert oracle.rel_diff(z, restate.matmul_fwd(x, y).ravel()) <= 1e-4
+
+
+def test_split_k_plan_and_determinism(ctx):
+    """Under-filled long-K GEMMs split K across CTAs; the parts of a tile are
+    added in part order (ticket), so repeated runs are bit-identical."""
+    m, n, k = 256, 256, 8192
+    src = P.contraction(m, n, k)
+    x, y = P.contraction_inputs(m, n, k, seed=3)
+    prog = dx.Program(src, ctx=ctx)
+    assert "split-K" in prog.plan
+    a = prog(x, y)[0]
+    b = prog(x, y)[0]
+    np.testing.assert_array_equal(a, b)
+    assert oracle.rel_diff(a, restate.contraction(x, y).ravel()) <= 1e-4
+
