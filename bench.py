@@ -349,6 +349,44 @@ def reference_rate(sample_n, chunks, reps, warm=1):
     return (sample_n / N_PER_GPU) / sec, sec, times
 
 
+def reference_sample_rate(config, chunks, reps=1):
+    """CPU baseline for the histogram / matmul / MLP lines: the unmodified
+    reference evaluator (oracle/_ref) on a bounded sample of the workload,
+    scaled to the full workload by the stated work ratio (an extrapolation:
+    the reference's cost grows at least linearly in that work)."""
+    import oracle
+    from paper_2104_05372_b200 import programs as P
+    if config == "histogram":
+        n, k = 200_000, 4096
+        args_ = (P.histogram_inputs(n, k, seed=7),)
+        src, scale = P.histogram(n, k), n / (1 << 28)
+        what = f"histogram of n={n} keys into {k} bins; scaled by n / 2^28"
+    elif config == "matmul":
+        n = 48
+        x, y = P.matmul_inputs(n, seed=7)
+        args_ = (x, y)
+        src, scale = P.matmul_grad(n), (n / 256) ** 3
+        what = f"matmul fwd+grad at n={n}; scaled by (n/256)^3"
+    elif config == "mlp":
+        b, i, h, o = 64, 32, 32, 32
+        x, w1, w2 = P.mlp_inputs(b, i, h, o, seed=7)
+        args_ = (x, [w1, w2])
+        src = P.mlp_grad(b, i, h, o)
+        scale = (b * (i * h + h * o)) / (8192 * (1024 * 1024 + 1024 * 1024))
+        what = f"MLP fwd+grad at batch {b}, widths {i}/{h}/{o}; scaled by B(IH + HO)"
+    else:
+        return None
+    prog = oracle.RefProgram(src)
+    prog(*args_, chunks=chunks)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        prog(*args_, chunks=chunks)
+        times.append(time.perf_counter() - t0)
+    sec = statistics.mean(times)
+    return scale / sec, sec, what
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
@@ -528,6 +566,16 @@ def main():
                                f"3 evals, {sec:.3f} s/eval, scaled linearly to 1M points (the reference's "
                                f"transposed sum is O(n^2): optimistic for the reference)")}
             except Exception as e:  # the oracle library must travel with the repo
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+        if world == 1 and not args.no_cpu_baseline and not args.profile and args.config in ("histogram", "matmul", "mlp"):
+            try:
+                cores = os.cpu_count() or 1
+                rate, sec, what = reference_sample_rate(args.config, cores)
+                line["cpu_baseline"] = {
+                    "value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": f"reference evalExpr (oracle/_ref), chunks={cores}: {what}; {sec:.3f} s per sample eval"}
+            except Exception as e:
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
         if world == 1 and not args.no_cpu_baseline and not args.profile and spec.get("gmm"):
