@@ -124,6 +124,7 @@ static int launch(dxg_gmm* g, int k, unsigned grid, unsigned block, unsigned sme
 extern "C" {
 
 int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global, dxg_gmm** out) {
+  if (!cx || !out) { setError("dxg_gmm_create: null argument"); return DXC_E_ARG; }
   if (d != D) { setError("dxg_gmm_create: d must be 64"); return DXC_E_ARG; }
   if (k < 1 || n_local < 1 || n_global < n_local) { setError("dxg_gmm_create: bad sizes"); return DXC_E_ARG; }
   dxrt::Ctx* ctx = cx;
@@ -215,6 +216,7 @@ int dxg_gmm_destroy(dxg_gmm* g) {
 }
 
 int dxg_gmm_set_params(dxg_gmm* g, const float* alphas, const float* means, const float* icf) {
+  if (!g || !alphas || !means || !icf) { setError("dxg_gmm_set_params: null argument"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
   CUstream s = g->ctx->stream;
@@ -226,6 +228,7 @@ int dxg_gmm_set_params(dxg_gmm* g, const float* alphas, const float* means, cons
 }
 
 int dxg_gmm_set_points(dxg_gmm* g, const float* x) {
+  if (!g || !x) { setError("dxg_gmm_set_points: null argument"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
   return check(cuMemcpyHtoDAsync(g->x, x, (size_t)g->n * D * 4, g->ctx->stream), "H2D x");
@@ -240,6 +243,8 @@ int dxg_gmm_input_device_ptrs(dxg_gmm* g, void** alphas, void** means, void** ic
 }
 
 int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
+  if (!g) { setError("dxg_gmm_run: null plan"); return DXC_E_ARG; }
+  if (!(gamma > 0.0) || wm < 0) { setError("dxg_gmm_run: Wishart gamma must be > 0 and m >= 0"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
   g->gamma = gamma;

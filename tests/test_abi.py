@@ -152,3 +152,13 @@ def test_gmm_module_compiles_for_sm100a():
         assert f"Function : {k}" in sass, k
     assert "UTCHMMA" in sass
     assert "UBLKCP" in sass
+
+
+def test_gmm_abi_rejects_bad_arguments():
+    """Argument checks run before any device work (no GPU needed)."""
+    lib = dx.lib()
+    g = ctypes.c_void_p()
+    assert lib.dxg_gmm_create(None, 64, 4, 100, 100, ctypes.byref(g)) == dx.DXC_E_ARG
+    assert lib.dxg_gmm_set_params(None, None, None, None) == dx.DXC_E_ARG
+    assert lib.dxg_gmm_set_points(None, None) == dx.DXC_E_ARG
+    assert lib.dxg_gmm_run(None, 1.0, 0, 1) == dx.DXC_E_ARG
