@@ -39,7 +39,11 @@
 
 #define DXG_D 64
 #define DXG_ICF (DXG_D * (DXG_D + 1) / 2)
-#define DXG_GC 8                 // components resident per forward CTA
+#ifndef DXG_GC
+#define DXG_GC 8                 // components resident per forward CTA (8; 4 measured slower: 5.4 vs 4.1 ms)
+#endif
+#define DXG_FXS (DXG_GC == 4 ? 4 : 2)  // forward X-tile stages
+#define DXG_NH (DXG_GC / 4)          // N=256 MMA groups (TMEM halves) per tile
 #define DXG_TM 128               // points per forward tile (MMA M)
 #define DXG_BC 64                // points per backward chunk (MMA K extent)
 #define DXG_BN 64                // backward MMA N: the 64 dims of X^T
@@ -270,7 +274,7 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_prep_x(const float* x, 
 // epilogue (warp w drains TMEM lanes 32*(w%4)..+31 = tile rows, of one half).  TMEM: 512
 // columns = 8 components x 64, in two halves of 4 components that alternate
 // between MMA and epilogue.
-#define DXG_FWD_SMEM (2 * DXG_GC * 64 * 128 + 2 * 2 * DXG_TM * 128 + 1024)
+#define DXG_FWD_SMEM (2 * DXG_GC * 64 * 128 + DXG_FXS * 2 * DXG_TM * 128 + 1024)
 extern "C" __global__ void __launch_bounds__(320, 1)
     dx_gmm_fwd(const unsigned char* __restrict__ qimg, const unsigned char* __restrict__ ximg,
                const float* __restrict__ bvec, const float* __restrict__ cvec, const float* __restrict__ svec,
@@ -279,8 +283,8 @@ extern "C" __global__ void __launch_bounds__(320, 1)
   extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
   unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
   unsigned char* qs = smem;                                // 128 KB: hi (64 KB) then lo
-  unsigned char* xsm = smem + 2 * DXG_GC * 64 * 128;       // 2 stages x 32 KB
-  __shared__ __align__(8) unsigned long long xfull[2], xempty[2], tfull[2], tempty[2], qfull, qempty;
+  unsigned char* xsm = smem + 2 * DXG_GC * 64 * 128;       // DXG_FXS stages x 32 KB
+  __shared__ __align__(8) unsigned long long xfull[DXG_FXS], xempty[DXG_FXS], tfull[2], tempty[2], qfull, qempty;
   __shared__ float bsm[DXG_GC][DXG_D], dsm[DXG_GC][DXG_D];
   __shared__ float csm[DXG_GC], ssm[DXG_GC];
   __shared__ unsigned tmem_base;
@@ -290,11 +294,13 @@ extern "C" __global__ void __launch_bounds__(320, 1)
   const int units = NG * P;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < DXG_FXS; ++s) {
       dx_mbar_init(&xfull[s], 1);
       dx_mbar_init(&xempty[s], 9);  // MMA commit + the 8 epilogue warps (they read x)
+    }
+    for (int s = 0; s < 2; ++s) {
       dx_mbar_init(&tfull[s], 1);
-      dx_mbar_init(&tempty[s], 4);
+      dx_mbar_init(&tempty[s], 32 / DXG_GC);  // epilogue warps per TMEM buffer
     }
     dx_mbar_init(&qfull, 1);
     dx_mbar_init(&qempty, 1);
@@ -321,8 +327,8 @@ extern "C" __global__ void __launch_bounds__(320, 1)
         dx_mbar_expect_tx(&qfull, 2 * DXG_GC * 64 * 128);
         dx_bulk_g2s(qs, qimg + (long long)g * 2 * DXG_GC * 64 * 128, 2 * DXG_GC * 64 * 128, &qfull);
         for (long long t = t0; t < t1; ++t, ++it) {
-          const int s = it & 1;
-          if (it >= 2) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it >> 1) - 1) & 1));
+          const int s = it % DXG_FXS;
+          if (it >= DXG_FXS) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it / DXG_FXS) - 1) & 1));
           dx_mbar_expect_tx(&xfull[s], 2 * DXG_TM * 128);
           dx_bulk_g2s(xsm + s * 2 * DXG_TM * 128, ximg + t * 2 * DXG_TM * 128, 2 * DXG_TM * 128, &xfull[s]);
         }
@@ -339,14 +345,15 @@ extern "C" __global__ void __launch_bounds__(320, 1)
         dx_mbar_wait_bounded(&qfull, (unsigned)(qn & 1));
         dxg_fence_after();
         for (long long t = t0; t < t1; ++t, ++it) {
-          const int s = it & 1;
-          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+          const int s = it % DXG_FXS;
+          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it / DXG_FXS) & 1));
           dxg_fence_after();
           const unsigned xa = xaddr + (unsigned)(s * 2 * DXG_TM * 128);
-          for (int h = 0; h < 2; ++h, ++tt) {
-            if (tt >= 2) dx_mbar_wait_bounded(&tempty[h], (unsigned)(((tt >> 1) - 1) & 1));
+          for (int h = 0; h < DXG_NH; ++h, ++tt) {
+            const int bb = tt & 1;  // TMEM buffer (with DXG_GC = 4: alternates per tile)
+            if (tt >= 2) dx_mbar_wait_bounded(&tempty[bb], (unsigned)(((tt >> 1) - 1) & 1));
             dxg_fence_after();
-            const unsigned td = tmem + (unsigned)(h * 256);
+            const unsigned td = tmem + (unsigned)(bb * 256);
             const unsigned qh = qaddr + (unsigned)(h * 256 * 128), ql = qh + DXG_GC * 64 * 128;
 #pragma unroll
             for (int kk = 0; kk < DXG_D / 16; ++kk) {
@@ -358,7 +365,7 @@ extern "C" __global__ void __launch_bounds__(320, 1)
               dxg_umma_f16(td, ah, bl, idesc, 1u);
               dxg_umma_f16(td, al, bh, idesc, 1u);
             }
-            dx_umma_commit(&tfull[h]);
+            dx_umma_commit(&tfull[bb]);
           }
           dx_umma_commit(&xempty[s]);
         }
@@ -366,8 +373,8 @@ extern "C" __global__ void __launch_bounds__(320, 1)
       }
     }
   } else {
-    // epilogue: warps 2..9; warp w drains TMEM lane quarter w % 4 of half
-    // (w - 2) / 4 (components 0-3 or 4-7 of the resident group)
+    // epilogue: warps 2..9; warp w drains TMEM lane quarter w % 4 for the
+    // components [hsel * GC/2, (hsel + 1) * GC/2) of the resident group
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int hsel = (warp - 2) >> 2;
@@ -394,8 +401,8 @@ extern "C" __global__ void __launch_bounds__(320, 1)
         // this row's scaled point sx*x from the A stage (fp16 hi + lo)
         float xr[DXG_D];
         {
-          const int s = it & 1;
-          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it >> 1) & 1));
+          const int s = it % DXG_FXS;
+          dx_mbar_wait_bounded(&xfull[s], (unsigned)((it / DXG_FXS) & 1));
           const unsigned char* xh = xsm + s * 2 * DXG_TM * 128;
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
@@ -412,15 +419,16 @@ extern "C" __global__ void __launch_bounds__(320, 1)
           __syncwarp();
           if (lane == 0) dx_mbar_arrive(&xempty[s]);
         }
-        for (int h = 0; h < 2; ++h, ++tt) {
-          if (h != hsel) continue;
-          dx_mbar_wait_bounded(&tfull[h], (unsigned)((tt >> 1) & 1));
+        for (int h = 0; h < DXG_NH; ++h, ++tt) {
+          const int bb = tt & 1;
+          if (DXG_NH == 2 && h != hsel) continue;
+          dx_mbar_wait_bounded(&tfull[bb], (unsigned)((tt >> 1) & 1));
           dxg_fence_after();
 #pragma unroll 1
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = h * 4 + jj;
+          for (int jj = 0; jj < DXG_GC / 2; ++jj) {
+            const int j = hsel * (DXG_GC / 2) + jj;  // component within the group
             unsigned v0[16], v1[16], v2[16], v3[16];
-            const unsigned ta = lanebase + (unsigned)(h * 256 + jj * 64);
+            const unsigned ta = lanebase + (unsigned)(bb * 256 + (j % 4) * 64);
             DXG_TMEM_LD16(ta, v0);
             DXG_TMEM_LD16(ta + 16, v1);
             DXG_TMEM_LD16(ta + 32, v2);
@@ -448,7 +456,7 @@ extern "C" __global__ void __launch_bounds__(320, 1)
           }
           dxg_fence_before();
           __syncwarp();
-          if (lane == 0) dx_mbar_arrive(&tempty[h]);
+          if (lane == 0) dx_mbar_arrive(&tempty[bb]);
         }
       }
     }

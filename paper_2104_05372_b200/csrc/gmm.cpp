@@ -22,7 +22,8 @@ namespace {
 
 constexpr int D = 64;
 constexpr int ICF = D * (D + 1) / 2;
-constexpr int GC = 8;
+constexpr int GC = 8;      // DXG_GC
+constexpr int FXS = 2;     // DXG_FXS
 constexpr int TM = 128;
 constexpr int BC = 64;
 constexpr int BN = 64;
@@ -30,7 +31,7 @@ constexpr int WP = 2 * (1 + 64);  // DXG_WP
 constexpr int FMAX = 8;
 constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
-constexpr int FWD_SMEM = 2 * GC * 64 * 128 + 2 * 2 * TM * 128 + 1024;
+constexpr int FWD_SMEM = 2 * GC * 64 * 128 + FXS * 2 * TM * 128 + 1024;
 inline int bwd4Smem() { return NXS * 2 * (BN * 128) + 2 * BN * 128 * 4 + 1024; }
 inline int bwdSmem() {
   const bool smemA = std::getenv("DEXLET_GMM_SMEM_A") != nullptr;
