@@ -468,6 +468,15 @@ struct KGen {
   bool usesErr = false;
   bool usesScratch = false;
   int curBranch = 0;
+  // Warp-per-ordinal mode for kernels whose outer loop is short and whose
+  // body is a long reduction loop into local scalar cells (row sums): the
+  // lanes split that loop and warp-sum the cells after it.
+  bool warpRowOK = true;          // pass 0: nothing disqualifies the mode
+  int laneLoopId = -1;            // pass 0: the reduction loop (depth 1, trip >= 64, effect-only)
+  bool inCand = false;            // pass 0: inside the candidate loop's body
+  bool warpRow = false;           // pass 1: emit in warp-per-ordinal mode
+  bool inLaneLoop = false;        // pass 1: inside the lane loop's body
+  std::set<std::string> innerCells, laneCells;  // local cells created in / reduced after the lane loop
 
   explicit KGen(Lowering& l) : L(l) {}
 
@@ -2230,6 +2239,10 @@ class Lowering {
     // Emit the loop body into a side buffer first to learn the element type.
     std::string q = g.fresh("j");
     int id = openLoop(g, n);
+    const bool cand = g.pass == 0 && g.loopDepth[id] == 1 && n >= 64 && g.laneLoopId < 0 && !g.inCand;
+    const bool lane = g.pass == 1 && g.warpRow && id == g.laneLoopId;
+    if (cand) { g.inCand = true; g.innerCells.clear(); }
+    if (lane) { g.inLaneLoop = true; g.innerCells.clear(); g.laneCells.clear(); }
     std::string saved;
     std::string* outer = g.out;
     std::string bodyCode;
@@ -2243,13 +2256,19 @@ class Lowering {
     // result storage
     DTy tt = tTable(d, elem->ty);
     std::vector<LeafInfo> el = leaves(elem->ty);
+    if (cand) {
+      g.inCand = false;
+      if (el.empty()) g.laneLoopId = id;  // effect-only: a reduction into local cells
+    }
+    if (lane) g.inLaneLoop = false;
     g.out = outer;
     g.ind = savedInd;
     std::vector<Slot> slots;
     if (!el.empty()) slots = localArrays(g, tt);
     if (g.out) {
       g.line(std::string(n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
-      g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
+      if (lane) g.line("for (int " + q + " = dx_lane; " + q + " < " + lit(n) + "; " + q + " += 32) {");
+      else g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
       g.out->append(bodyCode);
     }
     g.ind = savedInd + 1;
@@ -2260,6 +2279,8 @@ class Lowering {
     }
     g.ind = savedInd;
     g.line("}");
+    if (lane)  // every lane holds a partial of each cell the loop accumulated
+      for (const std::string& c : g.laneCells) g.line(c + "[0] = dx_warp_sum(" + c + "[0]);");
     closeLoop(g);
     if (el.empty()) {
       auto k = std::make_shared<KVal>();
@@ -2513,6 +2534,8 @@ class Lowering {
       if (KV m = accumToMapK(g, s, r, payload)) return m;
     std::vector<Slot> slots = localArrays(g, payload, true);
     std::vector<LeafInfo> plv = leaves(payload);
+    if (g.inCand || g.inLaneLoop)
+      for (auto& sl : slots) g.innerCells.insert(sl.base);
     for (size_t l = 0; l < slots.size(); ++l)
       if (plv[l].count == 1) g.freshCell[slots[l].base] = (int)g.loopStack.size();
     auto ref = std::make_shared<KVal>();
@@ -2572,6 +2595,11 @@ class Lowering {
                    const KV& val, Span sp) {
     const Slot& sl = ref->slots[leaf];
     if (ref->cell < 0) {  // thread-local cell
+      if ((g.inCand || g.inLaneLoop) && !g.innerCells.count(sl.base)) {
+        // an outer cell accumulated by the reduction loop: scalar cells only
+        if (sl.off != "0" || ref->slots.size() != 1) g.warpRowOK = false;
+        if (g.inLaneLoop) g.laneCells.insert(sl.base);
+      }
       auto fr = g.freshCell.find(sl.base);
       if (fr != g.freshCell.end() && fr->second == (int)g.loopStack.size() && sl.off == "0") {
         // first write into a zeroed cell, executed at most once: a store
@@ -2582,6 +2610,7 @@ class Lowering {
       if (fr != g.freshCell.end()) g.freshCell.erase(fr);
       return;
     }
+    g.warpRowOK = false;  // a plan cell: every lane would add its contribution
     int site = g.accumSiteCounter++;
     CellUse& cu = cellUse(g, ref->cell, sl.cellLeaf);
     if (g.pass == 0) {
@@ -2706,6 +2735,7 @@ class Lowering {
 
   KV getK(KGen& g, const KV& ref, Span sp) {
     if (ref->k != KVal::Ref) notLowerable("get of a non-reference", sp);
+    if (g.inCand) g.warpRowOK = false;
     std::vector<Slot> slots = ref->slots;
     if (ref->cell >= 0) {
       if (!g.serial) fail(ErrCode::StateInParallel, "state cell read inside a parallel kernel", sp);
@@ -2719,6 +2749,7 @@ class Lowering {
   }
 
   void putK(KGen& g, const KV& ref, const KV& v, Span sp) {
+    g.warpRowOK = false;
     if (ref->k != KVal::Ref) notLowerable("put of a non-reference", sp);
     std::vector<Slot> slots = ref->slots;
     if (ref->cell >= 0) {
@@ -2917,6 +2948,11 @@ void Lowering::decideStrategies(KGen& g) {
 KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial, int U,
                       std::vector<int>& outBufs, std::vector<long long>& outOffs,
                       const std::vector<int>* intoBufs, const std::vector<long long>* intoOffs) {
+  if (g.pass == 0) {
+    g.warpRowOK = true;
+    g.laneLoopId = -1;
+  }
+  g.inCand = g.inLaneLoop = false;
   g.loopStack.clear();
   g.loopDepth.clear();
   g.loopTrip.clear();
@@ -3168,8 +3204,11 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       if (g.streamUse[b].first == cu.rowD && plan.bufs[b].kind == SK::F && !std::getenv("DEXLET_NO_ALIAS"))
         cu.aliasStage = b;
   }
+  // warp per ordinal for short outer loops over long reductions (row sums)
+  g.warpRow = !serial && g.warpRowOK && g.laneLoopId >= 0 && g.cells.empty() && !hasRow && !g.tile &&
+              kb0.dims.size() == 1 && total <= 148LL * 256 && !std::getenv("DEXLET_NO_WARPROW");
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
-  int U = (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
+  int U = g.warpRow ? 1 : (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
   // more 16-byte loads in flight per thread for the tiniest bodies (histograms):
   // one load per thread and grid-stride step leaves HBM latency exposed
   if (U == 4 && g.lines <= 8) {
@@ -3480,6 +3519,10 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       // block-uniform tiles: every thread runs the same trip count
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride) {\n";
       src << "    const long long dx_s = dx_base + threadIdx.x;\n";
+    } else if (g.warpRow) {
+      // one warp per ordinal (warp-uniform), the lanes split the reduction loop
+      src << "  for (long long dx_base = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dx_base < dx_n; dx_base += dx_stride >> 5) {\n";
+      src << "    const long long dx_s = dx_base;\n";
     } else {
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); dx_base < dx_n; dx_base += dx_stride) {\n";
       src << "    const long long dx_s = dx_base + dx_lane;\n";
@@ -3636,8 +3679,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   ks.threads = serial ? 32 : g.threads;
   ks.smem = smem;
   ks.minGrid = U;
+  ks.warpRow = g.warpRow;
   ks.coop = coop;
-  ks.note = note;
+  ks.note = note + (g.warpRow ? " (warp per ordinal)" : "");
   addStep(ks);
   int kstep = (int)plan.steps.size() - 1;
   for (auto& cu : g.cells)

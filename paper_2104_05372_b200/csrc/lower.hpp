@@ -76,6 +76,7 @@ struct Step {
   int threads = 256;
   int smem = 0;           // dynamic shared memory bytes
   int minGrid = 0;        // ordinals per thread (U)
+  bool warpRow = false;   // one warp per ordinal (32 threads per iteration)
   bool coop = false;      // cooperative launch (in-kernel grid barrier + finalize)
   bool dead = false;      // Zero step taken over by the first kernel writing the buffer
   long long fixedGrid = 0;  // >0: launch exactly this many blocks (tile kernels: GEMM, transpose)

@@ -140,6 +140,7 @@ int Program::prepare() {
     if (const char* e = std::getenv("DEXLET_BLOCKS_PER_SM")) nb = std::max(1, std::min(nb, std::atoi(e)));  // (experiments)
     long long U = s.minGrid > 0 ? s.minGrid : 1;  // ordinals per thread
     long long need = ((hi - lo + U - 1) / U + s.threads - 1) / s.threads;
+    if (s.warpRow) need = ((hi - lo) * 32 + s.threads - 1) / s.threads;
     long long cap = (long long)ctx->smCount * nb;
     long long grid = std::max(1LL, std::min(need, cap));
     grids[i] = (int)grid;
