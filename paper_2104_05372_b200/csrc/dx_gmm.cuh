@@ -476,14 +476,18 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     // one pass, online max: s = sum exp(beta - m) rescaled when m grows
     float m = -3.0e38f, s = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < K; ++k) {
-      const float v = beta[(long long)k * npad + i];
-      if (v > m) {
-        s = s * __expf(m - v) + 1.f;
-        m = v;
-      } else {
-        s += __expf(v - m);
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      float v[8];  // the 8 loads of a step are independent (issued together)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = k0 + q < K ? beta[(long long)(k0 + q) * npad + i] : -3.0e38f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (v[q] > m) {
+          s = s * __expf(m - v[q]) + 1.f;
+          m = v[q];
+        } else {
+          s += __expf(v[q] - m);
+        }
       }
     }
     const float l = m + __logf(s);

@@ -150,7 +150,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   g->P2 = pickP2(g->quad ? (k + 3) / 4 : g->NP, g->C, sms);
   if (const char* e = std::getenv("DEXLET_GMM_P2")) g->P2 = std::max(1, std::atoi(e));  // (experiments)
   g->gridB = (int)std::min<long long>(sms, (long long)(g->quad ? (k + 3) / 4 : g->NP) * g->P2);
-  g->gridL = (int)std::min<long long>(4 * sms, (g->n + 255) / 256);
+  g->gridL = (int)std::min<long long>(8 * sms, (g->n + 255) / 256);  // 2048 threads per SM: more loads in flight
   // DEXLET_GMM_SMEM_A=1: backward A operand staged in shared memory (A/B)
   std::string src = std::string(std::getenv("DEXLET_GMM_SMEM_A") ? "#define DXG_TMEM_A 0\n" : "");
   if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
