@@ -122,3 +122,35 @@ def test_mlp_and_matmul_grad_on_tensor_cores():
     assert "8589934592" not in p  # no B*H*I tape
     p = dx.Program(P.matmul_grad(256), ctx=None).plan
     assert p.count("tcgen05 gemm") == 2, p
+
+
+def test_row_sum_runs_one_warp_per_row():
+    """A short outer loop over a long reduction (the matmul's row sums) runs
+    one warp per ordinal: the lanes split the inner loop and warp-sum."""
+    prog = dx.Program(P.matmul_grad(256), ctx=None)
+    assert "(warp per ordinal)" in prog.plan
+    src = prog.source
+    assert "+= 32)" in src and "dx_warp_sum(" in src
+
+
+def test_effect_nest_flattened_and_broadcast_kept_lazy():
+    """MLP dY: the per-row cotangent broadcast stays a lazy map inside the
+    kernel (no local array) and the (batch, out) nest runs flattened."""
+    prog = dx.Program(P.mlp_grad(8192, 64, 64, 1024), ctx=None)
+    assert "(flattened)" in prog.plan
+    src = prog.source
+    i = src.index("(flattened)")
+    body = src[i:src.index('extern "C"', i)]
+    assert "[1024] = {}" not in body
+
+
+def test_long_k_gemm_is_split():
+    prog = dx.Program(P.contraction(256, 256, 8192), ctx=None)
+    assert "split-K 8" in prog.plan
+    prog = dx.Program(P.contraction(1000, 520, 1024), ctx=None)
+    assert "split-K" not in prog.plan  # enough output tiles, short K
+
+
+def test_tiny_map_bodies_keep_three_vector_loads_in_flight():
+    prog = dx.Program(P.histogram(1 << 20, 4096), ctx=None)
+    assert prog.source.count("const int4 w = *(const int4*)") == 3
