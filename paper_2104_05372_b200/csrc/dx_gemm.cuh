@@ -225,10 +225,25 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
       CT* out = C + row * ldc + n0;
       const bool vec = sizeof(CT) == 4 && n0 + BN <= N && ((ldc | n0) & 3) == 0 &&
                        ((reinterpret_cast<unsigned long long>(C) & 15) == 0);
+      const bool vecd = sizeof(CT) == 8 && n0 + BN <= N && ((ldc | n0) & 1) == 0 &&
+                        ((reinterpret_cast<unsigned long long>(C) & 15) == 0);
       if (vec && mode == 0) {
 #pragma unroll
         for (int j = 0; j < BN; j += 4)
           *reinterpret_cast<float4*>(out + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+      } else if (vecd) {
+        // f64 cells: 16-byte read-modify-writes, 16 loads in flight per batch
+        // (the row-per-thread RMW is latency-bound when few tiles exist)
+        double2* o2 = reinterpret_cast<double2*>(out);
+#pragma unroll
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          double2 cur[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) cur[q] = mode == 0 ? make_double2(0.0, 0.0) : o2[j0 / 2 + q];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            o2[j0 / 2 + q] = make_double2(cur[q].x + (double)acc[j0 + 2 * q], cur[q].y + (double)acc[j0 + 2 * q + 1]);
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < BN; ++j) {
