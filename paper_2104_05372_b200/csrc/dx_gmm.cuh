@@ -518,7 +518,7 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
 #define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_Z_BYTES + DXG_BN * 128 * 8 + 1024)
 #endif
 extern "C" __global__ void __launch_bounds__(448, 1)
-    dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
+    dx_gmm_bwd_pair(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
                int K, long long n, long long npad, int P2,
                double* __restrict__ dpart, double* __restrict__ wpart, int* __restrict__ ppart) {
@@ -883,29 +883,32 @@ extern "C" __global__ void __launch_bounds__(448, 1)
   }
 }
 
-// ---- backward, two pairs (four components) per unit ---------------------------------
-// Same math as dx_gmm_bwd, but each X^T chunk staged by the bulk-copy ring
+// ---- backward, two pairs (four components) per unit (default) ----------------------
+// Same math as dx_gmm_bwd_pair, but each X^T chunk staged by the bulk-copy ring
 // feeds the MMAs of two component pairs (the single-pair kernel is bound by
 // re-streaming X^T once per pair).  TMEM: D[q][b] (pair q, buffer b, one merged
 // accumulator) at (2q + b) * 64, A[q][s] (pair q, stage s: hi 32 + lo 32
 // columns) at 256 + (2q + s) * 64.  Warps: 0 bulk copies, 1 MMA, 2-9
 // producers (warps 2-5 pair 0, 6-9 pair 1; each thread one row (k, b) over all
-// 64 points of the chunk), 10-13 epilogue (fp32 shared accumulators per unit,
-// flushed to fp64 partial slots, one slot per unit).
+// 64 points of the chunk), 10-17 epilogue (warps 10-13 pair 0, 14-17 pair 1:
+// fp32 register accumulators promoted after every chunk, spilled to fp64
+// shared memory every DXG_F64_EVERY chunks, one fp64 partial slot per unit).
+// Promoting every chunk (64 points, 12 MMAs per TMEM accumulation) keeps the
+// error of the tensor core's fp32 accumulation at the single-pair kernel's.
 #define DXG_QWP (4 * (1 + DXG_D))
-#define DXG_BWD4_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_BN * 128 * 4 + 1024)
+#define DXG_BWD4_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_BN * 128 * 8 + 1024)
 #ifndef DXG_PROMO4
-#define DXG_PROMO4 2
+#define DXG_PROMO4 1
 #endif
-extern "C" __global__ void __launch_bounds__(448, 1)
-    dx_gmm_bwd4(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
+extern "C" __global__ void __launch_bounds__(576, 1)
+    dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                 const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
                 int K, long long n, long long npad, int P2, double* __restrict__ dpart, double* __restrict__ wpart,
                 int* __restrict__ ppart) {
   extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
   unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
   unsigned char* bs = smem;                                                      // NXS x (hi 8 KB, lo 8 KB)
-  float* dacc = reinterpret_cast<float*>(smem + DXG_NXS * 2 * DXG_XB_BYTES);   // [2][64][128]
+  double* dacc = reinterpret_cast<double*>(smem + DXG_NXS * 2 * DXG_XB_BYTES);  // [2][64][128]
   __shared__ __align__(16) float gin[DXG_NXS][5][DXG_BC];
   __shared__ __align__(16) float gw[8][64];
   __shared__ __align__(8) unsigned long long xfull[DXG_NXS], xempty[DXG_NXS], zfull[2][2], zempty[2][2],
@@ -930,7 +933,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     }
     dx_fence_mbar_init();
   }
-  for (int e = threadIdx.x; e < 2 * DXG_BN * 128; e += blockDim.x) dacc[e] = 0.f;
+  for (int e = threadIdx.x; e < 2 * DXG_BN * 128; e += blockDim.x) dacc[e] = 0.0;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
                  "r"(512)
@@ -1072,11 +1075,23 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       wp[1 + b] = msum;
     }
   } else {
-    // epilogue: warps 10..13 -> TMEM lane quarter (warp & 3); fp32 shared accumulators
-    const int qr = warp & 3;
+    // epilogue: warps 10..17 -> pair q = (warp - 10) / 4, TMEM lane quarter warp & 3
+    const int q = (warp - 10) >> 2, qr = warp & 3;
     const int row = qr * 32 + lane;
     const unsigned lanebase = tmem + ((unsigned)(qr * 32) << 16);
-    int pc = 0, slot = 0;
+    double* dq = dacc + q * DXG_BN * 128 + row;
+    float acc[DXG_BN];
+#pragma unroll
+    for (int j = 0; j < DXG_BN; ++j) acc[j] = 0.f;
+    int pc = 0, slot = 0, nacc = 0;
+    auto spill = [&]() {
+#pragma unroll
+      for (int j = 0; j < DXG_BN; ++j) {
+        dq[j * 128] += (double)acc[j];
+        acc[j] = 0.f;
+      }
+      nacc = 0;
+    };
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
       const long long qd = u % NQ, p = u / NQ;
       const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
@@ -1084,34 +1099,31 @@ extern "C" __global__ void __launch_bounds__(448, 1)
       for (long long c = c0; c < c1; ++c) {
         if (++inb == DXG_PROMO4 || c + 1 == c1) {
           const int bb = pc & 1;
-          for (int q = 0; q < 2; ++q) {
-            dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
-            dxg_fence_after();
+          dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
+          dxg_fence_after();
 #pragma unroll
-            for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
-              unsigned v[16];
-              DXG_TMEM_LD16(lanebase + (unsigned)((2 * q + bb) * 64 + j0), v);
-              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
+            unsigned v[16];
+            DXG_TMEM_LD16(lanebase + (unsigned)((2 * q + bb) * 64 + j0), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-              for (int j = 0; j < 16; ++j) dacc[(q * DXG_BN + j0 + j) * 128 + row] += __uint_as_float(v[j]);
-            }
-            dxg_fence_before();
-            __syncwarp();
-            if (lane == 0) dx_mbar_arrive(&tempty[q][bb]);
+            for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]);
           }
+          dxg_fence_before();
+          __syncwarp();
+          if (lane == 0) dx_mbar_arrive(&tempty[q][bb]);
           ++pc;
           inb = 0;
+          if (++nacc == DXG_F64_EVERY) spill();
         }
       }
       // flush this unit: rows (q, row) of the quad's D to an fp64 slot
-      double* dst = dpart + ((long long)blockIdx.x * DXG_FMAX + slot) * 256 * DXG_BN;
-      for (int q = 0; q < 2; ++q) {
-        double* dq = dst + ((long long)q * 128 + row) * DXG_BN;
+      spill();
+      double* dst = dpart + (((long long)blockIdx.x * DXG_FMAX + slot) * 256 + q * 128 + row) * DXG_BN;
 #pragma unroll 4
-        for (int j = 0; j < DXG_BN; ++j) {
-          dq[j] = (double)dacc[(q * DXG_BN + j) * 128 + row];
-          dacc[(q * DXG_BN + j) * 128 + row] = 0.f;
-        }
+      for (int j = 0; j < DXG_BN; ++j) {
+        dst[j] = dq[j * 128];
+        dq[j * 128] = 0.0;
       }
       if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)qd;
     }
@@ -1130,7 +1142,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* dpart, const double* wpart,
                                                                  const int* ppart, int nslot, const unsigned* xmax,
                                                                  int G, double* mom) {
-  // G components per partial slot (2: dx_gmm_bwd, 4: dx_gmm_bwd4)
+  // G components per partial slot (4: dx_gmm_bwd, 2: dx_gmm_bwd_pair)
   // the operands were scaled by the points' scale sx: D = sx^2 P, m~ sums sx m~
   const double isx = 1.0 / (double)dxg_scale_for(__uint_as_float(*xmax));
   __shared__ int slots[2048];  // host guarantees nslot <= 2048
