@@ -900,6 +900,9 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 #ifndef DXG_PROMO4
 #define DXG_PROMO4 1
 #endif
+#ifndef DXG_N128
+#define DXG_N128 1  // one N=128 MMA over [X^T hi ; X^T lo] per A split (0: three N=64 MMAs)
+#endif
 extern "C" __global__ void __launch_bounds__(576, 1)
     dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                 const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
@@ -967,6 +970,39 @@ extern "C" __global__ void __launch_bounds__(576, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
+#if DXG_N128
+      // B = [X^T hi ; X^T lo]: the two images of a chunk are contiguous SW128
+      // row groups, i.e. one N=128 operand.  D[q] (128 columns: products with
+      // x hi | x lo) = A_hi B + A_lo B over one chunk, drained every chunk.
+      const unsigned idesc = dxg_idesc_f16<2 * DXG_BN>();
+      const unsigned baddr = dx_smem_addr(bs);
+      int it = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long p = u / NQ;
+        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+        for (long long c = c0; c < c1; ++c, ++it) {
+          const int xs = it % DXG_NXS, s = it & 1;
+          dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
+          const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES);
+          for (int q = 0; q < 2; ++q) {
+            if (it > 0) dx_mbar_wait_bounded(&tempty[q][0], (unsigned)((it - 1) & 1));
+            dx_mbar_wait_bounded(&zfull[q][s], (unsigned)((it >> 1) & 1));
+            dxg_fence_after();
+            const unsigned td = tmem + (unsigned)(q * 128);
+            const unsigned tah = tmem + (unsigned)(256 + (2 * q + s) * 64), tal = tah + 32;
+#pragma unroll
+            for (int kk = 0; kk < DXG_BC / 16; ++kk) {
+              const unsigned long long db = dx_umma_desc_sw128(bh + kk * 32);
+              dxg_umma_f16_ta(td, tah + kk * 8, db, idesc, kk > 0 ? 1u : 0u);
+              dxg_umma_f16_ta(td, tal + kk * 8, db, idesc, 1u);
+            }
+            dx_umma_commit(&zempty[q][s]);
+            dx_umma_commit(&tfull[q][0]);
+          }
+          dx_umma_commit(&xempty[xs]);
+        }
+      }
+#else
       const unsigned idesc = dxg_idesc_f16<DXG_BN>();
       const unsigned baddr = dx_smem_addr(bs);
       int it = 0, pc = 0, inb = 0;
@@ -1002,6 +1038,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           }
         }
       }
+#endif
     }
   } else if (warp < 10) {
     const int pw = warp - 2, q = pw >> 2;           // pair of this producer warp
@@ -1095,8 +1132,30 @@ extern "C" __global__ void __launch_bounds__(576, 1)
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
       const long long qd = u % NQ, p = u / NQ;
       const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+#if !DXG_N128
       int inb = 0;
+#endif
       for (long long c = c0; c < c1; ++c) {
+#if DXG_N128
+        {
+          dx_mbar_wait_bounded(&tfull[q][0], (unsigned)(pc & 1));
+          dxg_fence_after();
+#pragma unroll
+          for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
+            unsigned v[16], w[16];
+            DXG_TMEM_LD16(lanebase + (unsigned)(q * 128 + j0), v);
+            DXG_TMEM_LD16(lanebase + (unsigned)(q * 128 + DXG_BN + j0), w);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+          }
+          dxg_fence_before();
+          __syncwarp();
+          if (lane == 0) dx_mbar_arrive(&tempty[q][0]);
+          ++pc;
+          if (++nacc == DXG_F64_EVERY) spill();
+        }
+#else
         if (++inb == DXG_PROMO4 || c + 1 == c1) {
           const int bb = pc & 1;
           dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
@@ -1116,6 +1175,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           inb = 0;
           if (++nacc == DXG_F64_EVERY) spill();
         }
+#endif
       }
       // flush this unit: rows (q, row) of the quad's D to an fp64 slot
       spill();

@@ -161,6 +161,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   if (std::getenv("DEXLET_GMM_DBG_NOSTTM")) src += "#define DXG_DBG_NOSTTM 1\n";
   if (const char* e = std::getenv("DEXLET_GMM_NACC")) src += std::string("#define DXG_NACC ") + e + "\n";
   if (const char* e = std::getenv("DEXLET_GMM_PROMO4")) src += std::string("#define DXG_PROMO4 ") + e + "\n";
+  if (std::getenv("DEXLET_GMM_N64")) src += "#define DXG_N128 0\n";
   src += std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
   if ((rc = ctx->loadModule(src, &g->mod))) { delete g; return rc; }
   for (int i = 0; i < K_N; ++i)
