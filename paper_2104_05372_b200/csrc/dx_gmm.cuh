@@ -144,6 +144,11 @@ __device__ __forceinline__ void dxg_named_sync(int id, int n) { asm volatile("ba
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) \
       : "r"(taddr))
 
+#define DXG_TMEM_LD8(taddr, v)                                                                     \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                   \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) \
+               : "r"(taddr))
+
 // ---- max |x| (bit pattern of a non-negative float: atomicMax on u32 orders it)
 extern "C" __global__ void __launch_bounds__(256) dx_gmm_absmax(const float* __restrict__ x, long long cnt,
                                                                 unsigned* __restrict__ out) {
@@ -1074,6 +1079,10 @@ extern "C" __global__ void __launch_bounds__(576, 1)
         const unsigned char* xl = xh + DXG_XB_BYTES;
         unsigned th[32], tl[32];
         float mchunk = 0.f;
+#ifdef DXG_DBG_NOPROD  // (timing experiment: no SIMT producer math)
+#pragma unroll
+        for (int w = 0; w < 32; ++w) th[w] = tl[w] = 0u;
+#else
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {  // 8 x 8 points
           const unsigned off_x = dxg_sw((unsigned)b, (unsigned)(cc * 8));
@@ -1092,6 +1101,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
             dxg_split2(z0, z1, th[cc * 4 + w], tl[cc * 4 + w]);
           }
         }
+#endif
         msum += (double)mchunk;
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(256 + (2 * q + s) * 64);
@@ -1126,29 +1136,33 @@ extern "C" __global__ void __launch_bounds__(576, 1)
       for (int j = 0; j < DXG_BN; ++j) {
         dq[j * 128] += (double)acc[j];
         acc[j] = 0.f;
+        if ((j & 7) == 7) asm volatile("" ::: "memory");  // <= 8 fp64 loads in flight (registers)
       }
       nacc = 0;
     };
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++slot) {
-      const long long qd = u % NQ, p = u / NQ;
-      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
+      const int qd = (int)(u % NQ);
+      const long long p = u / NQ;
+      const int nch = (int)((p + 1) * C / P2 - p * C / P2);  // chunks of this unit (32-bit: registers)
 #if !DXG_N128
       int inb = 0;
 #endif
-      for (long long c = c0; c < c1; ++c) {
+      for (int c = 0; c < nch; ++c) {
 #if DXG_N128
         {
           dx_mbar_wait_bounded(&tfull[q][0], (unsigned)(pc & 1));
           dxg_fence_after();
 #pragma unroll
-          for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
-            unsigned v[16], w[16];
-            DXG_TMEM_LD16(lanebase + (unsigned)(q * 128 + j0), v);
-            DXG_TMEM_LD16(lanebase + (unsigned)(q * 128 + DXG_BN + j0), w);
+#ifndef DXG_DBG_NODRAIN
+          for (int j0 = 0; j0 < DXG_BN; j0 += 8) {  // x8 loads: acc[64] + 16 in flight (96 registers at 576 threads)
+            unsigned v[8], w[8];
+            DXG_TMEM_LD8(lanebase + (unsigned)(q * 128 + j0), v);
+            DXG_TMEM_LD8(lanebase + (unsigned)(q * 128 + DXG_BN + j0), w);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+            for (int j = 0; j < 8; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
           }
+#endif
           dxg_fence_before();
           __syncwarp();
           if (lane == 0) dx_mbar_arrive(&tempty[q][0]);
@@ -1156,7 +1170,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           if (++nacc == DXG_F64_EVERY) spill();
         }
 #else
-        if (++inb == DXG_PROMO4 || c + 1 == c1) {
+        if (++inb == DXG_PROMO4 || c + 1 == nch) {
           const int bb = pc & 1;
           dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
           dxg_fence_after();
@@ -1185,7 +1199,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
         dst[j] = dq[j * 128];
         dq[j * 128] = 0.0;
       }
-      if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)qd;
+      if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = qd;
     }
   }
   dxg_fence_before();

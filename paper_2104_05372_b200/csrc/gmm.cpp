@@ -156,6 +156,7 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   std::string src = std::string(std::getenv("DEXLET_GMM_SMEM_A") ? "#define DXG_TMEM_A 0\n" : "");
   if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
   if (std::getenv("DEXLET_GMM_DBG_NOPROD")) src += "#define DXG_DBG_NOPROD 1\n";
+  if (std::getenv("DEXLET_GMM_DBG_NODRAIN")) src += "#define DXG_DBG_NODRAIN 1\n";
   if (std::getenv("DEXLET_GMM_DBG_NOMMA")) src += "#define DXG_DBG_NOMMA 1\n";
   if (std::getenv("DEXLET_GMM_DBG_NOGIN")) src += "#define DXG_DBG_NOGIN 1\n";
   if (std::getenv("DEXLET_GMM_DBG_NOSTTM")) src += "#define DXG_DBG_NOSTTM 1\n";
