@@ -311,22 +311,26 @@ def peaks(bound="hbm"):
     return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s bf16)"
 
 
-def traffic_per_launch(config="kmeans"):
+def traffic_per_launch(config="kmeans", kernel=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from
-    the committed ncu --set full capture (profiles/r01c_<config>_ncu_summary.json)."""
-    p = os.path.join(ROOT, "profiles", f"r01c_{config}_ncu_summary.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        j = json.load(f)
+    the committed ncu --set full capture (profiles/r01{d,c}_<config>_ncu_summary.json,
+    newest first), per launch; None when no capture of that kernel is committed."""
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for k in j.get("kernels", []):
-        m = k["metrics"]
-        try:
-            rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
-            return float(rd["value"]) * scale[rd["unit"]] + float(wr["value"]) * scale[wr["unit"]]
-        except (KeyError, ValueError):
+    for tag in ("r01d", "r01c"):
+        p = os.path.join(ROOT, "profiles", f"{tag}_{config}_ncu_summary.json")
+        if not os.path.exists(p):
             continue
+        with open(p) as f:
+            j = json.load(f)
+        for k in j.get("kernels", []):
+            if kernel is not None and k.get("name") != kernel:
+                continue
+            m = k["metrics"]
+            try:
+                rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
+                return float(rd["value"]) * scale[rd["unit"]] + float(wr["value"]) * scale[wr["unit"]]
+            except (KeyError, ValueError):
+                continue
     return None
 
 
@@ -533,7 +537,7 @@ def main():
         # the dominant kernel's own algorithmic work (GMM: per kernel; else the whole step)
         work = spec.get("work_by_kernel", {}).get(dom[0], work)
         achieved = work / (dom_ms_max * 1e-3) / (1e9 if spec["bound"] == "hbm" else 1e12)
-        tr = traffic_per_launch(args.config) if args.config in ("kmeans", "histogram") else None
+        tr = traffic_per_launch(args.config, dom[0])
         line = {
             "metric": spec["metric"], "value": world * 1000.0 / ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
