@@ -154,3 +154,14 @@ def test_long_k_gemm_is_split():
 def test_tiny_map_bodies_keep_three_vector_loads_in_flight():
     prog = dx.Program(P.histogram(1 << 20, 4096), ctx=None)
     assert prog.source.count("const int4 w = *(const int4*)") == 3
+
+
+def test_transposed_gemm_operands_use_a_tiled_prologue():
+    # an operand read along its row variable (stride 1 over rows) goes through a
+    # 32x32 shared-memory transpose; a K-contiguous operand is a vector map
+    prog = dx.Program(P.contraction(130, 260, 36, True, False), ctx=None)
+    ops = [l for l in prog.plan.split("\n") if "gemm operand" in l]
+    assert len(ops) == 2
+    assert "tiled transpose" not in ops[0] and "tiled transpose" in ops[1]
+    assert "__shared__ float th[32][33]" in prog.source
+    assert "reinterpret_cast<float4*>(hi)[t]" in prog.source
