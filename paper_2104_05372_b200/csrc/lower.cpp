@@ -3639,9 +3639,14 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         default: break;
       }
     }
+    // (timing experiment, wrong results: DEXLET_DBG_COOP=1 drops the folds,
+    // 2 also the grid barrier)
+    static const int dbgCoop = std::getenv("DEXLET_DBG_COOP") ? std::atoi(std::getenv("DEXLET_DBG_COOP")) : 0;
+    if (coop && dbgCoop >= 2) src << "  return;\n";
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
       src << "  dx_grid_barrier(p" << syncBuf << ");\n";
+      if (dbgCoop >= 1) src << "  return;\n";
       if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
       for (size_t i = 0; i < g.cells.size(); ++i) {
         CellUse& cu = g.cells[i];

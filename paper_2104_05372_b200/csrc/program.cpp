@@ -266,7 +266,9 @@ int Program::run() {
   if (!graphExec) {
     // capture the whole plan once; replay it with a single launch per run
     if ((rc = dxrt::check(cuStreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture"))) return rc;
+    capturing = true;
     int irc = issue();
+    capturing = false;
     CUgraph graph = nullptr;
     CUresult er = cuStreamEndCapture(ctx->stream, &graph);
     if (irc) { if (graph) cuGraphDestroy(graph); return irc; }
@@ -340,7 +342,7 @@ int Program::issue() {
         if (timing) {
           for (size_t e = 0; e < kernelEventStep.size(); ++e)
             if (kernelEventStep[e] == (int)i) ev = (int)e;
-          if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].first, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
+          if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].first, st, capturing ? CU_EVENT_RECORD_EXTERNAL : CU_EVENT_RECORD_DEFAULT), "event"))) return rc;
         }
         if (s.coop) {
           CUlaunchConfig cfg = {};
@@ -357,7 +359,7 @@ int Program::issue() {
         } else if ((rc = launch(funcs[i], grids[i], s.threads, s.smem, argv.data()))) {
           return rc;
         }
-        if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].second, st, CU_EVENT_RECORD_EXTERNAL), "event"))) return rc;
+        if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].second, st, capturing ? CU_EVENT_RECORD_EXTERNAL : CU_EVENT_RECORD_DEFAULT), "event"))) return rc;
         ++launches;
         break;
       }

@@ -47,6 +47,7 @@ struct Program {
   int buildTensorMaps();
   CUgraphExec graphExec = nullptr;
   bool useGraph = true;
+  bool capturing = false;  // issue() is being captured into the graph (external event nodes)
   bool timing = false;
   std::vector<std::pair<CUevent, CUevent>> kernelEvents;  // per kernel step
   std::vector<int> kernelEventStep;
