@@ -46,6 +46,16 @@ UNIT = "evals/s"
 
 
 def config_spec(name, world):
+    """Workloads of BASELINE.json configs; metric and workload text are shared
+    with the reference arm (ref_config)."""
+    spec = _config_spec(name, world)
+    if spec is not None:
+        spec["metric"], cfg = ref_config(name, world)
+        spec["workload"] = cfg["workload"]
+    return spec
+
+
+def _config_spec(name, world):
     """Workloads of BASELINE.json configs.  The default (driver) run is
     kmeans = configs[1]; the others are for DESIGN.md measurements."""
     from paper_2104_05372_b200 import programs as P
@@ -398,42 +408,66 @@ def reference_sample_rate(config, chunks, reps=1):
     return scale / sec, sec, what
 
 
+def ref_config(name, world):
+    """metric + config of our arm for args.config (the reference arm reports on
+    the same ones); inputs are not built."""
+    meta = {
+        "kmeans": (METRIC, "kmeans cost+grad, n=1M points per GPU, d=16, K=64, fixed assignments "
+                           "(BASELINE configs[1]); value_and_grad via linearize+transpose",
+                   {"n_total": N_PER_GPU * world, "d": D, "k": K}),
+        "gmm": ("GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)",
+                "ADBench GMM log-likelihood + gradient w.r.t. (alphas, means, icf), n=1M points per GPU, "
+                "d=64, K=200, Wishart gamma=1 m=0 (BASELINE configs[2])",
+                {"n_total": N_PER_GPU * world, "d": 64, "k": 200}),
+        "histogram": ("histogram evals/s (2^28 int32 keys/GPU into 4096 bins)",
+                      "index-set histogram h!(p.i) += 1.0, 2^28 uniform keys per GPU, 4096 bins, bit-exact "
+                      "(BASELINE configs[3])", {"n_total": (1 << 28) * world, "bins": 4096}),
+        "matmul": ("matmul n=256 fwd+grad evals/s",
+                   "pointful matmul sum(x.y) value and gradient wrt x, n=256 (BASELINE configs[0])", {"n": 256}),
+        "mlp": ("MLP fwd+grad evals/s (batch 8192/GPU, 1024^3, square activation)",
+                "2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) (BASELINE configs[4])",
+                {"batch_total": 8192 * world}),
+    }
+    metric, workload, extra = meta[name]
+    return metric, dict({"workload": workload}, **extra)
+
+
 def run_reference(args, world, rank):
+    """The reference's own CPU implementation of the path on the host cores
+    (oracle/_ref = the unmodified reference evaluator; for GMM, which the
+    language cannot express, the fp64 port of ADBench's algorithm), on our
+    arm's metric and config, each step a bounded sample of the workload."""
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
+    metric, config = ref_config(args.config, world)
     if args.config == "gmm":
-        # no reference implementation exists (no exp/log in the language): the
-        # fp64 port of ADBench's algorithm is the CPU arm
         rates = [gmm_cpu_rate(reps=1) for _ in range(max(1, args.steps))]
         rate = statistics.mean(r for r, _ in rates)
         sec = statistics.mean(t for _, t in rates)
-        line = {
-            "impl": "reference", "metric": "GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)",
-            "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (oracle/gmm.py:gmm_inputs, seed 7)",
-            "config": {"workload": "ADBench GMM objective + gradient, d=64, K=200 (BASELINE configs[2])",
-                       "reference_sample_points": 2000},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"oracle/gmm.py fp64 port on n=2000 points, {sec:.3f} s/eval, "
-                                       f"scaled linearly to 1M points"},
-            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
-        return 0
-    rate, sec, times = reference_rate(args.ref_sample, cores, args.steps, warm=args.warmup)
-    sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2) on "
-              f"n={args.ref_sample} points (d={D}, K={K}), chunks={cores}; {sec:.3f} s/eval; "
-              f"scaled linearly to 1M points")
+        kind, dtype = "port", "f64"
+        sample = (f"oracle/gmm.py fp64 port on n=2000 points, {sec:.3f} s/eval, scaled linearly to 1M points")
+        config["reference_sample_points"] = 2000
+    elif args.config == "kmeans":
+        rate, sec, times = reference_rate(args.ref_sample, cores, args.steps, warm=args.warmup)
+        kind, dtype = "reference", "f32"
+        sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2) on "
+                  f"n={args.ref_sample} points (d={D}, K={K}), chunks={cores}; {sec:.3f} s/eval; "
+                  f"scaled linearly to 1M points")
+        config["reference_sample_points"] = args.ref_sample
+    else:
+        runs = [reference_sample_rate(args.config, cores) for _ in range(max(1, args.steps))]
+        rate = statistics.mean(r for r, _, _ in runs)
+        sec = statistics.mean(t for _, t, _ in runs)
+        kind, dtype = "reference", "f32"
+        sample = f"reference evalExpr (oracle/_ref) chunks={cores}: {runs[0][2]}; {sec:.3f} s per sample"
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded N(0,1) points, centroids sampled from points, nearest-centroid assignments)",
-        "config": {"workload": "kmeans cost+grad, d=16, K=64, fixed assignments (BASELINE configs[1])",
-                   "reference_sample_points": args.ref_sample},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "impl": "reference", "metric": metric, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate if rate > 0 else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded; same generators as our arm, bounded sample)",
+        "config": config,
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
