@@ -48,7 +48,8 @@ def ctx():
     return dx.Context(0)
 
 
-@pytest.mark.parametrize("n,k", [(1000, 3), (4999, 10), (8192, 17), (20000, 24)])
+@pytest.mark.parametrize("n,k", [(1000, 3), (4999, 10), (8192, 17), (20000, 24),
+                                 (1, 1), (65, 2), (127, 5), (300, 200)])  # ragged / tiny edge cases
 def test_gmm_objective_grad(ctx, n, k):
     import paper_2104_05372_b200 as dx
     a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=100 + k)
