@@ -95,10 +95,45 @@ __device__ __forceinline__ float dxg_h_hi(unsigned w) {
   asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; cvt.f32.f16 %0, h; }" : "=f"(f) : "r"(w));
   return f;
 }
+// Paired fp32 arithmetic (sm_100 FADD2 / FFMA2: two IEEE fp32 operations per
+// instruction, each lane rounded exactly as the scalar op)
+__device__ __forceinline__ float2 dxg_sub2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dxg_add2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dxg_mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dxg_fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
 // split two floats into packed f16x2 hi and lo words (x0 in the low half)
 __device__ __forceinline__ void dxg_split2(float x0, float x1, unsigned& hi, unsigned& lo) {
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(x1 - dxg_h_hi(hi)), "f"(x0 - dxg_h_lo(hi)));
+}
+__device__ __forceinline__ void dxg_split2v(float2 z, unsigned& hi, unsigned& lo) {  // f32x2 residual
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(z.y), "f"(z.x));
+  const float2 r = dxg_sub2(z, make_float2(dxg_h_lo(hi), dxg_h_hi(hi)));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r.y), "f"(r.x));
 }
 // exact power-of-two scale s with max_abs * s < 2^14 (fp16 max is 65504)
 __device__ __forceinline__ float dxg_scale_for(float max_abs) {
@@ -290,7 +325,7 @@ extern "C" __global__ void __launch_bounds__(320, 1)
   unsigned char* qs = smem;                                // 128 KB: hi (64 KB) then lo
   unsigned char* xsm = smem + 2 * DXG_GC * 64 * 128;       // DXG_FXS stages x 32 KB
   __shared__ __align__(8) unsigned long long xfull[DXG_FXS], xempty[DXG_FXS], tfull[2], tempty[2], qfull, qempty;
-  __shared__ float bsm[DXG_GC][DXG_D], dsm[DXG_GC][DXG_D];
+  __shared__ __align__(16) float bsm[DXG_GC][DXG_D], dsm[DXG_GC][DXG_D];
   __shared__ float csm[DXG_GC], ssm[DXG_GC];
   __shared__ unsigned tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -417,8 +452,10 @@ extern "C" __global__ void __launch_bounds__(320, 1)
             const unsigned hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-              xr[ch * 8 + 2 * w] = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]);
-              xr[ch * 8 + 2 * w + 1] = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]);
+              const float2 xv = dxg_add2(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
+                                         make_float2(dxg_h_lo(lw[w]), dxg_h_hi(lw[w])));
+              xr[ch * 8 + 2 * w] = xv.x;
+              xr[ch * 8 + 2 * w + 1] = xv.y;
             }
           }
           __syncwarp();
@@ -439,14 +476,16 @@ extern "C" __global__ void __launch_bounds__(320, 1)
             DXG_TMEM_LD16(ta + 32, v2);
             DXG_TMEM_LD16(ta + 48, v3);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float s0 = 0.f, s1 = 0.f;
+            float2 s2 = make_float2(0.f, 0.f);  // even / odd columns
             // y~_c = MMA_c - bvec_c + dvec_c * x~_c  (= sx sq Q (x - mu))
+            // (columns c, c+1 as one f32x2 pair: same per-lane rounding as the scalar form)
 #define DXG_Y(V, c0)                                                                                        \
   {                                                                                                         \
-    const float y0 = fmaf(dsm[j][c0 + c], xr[c0 + c], __uint_as_float(V[c]) - bsm[j][c0 + c]);             \
-    const float y1 = fmaf(dsm[j][c0 + c + 1], xr[c0 + c + 1], __uint_as_float(V[c + 1]) - bsm[j][c0 + c + 1]); \
-    s0 = fmaf(y0, y0, s0);                                                                                  \
-    s1 = fmaf(y1, y1, s1);                                                                                  \
+    const float2 t = dxg_sub2(make_float2(__uint_as_float(V[c]), __uint_as_float(V[c + 1])),               \
+                              *reinterpret_cast<const float2*>(&bsm[j][c0 + c]));                           \
+    const float2 y = dxg_fma2(*reinterpret_cast<const float2*>(&dsm[j][c0 + c]),                            \
+                              make_float2(xr[c0 + c], xr[c0 + c + 1]), t);                                  \
+    s2 = dxg_fma2(y, y, s2);                                                                                \
   }
 #pragma unroll
             for (int c = 0; c < 16; c += 2) {
@@ -457,7 +496,7 @@ extern "C" __global__ void __launch_bounds__(320, 1)
             }
 #undef DXG_Y
             const int k = g * DXG_GC + j;
-            if (k < K && i < n) beta[(long long)k * npad + i] = csm[j] - 0.5f * ssm[j] * (s0 + s1);
+            if (k < K && i < n) beta[(long long)k * npad + i] = csm[j] - 0.5f * ssm[j] * (s2.x + s2.y);
           }
           dxg_fence_before();
           __syncwarp();
@@ -1078,7 +1117,7 @@ extern "C" __global__ void __launch_bounds__(576, 1)
         const unsigned char* xh = bs + (xs * 2) * DXG_XB_BYTES;
         const unsigned char* xl = xh + DXG_XB_BYTES;
         unsigned th[32], tl[32];
-        float mchunk = 0.f;
+        float2 mchunk = make_float2(0.f, 0.f);  // even / odd points
 #ifdef DXG_DBG_NOPROD  // (timing experiment: no SIMT producer math)
 #pragma unroll
         for (int w = 0; w < 32; ++w) th[w] = tl[w] = 0u;
@@ -1093,16 +1132,16 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
           const unsigned hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const float x0 = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]) - mub;
-            const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
-            const float z0 = gv[2 * w] * x0, z1 = gv[2 * w + 1] * x1;
-            mchunk += z0 + z1;
-            dxg_split2(z0, z1, th[cc * 4 + w], tl[cc * 4 + w]);
+          for (int w = 0; w < 4; ++w) {  // points (2w, 2w+1) as one f32x2 pair
+            const float2 xs = dxg_add2(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
+                                       make_float2(dxg_h_lo(lw[w]), dxg_h_hi(lw[w])));
+            const float2 z = dxg_mul2(make_float2(gv[2 * w], gv[2 * w + 1]), dxg_sub2(xs, make_float2(mub, mub)));
+            mchunk = dxg_add2(mchunk, z);
+            dxg_split2v(z, th[cc * 4 + w], tl[cc * 4 + w]);
           }
         }
 #endif
-        msum += (double)mchunk;
+        msum += (double)(mchunk.x + mchunk.y);
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(256 + (2 * q + s) * 64);
           DXG_TMEM_ST16(ta, th);
@@ -1160,7 +1199,13 @@ extern "C" __global__ void __launch_bounds__(576, 1)
             DXG_TMEM_LD8(lanebase + (unsigned)(q * 128 + DXG_BN + j0), w);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+            for (int j = 0; j < 8; j += 2) {  // f32x2: acc += (hi-column + lo-column) products
+              const float2 t = dxg_add2(make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
+                                        make_float2(__uint_as_float(w[j]), __uint_as_float(w[j + 1])));
+              const float2 a2 = dxg_add2(make_float2(acc[j0 + j], acc[j0 + j + 1]), t);
+              acc[j0 + j] = a2.x;
+              acc[j0 + j + 1] = a2.y;
+            }
           }
 #endif
           dxg_fence_before();

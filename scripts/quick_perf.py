@@ -27,9 +27,9 @@ if which == "kmeans":
     e = pts.astype(np.float64) - cs.astype(np.float64)[asg]
     cost = (e*e).sum(); g = np.zeros((k, d)); np.add.at(g, asg, -2*e)
     print("cost rel", abs(out[0][0]-cost)/(1+abs(cost)), "grad rel", np.max(np.abs(out[1]-g.ravel())/(1+np.abs(g.ravel()))))
-elif which == "hist":
+elif which in ("hist", "histz"):
     n, k = 1 << 28, 4096
-    keys = P.histogram_inputs(n, k)
+    keys = P.histogram_inputs(n, k, zipf=1.1 if which == "histz" else 0.0)
     prog = dx.Program(P.histogram(n, k), ctx=ctx)
     out = prog(keys)
     ms = timeit(prog, 10)
