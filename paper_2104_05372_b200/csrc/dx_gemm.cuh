@@ -202,7 +202,13 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         DX_TMEM_LD32(lanebase + (unsigned)(b * 2 * BN + BN + q * 32), vs);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[q * 32 + j] += __uint_as_float(vb[j]) + __uint_as_float(vs[j]);
+        for (int j = 0; j < 32; j += 2) {  // f32x2 pairs, same per-lane rounding
+          const float2 t = dx_f2add(make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])),
+                                    make_float2(__uint_as_float(vs[j]), __uint_as_float(vs[j + 1])));
+          const float2 a2 = dx_f2add(make_float2(acc[q * 32 + j], acc[q * 32 + j + 1]), t);
+          acc[q * 32 + j] = a2.x;
+          acc[q * 32 + j + 1] = a2.y;
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();

@@ -95,36 +95,6 @@ __device__ __forceinline__ float dxg_h_hi(unsigned w) {
   asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; cvt.f32.f16 %0, h; }" : "=f"(f) : "r"(w));
   return f;
 }
-// Paired fp32 arithmetic (sm_100 FADD2 / FFMA2: two IEEE fp32 operations per
-// instruction, each lane rounded exactly as the scalar op)
-__device__ __forceinline__ float2 dxg_sub2(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dxg_add2(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dxg_mul2(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dxg_fma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
 // split two floats into packed f16x2 hi and lo words (x0 in the low half)
 __device__ __forceinline__ void dxg_split2(float x0, float x1, unsigned& hi, unsigned& lo) {
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
@@ -132,7 +102,7 @@ __device__ __forceinline__ void dxg_split2(float x0, float x1, unsigned& hi, uns
 }
 __device__ __forceinline__ void dxg_split2v(float2 z, unsigned& hi, unsigned& lo) {  // f32x2 residual
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(z.y), "f"(z.x));
-  const float2 r = dxg_sub2(z, make_float2(dxg_h_lo(hi), dxg_h_hi(hi)));
+  const float2 r = dx_f2sub(z, make_float2(dxg_h_lo(hi), dxg_h_hi(hi)));
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r.y), "f"(r.x));
 }
 // exact power-of-two scale s with max_abs * s < 2^14 (fp16 max is 65504)
@@ -452,7 +422,7 @@ extern "C" __global__ void __launch_bounds__(320, 1)
             const unsigned hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-              const float2 xv = dxg_add2(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
+              const float2 xv = dx_f2add(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
                                          make_float2(dxg_h_lo(lw[w]), dxg_h_hi(lw[w])));
               xr[ch * 8 + 2 * w] = xv.x;
               xr[ch * 8 + 2 * w + 1] = xv.y;
@@ -481,11 +451,11 @@ extern "C" __global__ void __launch_bounds__(320, 1)
             // (columns c, c+1 as one f32x2 pair: same per-lane rounding as the scalar form)
 #define DXG_Y(V, c0)                                                                                        \
   {                                                                                                         \
-    const float2 t = dxg_sub2(make_float2(__uint_as_float(V[c]), __uint_as_float(V[c + 1])),               \
+    const float2 t = dx_f2sub(make_float2(__uint_as_float(V[c]), __uint_as_float(V[c + 1])),               \
                               *reinterpret_cast<const float2*>(&bsm[j][c0 + c]));                           \
-    const float2 y = dxg_fma2(*reinterpret_cast<const float2*>(&dsm[j][c0 + c]),                            \
+    const float2 y = dx_f2fma(*reinterpret_cast<const float2*>(&dsm[j][c0 + c]),                            \
                               make_float2(xr[c0 + c], xr[c0 + c + 1]), t);                                  \
-    s2 = dxg_fma2(y, y, s2);                                                                                \
+    s2 = dx_f2fma(y, y, s2);                                                                                \
   }
 #pragma unroll
             for (int c = 0; c < 16; c += 2) {
@@ -1133,10 +1103,10 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           const unsigned hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) {  // points (2w, 2w+1) as one f32x2 pair
-            const float2 xs = dxg_add2(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
+            const float2 xs = dx_f2add(make_float2(dxg_h_lo(hw[w]), dxg_h_hi(hw[w])),
                                        make_float2(dxg_h_lo(lw[w]), dxg_h_hi(lw[w])));
-            const float2 z = dxg_mul2(make_float2(gv[2 * w], gv[2 * w + 1]), dxg_sub2(xs, make_float2(mub, mub)));
-            mchunk = dxg_add2(mchunk, z);
+            const float2 z = dx_f2mul(make_float2(gv[2 * w], gv[2 * w + 1]), dx_f2sub(xs, make_float2(mub, mub)));
+            mchunk = dx_f2add(mchunk, z);
             dxg_split2v(z, th[cc * 4 + w], tl[cc * 4 + w]);
           }
         }
@@ -1200,9 +1170,9 @@ extern "C" __global__ void __launch_bounds__(576, 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {  // f32x2: acc += (hi-column + lo-column) products
-              const float2 t = dxg_add2(make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
+              const float2 t = dx_f2add(make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
                                         make_float2(__uint_as_float(w[j]), __uint_as_float(w[j + 1])));
-              const float2 a2 = dxg_add2(make_float2(acc[j0 + j], acc[j0 + j + 1]), t);
+              const float2 a2 = dx_f2add(make_float2(acc[j0 + j], acc[j0 + j + 1]), t);
               acc[j0 + j] = a2.x;
               acc[j0 + j + 1] = a2.y;
             }
