@@ -90,16 +90,23 @@ __device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
 // promotion of chunk c overlaps the MMAs of chunk c+1.
 #define DX_GEMM_CHUNK 1
 
-// Warps 0-3: epilogue (warp w owns TMEM lanes / tile rows 32w..32w+31);
-// warp 4: TMA producer; warp 5: MMA issuer.  mode 0: C = acc, 1: C += acc.
-template <int BN, int STAGES, class CT>
+// Warps 0..EW-1: epilogue (warp w owns TMEM lanes / tile rows 32(w%4)..+31 and
+// accumulator columns [128(w/4), +128)); warp EW: TMA producer; warp EW+1:
+// MMA issuer.  mode 0: C = acc, 1: C += acc.  MERGED: the three products
+// share one accumulator (BN = 256 fits TMEM double-buffered; the promotion
+// every 32 k keeps the truncation error at fp32 level).
+template <int BN, int STAGES, class CT, bool MERGED = false>
 __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap* tal, const dx_tmap* tb,
                                                const dx_tmap* tbl, long long M, long long N, long long K, CT* C,
                                                long long ldc, long long mode, long long ksplit,
                                                unsigned* tickets) {
   constexpr unsigned A_BYTES = DX_GEMM_BM * 128, B_BYTES = BN * 128;
   constexpr unsigned STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr unsigned TMEM_COLS = 4 * BN;
+  constexpr int NACC = MERGED ? 1 : 2;                   // accumulators per buffer
+  constexpr unsigned TMEM_COLS = 2 * NACC * BN;
+  constexpr int CW = BN < 128 ? BN : 128;                // accumulator columns per epilogue warp
+  constexpr int EW = 4 * (BN / CW);                      // epilogue warps
+  constexpr int TMA_W = EW, MMA_W = EW + 1;
   static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
   extern __shared__ __align__(1024) unsigned char dx_gemm_smem_raw[];
   unsigned char* smem = dx_gemm_smem_raw + ((1024u - (dx_smem_addr(dx_gemm_smem_raw) & 1023u)) & 1023u);
@@ -125,11 +132,11 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
     }
     for (int b = 0; b < 2; ++b) {
       dx_mbar_init(&tfull[b], 1);
-      dx_mbar_init(&tempty[b], 4);
+      dx_mbar_init(&tempty[b], EW);
     }
     dx_fence_mbar_init();
   }
-  if (warp == 4) {
+  if (warp == TMA_W) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
                  "r"(TMEM_COLS)
                  : "memory");
@@ -140,7 +147,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem = tmem_base;
 
-  if (warp == 4) {
+  if (warp == TMA_W) {
     if (lane == 0) {
       for (int kb = 0; kb < KB; ++kb) {
         const int s = kb % STAGES;
@@ -154,14 +161,14 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         dx_tma_2d(st + 2 * A_BYTES + B_BYTES, tbl, kc, n0, &full[s]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_W) {
     if (lane == 0) {
       const unsigned idesc = dx_idesc_tf32<BN>();
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
         if (c >= 2) dx_mbar_wait_bounded(&tempty[b], (unsigned)(((c >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const unsigned tbig = tmem + (unsigned)(b * 2 * BN), tsmall = tbig + BN;
+        const unsigned tbig = tmem + (unsigned)(b * NACC * BN), tsmall = MERGED ? tbig : tbig + BN;
         const int k1 = min(KB, (c + 1) * DX_GEMM_CHUNK);
         for (int kb = c * DX_GEMM_CHUNK; kb < k1; ++kb) {
           const int s = kb % STAGES;
@@ -177,7 +184,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
             const unsigned long long bl = dx_umma_desc_sw128(st + 2 * A_BYTES + B_BYTES + kk * 32);
             const unsigned accum = !(first && kk == 0);
             dx_umma_tf32(tbig, ah, bh, idesc, accum);
-            dx_umma_tf32(tsmall, ah, bl, idesc, accum);
+            dx_umma_tf32(tsmall, ah, bl, idesc, MERGED ? 1u : accum);
             dx_umma_tf32(tsmall, al, bh, idesc, 1u);
           }
           dx_umma_commit(&empty[s]);  // frees the stage once these MMAs retire
@@ -187,24 +194,45 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
     }
   } else {
     // epilogue warps: promote each chunk into fp32 registers (RN adds)
-    float acc[BN];
+    const int wq = warp & 3, cb = (warp >> 2) * CW;  // lane quarter, first column
+    float acc[CW];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    const unsigned lanebase = tmem + ((unsigned)(warp * 32) << 16);
+    for (int j = 0; j < CW; ++j) acc[j] = 0.f;
+    const unsigned lanebase = tmem + ((unsigned)(wq * 32) << 16) + (unsigned)cb;
     for (int c = 0; c < NC; ++c) {
       const int b = c & 1;
       dx_mbar_wait_bounded(&tfull[b], (unsigned)((c >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (MERGED) {  // x16 loads: acc[128] + 16 in flight fit the 168 registers of 10 warps
 #pragma unroll
-      for (int q = 0; q < BN / 32; ++q) {
+        for (int q = 0; q < CW / 16; ++q) {
+          unsigned v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(lanebase + (unsigned)(b * NACC * BN + q * 16)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const float2 a2 = dx_f2add(make_float2(acc[q * 16 + j], acc[q * 16 + j + 1]),
+                                       make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
+            acc[q * 16 + j] = a2.x;
+            acc[q * 16 + j + 1] = a2.y;
+          }
+        }
+      } else
+#pragma unroll
+      for (int q = 0; q < CW / 32; ++q) {
         unsigned vb[32], vs[32];
-        DX_TMEM_LD32(lanebase + (unsigned)(b * 2 * BN + q * 32), vb);
-        DX_TMEM_LD32(lanebase + (unsigned)(b * 2 * BN + BN + q * 32), vs);
+        DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + q * 32), vb);
+        if (!MERGED) DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + BN + q * 32), vs);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {  // f32x2 pairs, same per-lane rounding
-          const float2 t = dx_f2add(make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])),
-                                    make_float2(__uint_as_float(vs[j]), __uint_as_float(vs[j + 1])));
+          const float2 hb = make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1]));
+          const float2 t =
+              MERGED ? hb : dx_f2add(hb, make_float2(__uint_as_float(vs[j]), __uint_as_float(vs[j + 1])));
           const float2 a2 = dx_f2add(make_float2(acc[q * 32 + j], acc[q * 32 + j + 1]), t);
           acc[q * 32 + j] = a2.x;
           acc[q * 32 + j + 1] = a2.y;
@@ -223,52 +251,67 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
           __nanosleep(64);
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(EW * 32) : "memory");
       if (part > 0) mode = 1;
     }
-    const long long row = m0 + warp * 32 + lane;
+    const long long row = m0 + wq * 32 + lane;
     if (row < M) {
-      CT* out = C + row * ldc + n0;
-      const bool vec = sizeof(CT) == 4 && n0 + BN <= N && ((ldc | n0) & 3) == 0 &&
-                       ((reinterpret_cast<unsigned long long>(C) & 15) == 0);
-      const bool vecd = sizeof(CT) == 8 && n0 + BN <= N && ((ldc | n0) & 1) == 0 &&
-                        ((reinterpret_cast<unsigned long long>(C) & 15) == 0);
+      const int nc = n0 + cb;  // this warp's first output column
+      CT* out = C + row * ldc + nc;
+      // MERGED (N = 256) kernels are only planned for full, 16-byte aligned
+      // column tiles (contract.inc), so they carry no scalar fallback (whose
+      // unrolled code would push acc[] out of the 168 registers of 10 warps)
+      const bool vec = sizeof(CT) == 4 && (MERGED || (nc + CW <= N && ((ldc | nc) & 3) == 0 &&
+                                                      ((reinterpret_cast<unsigned long long>(C) & 15) == 0)));
+      const bool vecd = sizeof(CT) == 8 && (MERGED || (nc + CW <= N && ((ldc | nc) & 1) == 0 &&
+                                                       ((reinterpret_cast<unsigned long long>(C) & 15) == 0)));
       if (vec && mode == 0) {
 #pragma unroll
-        for (int j = 0; j < BN; j += 4)
+        for (int j = 0; j < CW; j += 4)
           *reinterpret_cast<float4*>(out + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
       } else if (vecd) {
         // f64 cells: 16-byte read-modify-writes, 16 loads in flight per batch
         // (the row-per-thread RMW is latency-bound when few tiles exist)
         double2* o2 = reinterpret_cast<double2*>(out);
+        constexpr int QB = 16;  // 16-byte loads per batch
 #pragma unroll
-        for (int j0 = 0; j0 < BN; j0 += 32) {
-          double2 cur[16];
+        for (int j0 = 0; j0 < CW; j0 += 2 * QB) {
+          double2 cur[QB];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) cur[q] = mode == 0 ? make_double2(0.0, 0.0) : o2[j0 / 2 + q];
+          for (int q = 0; q < QB; ++q) cur[q] = mode == 0 ? make_double2(0.0, 0.0) : o2[j0 / 2 + q];
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
+          for (int q = 0; q < QB; ++q)
             o2[j0 / 2 + q] = make_double2(cur[q].x + (double)acc[j0 + 2 * q], cur[q].y + (double)acc[j0 + 2 * q + 1]);
         }
-      } else {
+      } else if (!MERGED) {
 #pragma unroll
-        for (int j = 0; j < BN; ++j) {
-          if (n0 + j < N) {
+        for (int j = 0; j < CW; ++j) {
+          if (nc + j < N) {
             if (mode == 0) out[j] = (CT)acc[j];
             else out[j] += (CT)acc[j];
           }
+        }
+      } else {  // f32 cells with += (no 16-byte RMW path for them)
+#pragma unroll
+        for (int j = 0; j < CW; j += 4) {
+          float4 o = *reinterpret_cast<float4*>(out + j);
+          o.x += acc[j];
+          o.y += acc[j + 1];
+          o.z += acc[j + 2];
+          o.w += acc[j + 3];
+          *reinterpret_cast<float4*>(out + j) = o;
         }
       }
     }
     if (S > 1) {  // release the next part
       __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(EW * 32) : "memory");
       if (threadIdx.x == 0) atomicAdd(tickets + tile, 1u);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) {
+  if (warp == TMA_W) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
@@ -288,4 +331,14 @@ extern "C" __global__ void __launch_bounds__(192, 1)
                           long long N, long long K, double* C, long long ldc, long long mode, long long ksplit,
                           unsigned* tickets) {
   dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
+}
+// N = 256 tiles (merged accumulator, 2 stages of 96 KB, 8 epilogue warps):
+// half the MMA instructions per flop of the N = 128 kernel.  fp32 outputs
+// only: with f64 cells the epilogue's accumulators spill at 168 registers.
+extern "C" __global__ void __launch_bounds__(320, 1)
+    dx_gemm_tf32x3_n256(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
+                        const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
+                        long long N, long long K, float* C, long long ldc, long long mode, long long ksplit,
+                        unsigned* tickets) {
+  dx_gemm_tf32x3<256, 2, float, true>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
 }

@@ -24,6 +24,8 @@ SHAPES = [
     (384, 128, 4096, True, True),    # long K: many pipeline wraps; split-K 4
     (256, 256, 8192, True, False),   # split-K 8 (4 tiles would leave 144 SMs idle)
     (1, 1, 8, True, False),          # single element
+    (12800, 256, 96, True, False),   # N = 256 tiles (100 of them), K not a multiple of 32
+    (12800, 512, 40, False, True),   # N = 256 tiles, transposed operands
 ]
 
 
