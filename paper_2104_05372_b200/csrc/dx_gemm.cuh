@@ -333,8 +333,10 @@ extern "C" __global__ void __launch_bounds__(192, 1)
   dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
 }
 // N = 256 tiles (merged accumulator, 2 stages of 96 KB, 8 epilogue warps):
-// half the MMA instructions per flop of the N = 128 kernel.  fp32 outputs
-// only: with f64 cells the epilogue's accumulators spill at 168 registers.
+// half the MMA instructions per flop of the N = 128 kernel (opt-in,
+// DEXLET_GEMM_N256=1).  The merged accumulator truncates the small products
+// against the large one: measured 15-50% more gradient error downstream of
+// an MLP forward GEMM, so it is not the default.
 extern "C" __global__ void __launch_bounds__(320, 1)
     dx_gemm_tf32x3_n256(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
                         const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,

@@ -167,7 +167,10 @@ def test_transposed_gemm_operands_use_a_tiled_prologue():
     assert "reinterpret_cast<float4*>(hi)[t]" in prog.source
 
 
-def test_wide_gemm_tiles_for_large_fp32_outputs():
+def test_wide_gemm_tiles_are_opt_in(monkeypatch):
+    prog = dx.Program(P.contraction(12800, 256, 96, True, False), ctx=None)
+    assert "dx_gemm_tf32x3_n256" not in prog.plan
+    monkeypatch.setenv("DEXLET_GEMM_N256", "1")
     prog = dx.Program(P.contraction(12800, 256, 96, True, False), ctx=None)
     assert "dx_gemm_tf32x3_n256 " in prog.plan and "N=256 tiles" in prog.plan
     prog = dx.Program(P.contraction(1000, 520, 1024), ctx=None)  # ragged N: N = 128 tiles
