@@ -73,10 +73,20 @@
 #ifndef DXG_NACC
 #define DXG_NACC 1               // TMEM accumulators per D buffer (1: merged, 3: hh / hl / lh)
 #endif
+#ifndef DXG_PN128  // pair kernel: one N=128 MMA over [X^T hi ; X^T lo] per A split
+#define DXG_PN128 (DXG_TMEM_A && DXG_NACC == 1)
+#endif
+#if DXG_PN128
+#define DXG_TD(b) ((b) * 128)  // D buffer b: 128 columns (products with x hi | x lo)
+#define DXG_TACC(i) 0
+#define DXG_NZS 4
+#define DXG_TA(s) (256 + 64 * (s))
+#else
 #define DXG_TD(b) ((b) * 64 * DXG_NACC)
 #define DXG_TACC(i) ((DXG_NACC == 3 ? (i) : 0) * 64)
 #define DXG_NZS ((512 - 128 * DXG_NACC) / 64)  // A stages filling the rest of TMEM
 #define DXG_TA(s) (128 * DXG_NACC + 64 * (s))
+#endif
 
 // ---- shared helpers ----------------------------------------------------------
 // byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
@@ -615,7 +625,7 @@ extern "C" __global__ void __launch_bounds__(448, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const unsigned idesc = dxg_idesc_f16<DXG_BN>();
+      const unsigned idesc = dxg_idesc_f16<DXG_PN128 ? 2 * DXG_BN : DXG_BN>();
       const unsigned baddr = dx_smem_addr(bs), zaddr = dx_smem_addr(zs);
       int it = 0, pc = 0;
       long long prevPair = -1;
@@ -649,9 +659,15 @@ extern "C" __global__ void __launch_bounds__(448, 1)
             const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
             const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
 #ifndef DXG_DBG_NOMMA  // (timing experiment: the pipeline without tensor-core work)
+#if DXG_PN128
+            (void)dbl;
+            dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
+            dxg_umma_f16_ta(td, tal + kk * 8, dbh, idesc, 1u);
+#else
             dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
             dxg_umma_f16_ta(td + DXG_TACC(1), tah + kk * 8, dbl, idesc, DXG_NACC == 3 ? acc : 1u);
             dxg_umma_f16_ta(td + DXG_TACC(2), tal + kk * 8, dbh, idesc, DXG_NACC == 3 ? acc : 1u);
+#endif
 #else
             (void)acc; (void)dbh; (void)dbl;
 #endif
@@ -849,6 +865,19 @@ extern "C" __global__ void __launch_bounds__(448, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + (__uint_as_float(w[j]) + __uint_as_float(x[j]));
+#elif DXG_PN128
+        unsigned v[16], w[16];
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
+        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + DXG_BN + j0), w);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const float2 t = dx_f2add(make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
+                                    make_float2(__uint_as_float(w[j]), __uint_as_float(w[j + 1])));
+          const float2 a2 = dx_f2add(make_float2(acc[j0 + j], acc[j0 + j + 1]), t);
+          acc[j0 + j] = a2.x;
+          acc[j0 + j + 1] = a2.y;
+        }
 #else
         unsigned v[16];
         DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
