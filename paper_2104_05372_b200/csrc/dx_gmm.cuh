@@ -1274,11 +1274,23 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_moments(const double* d
   }
   __syncthreads();
   double* out = mom + (long long)k * DXG_MOM;
-  for (int e = threadIdx.x; e < DXG_D * DXG_D; e += blockDim.x) {
-    const int b = e / DXG_D, a = e % DXG_D;
-    double s = 0.0;
-    for (int sl = 0; sl < nsl; ++sl) s += dpart[((long long)slots[sl] * (G * 64) + kl * 64 + b) * DXG_BN + a];
-    out[b * DXG_D + a] = s * isx * isx;
+  // four entries per thread: four independent slot chains in flight (each
+  // entry still sums its slots in slot order)
+  for (int e0 = threadIdx.x; e0 < DXG_D * DXG_D; e0 += 4 * blockDim.x) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int sl = 0; sl < nsl; ++sl) {
+      const double* src = dpart + ((long long)slots[sl] * (G * 64) + kl * 64) * DXG_BN;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < DXG_D * DXG_D) s[u] += src[(e / DXG_D) * DXG_BN + e % DXG_D];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < DXG_D * DXG_D) out[e] = s[u] * isx * isx;
+    }
   }
   if (threadIdx.x <= DXG_D) {
     double s = 0.0;  // threadIdx 0: W; 1 + b: m~_b
