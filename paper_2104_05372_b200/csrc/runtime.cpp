@@ -162,10 +162,15 @@ int compileCubin(const std::string& source, std::string& cubin) {
 // NCCL via dlopen.  Only the handful of entry points the allreduce needs.
 
 typedef int ncclResult_t_;
+// ncclUniqueId is a 128-byte struct passed BY VALUE to ncclCommInitRank (a
+// `char[128]` parameter would decay to a pointer and break the call ABI)
+struct NcclUniqueId_ {
+  char internal[128];
+};
 struct NcclApi {
   void* lib = nullptr;
-  ncclResult_t_ (*getUniqueId)(void*) = nullptr;
-  ncclResult_t_ (*commInitRank)(void**, int, char[128], int) = nullptr;
+  ncclResult_t_ (*getUniqueId)(NcclUniqueId_*) = nullptr;
+  ncclResult_t_ (*commInitRank)(void**, int, NcclUniqueId_, int) = nullptr;
   ncclResult_t_ (*allReduce)(const void*, void*, size_t, int, int, void*, CUstream) = nullptr;
   ncclResult_t_ (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(ncclResult_t_) = nullptr;
@@ -455,15 +460,15 @@ int dxc_event_destroy(void* ev) { return check(cuEventDestroy((CUevent)ev), "cuE
 int dxc_nccl_unique_id(void* out128) {
   int rc = loadNccl();
   if (rc) return rc;
-  return ncclCheck(g_nccl.getUniqueId(out128), "ncclGetUniqueId");
+  return ncclCheck(g_nccl.getUniqueId(static_cast<NcclUniqueId_*>(out128)), "ncclGetUniqueId");
 }
 
 int dxc_comm_init(dxc_ctx* ctx, const void* uid, int nranks, int rank) {
   int rc = loadNccl();
   if (rc) return rc;
   ctx->makeCurrent();
-  char id[128];
-  std::memcpy(id, uid, 128);
+  NcclUniqueId_ id;
+  std::memcpy(id.internal, uid, 128);
   void* comm = nullptr;
   rc = ncclCheck(g_nccl.commInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
   if (rc) return rc;

@@ -1,0 +1,67 @@
+"""GPU: the multi-rank plumbing on one device -- NCCL (dlopen'ed, the copy
+torch maps) communicator of one rank through dxc_comm_init, and an in-place
+dxc_allreduce_sum of a device buffer (identity at world size 1).  The
+world-size-2 merge logic itself is covered on CPU with gloo
+(tests/test_distributed.py)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_single_rank_nccl_allreduce_is_identity():
+    import paper_2104_05372_b200 as dx
+    lib = dx._lib
+    ctx = dx.Context(0)
+    ctx.init_comm(dx.nccl_unique_id(), 1, 0)
+    vals = np.arange(1000, dtype=np.float64) * 0.5 - 7.0
+    buf = ctypes.c_void_p()
+    lib.dxc_buf_alloc.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    lib.dxc_buf_upload.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t]
+    lib.dxc_buf_download.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t]
+    lib.dxc_buf_ptr.argtypes = [ctypes.c_void_p]
+    lib.dxc_buf_ptr.restype = ctypes.c_void_p
+    lib.dxc_buf_free.argtypes = [ctypes.c_void_p]
+    assert lib.dxc_buf_alloc(ctx.handle, vals.nbytes, ctypes.byref(buf)) == 0
+    try:
+        assert lib.dxc_buf_upload(buf, 0, vals.ctypes.data, vals.nbytes) == 0
+        assert lib.dxc_allreduce_sum(ctx.handle, lib.dxc_buf_ptr(buf), vals.size, dx.DXC_F64) == 0
+        ctx.sync()
+        out = np.empty_like(vals)
+        assert lib.dxc_buf_download(buf, 0, out.ctypes.data, out.nbytes) == 0
+        assert np.array_equal(out, vals)
+    finally:
+        lib.dxc_buf_free(buf)
+
+
+@pytest.mark.parametrize("which", ["kmeans", "histogram"])
+def test_world2_shards_through_nccl_sum_to_the_whole(which):
+    """Both ranks of a world-size-2 sharded plan run on this device, each with
+    its Accum cells all-reduced over a one-rank NCCL communicator (the
+    plan's Allreduce steps execute for real, as identities); the two shard
+    results summed on the host equal the unsharded result."""
+    import oracle
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    ctx = dx.Context(0)
+    ctx.init_comm(dx.nccl_unique_id(), 1, 0)
+    if which == "kmeans":
+        n, d, k = 50_000, 16, 64
+        src, args = P.kmeans_cost_grad(n, d, k), P.kmeans_inputs(n, d, k)
+    else:
+        n, k = 1 << 20, 4096
+        src, args = P.histogram(n, k), (P.histogram_inputs(n, k, seed=5),)
+    whole = dx.Program(src, ctx=ctx)(*args)
+    parts = []
+    for rank in (0, 1):
+        prog = dx.Program(src, ctx=ctx, rank=rank, world=2)
+        assert "allreduce" in prog.plan
+        parts.append(prog(*args))
+    for w, p0, p1 in zip(whole, parts[0], parts[1]):
+        got = np.asarray(p0, dtype=np.float64) + np.asarray(p1, dtype=np.float64)
+        if which == "histogram":
+            assert np.array_equal(got, np.asarray(w, dtype=np.float64))  # integer counts: exact
+        else:
+            assert oracle.rel_diff(got, np.asarray(w, dtype=np.float64)) <= 1e-5
