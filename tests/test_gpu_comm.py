@@ -65,3 +65,19 @@ def test_world2_shards_through_nccl_sum_to_the_whole(which):
             assert np.array_equal(got, np.asarray(w, dtype=np.float64))  # integer counts: exact
         else:
             assert oracle.rel_diff(got, np.asarray(w, dtype=np.float64)) <= 1e-5
+
+
+def test_gmm_moments_allreduce_path():
+    """The GMM plan all-reduces its lse sum and fp64 moments when a
+    communicator is set: at one rank the results equal the local ones."""
+    import paper_2104_05372_b200 as dx
+    from oracle import gmm as G
+    n, k = 5000, 7
+    a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=9)
+    plain = dx.GMM(dx.Context(0), 64, k, n)(a, mu, icf, x)
+    ctx = dx.Context(0)
+    ctx.init_comm(dx.nccl_unique_id(), 1, 0)
+    comm = dx.GMM(ctx, 64, k, n, n)(a, mu, icf, x)
+    assert plain[0] == comm[0]
+    for u, v in zip(plain[1:], comm[1:]):
+        assert np.array_equal(u, v)
