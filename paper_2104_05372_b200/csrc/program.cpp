@@ -384,6 +384,10 @@ int Program::issue() {
         break;
       }
       case Step::Allreduce: {
+        if (!ctx->comm) {  // a sharded plan without its communicator would return shard-local cells
+          setError("sharded plan (world > 1): call dxc_comm_init on the context first");
+          return DXC_E_ARG;
+        }
         size_t es = storageBytes(plan.bufs[s.buf].kind, f64);
         SK k = plan.bufs[s.buf].kind;
         int dt = k == SK::D ? DXC_F64 : k == SK::F ? (f64 ? DXC_F64 : DXC_F32) : k == SK::I ? DXC_I64 : DXC_I32;

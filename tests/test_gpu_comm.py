@@ -81,3 +81,13 @@ def test_gmm_moments_allreduce_path():
     assert plain[0] == comm[0]
     for u, v in zip(plain[1:], comm[1:]):
         assert np.array_equal(u, v)
+
+
+def test_sharded_plan_without_communicator_fails_loudly():
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    ctx = dx.Context(0)
+    n, k = 4096, 64
+    prog = dx.Program(P.histogram(n, k), ctx=ctx, rank=0, world=2)
+    with pytest.raises(dx.DexError):
+        prog(P.histogram_inputs(n, k, seed=1))
