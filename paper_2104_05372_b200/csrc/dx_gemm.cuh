@@ -221,21 +221,21 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
             acc[q * 16 + j + 1] = a2.y;
           }
         }
-      } else
+      } else {  // big (hi*hi) + small (hi*lo + lo*hi) accumulators
 #pragma unroll
-      for (int q = 0; q < CW / 32; ++q) {
-        unsigned vb[32], vs[32];
-        DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + q * 32), vb);
-        if (!MERGED) DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + BN + q * 32), vs);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int q = 0; q < CW / 32; ++q) {
+          unsigned vb[32], vs[32];
+          DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + q * 32), vb);
+          DX_TMEM_LD32(lanebase + (unsigned)(b * NACC * BN + BN + q * 32), vs);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {  // f32x2 pairs, same per-lane rounding
-          const float2 hb = make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1]));
-          const float2 t =
-              MERGED ? hb : dx_f2add(hb, make_float2(__uint_as_float(vs[j]), __uint_as_float(vs[j + 1])));
-          const float2 a2 = dx_f2add(make_float2(acc[q * 32 + j], acc[q * 32 + j + 1]), t);
-          acc[q * 32 + j] = a2.x;
-          acc[q * 32 + j + 1] = a2.y;
+          for (int j = 0; j < 32; j += 2) {  // f32x2 pairs, same per-lane rounding
+            const float2 t = dx_f2add(make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])),
+                                      make_float2(__uint_as_float(vs[j]), __uint_as_float(vs[j + 1])));
+            const float2 a2 = dx_f2add(make_float2(acc[q * 32 + j], acc[q * 32 + j + 1]), t);
+            acc[q * 32 + j] = a2.x;
+            acc[q * 32 + j + 1] = a2.y;
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
