@@ -2266,7 +2266,9 @@ class Lowering {
     std::vector<Slot> slots;
     if (!el.empty()) slots = localArrays(g, tt);
     if (g.out) {
-      g.line(std::string(n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
+      // lane loops: 8 iterations unrolled so their independent loads are in
+      // flight together (each lane still adds in ascending q order)
+      g.line(std::string(lane ? "#pragma unroll 8" : n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
       if (lane) g.line("for (int " + q + " = dx_lane; " + q + " < " + lit(n) + "; " + q + " += 32) {");
       else g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
       g.out->append(bodyCode);
