@@ -97,7 +97,7 @@ def _config_spec(name, world):
                     workload="2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) "
                              "(BASELINE configs[4])", extra={"batch_total": b}, out_bytes=4 + 2 * 1024 * 1024 * 4)
     if name == "gmm":
-        from oracle.gmm import gmm_inputs  # seeded input generator only (no oracle compute)
+        gmm_inputs = P.gmm_inputs
         n, d, k = N_PER_GPU, 64, 200
         a, mu, icf, x = gmm_inputs(n, d, k)
         fwd = 2 * n * k * d * d
@@ -594,7 +594,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if not spec.get("gmm") else "f32 (fp16x3 tensor-core products, fp64 folds)",
-            "data": "synthetic (seeded; see paper_2104_05372_b200/programs.py, oracle/gmm.py:gmm_inputs)",
+            "data": "synthetic (seeded; see paper_2104_05372_b200/programs.py, programs.py:gmm_inputs)",
             "config": dict({"workload": spec["workload"],
                             "parallelism": (f"points sharded x{world} + NCCL allreduce of the fp64 moments"
                                             if spec.get("gmm") else

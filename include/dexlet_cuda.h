@@ -123,7 +123,11 @@ typedef struct dxl_options {
 enum {
   DXL_F_NO_FUSION = 1,     /* materialize every pure loop (debug)           */
   DXL_F_NO_ROWSCATTER = 2, /* use smem atomics instead of warp row flushes  */
-  DXL_F_DUMP = 4           /* write generated CUDA to $DEXLET_DUMP_DIR      */
+  DXL_F_DUMP = 4,          /* write generated CUDA to $DEXLET_DUMP_DIR      */
+  DXL_F_TEST_COMM_MISMATCH = 8, /* TEST ONLY: run a (world, rank) plan over a
+                                 * communicator of another size (one device
+                                 * emulating the ranks); never in production */
+  DXL_F_NO_GEMM = 16       /* contractions through the generic SIMT lowering */
 };
 
 /* Parse, typecheck, simplify, optimize and lower `entry` of `source`, where
@@ -146,16 +150,26 @@ int dxl_program_output_leaf(dxl_program* p, int leaf, int* kind, int64_t* count)
 /* Input leaves: copied from host memory (dtype DXC_*), or bound zero-copy to
  * device memory already holding the leaf in the program's storage type
  * (f32 or f64 for Float per options.float64, i32 for Index, i64 for Int).
- * Index leaves are bounds-checked on upload (E-bounds, the check that
- * fromOrdinal performs in the reference, index_set.cpp:99-106). */
+ * `host` must hold the leaf's element count (dxl_program_input_leaf);
+ * dxl_program_set_input_n takes that count and returns E-size on mismatch.
+ * Index leaves uploaded from host memory are range-checked on the device
+ * right after the upload (the check fromOrdinal performs in the reference,
+ * index_set.cpp:99-106); device-bound index leaves are checked (and clamped)
+ * by the kernels that read them.  Either violation is reported as E-bounds
+ * by dxl_program_get_output and by dxl_program_check. */
 int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host,
                           int dtype);
+int dxl_program_set_input_n(dxl_program* p, int input, int leaf, const void* host,
+                            int dtype, int64_t count);
 int dxl_program_bind_input_device(dxl_program* p, int input, int leaf,
                                   void* devptr);
 int dxl_program_input_device_ptr(dxl_program* p, int input, int leaf, void** out);
 
 /* Executes the lowered plan asynchronously on the context stream. */
 int dxl_program_run(dxl_program* p);
+/* Synchronizes the stream and returns E-bounds if any index check (upload
+ * or in-kernel) failed since the leaves were set; DXC_OK otherwise. */
+int dxl_program_check(dxl_program* p);
 /* Copies an output leaf to host memory (synchronizes the stream). */
 int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype);
 int dxl_program_output_device_ptr(dxl_program* p, int leaf, void** out);

@@ -176,12 +176,6 @@ def gmm_objective_grad(alphas, means, icf, x, gamma: float = 1.0, m: int = 0, bl
     return err, d_alphas, d_means, d_icf
 
 
-def gmm_inputs(n: int, d: int, K: int, seed: int = 20211):
-    """Synthetic inputs of SURVEY.md §8(d) config 3 (ADBench form): x, means ~
-    N(0,1), icf ~ U(-0.1, 0.1), alphas ~ N(0,1), fp32."""
-    rng = np.random.default_rng(seed)
-    alphas = rng.standard_normal(K).astype(np.float32)
-    means = rng.standard_normal((K, d)).astype(np.float32)
-    icf = rng.uniform(-0.1, 0.1, (K, icf_size(d))).astype(np.float32)
-    x = rng.standard_normal((n, d)).astype(np.float32)
-    return alphas, means, icf, x
+# Seeded input generator shared with the product bench (pure numpy, no
+# library load): lives with the other workload generators.
+from paper_2104_05372_b200.programs import gmm_inputs  # noqa: E402,F401

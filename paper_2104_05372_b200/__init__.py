@@ -21,12 +21,36 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdexlet_cuda.so")
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(
-        f"{LIB_PATH} is missing: build it with `make -C paper_2104_05372_b200/csrc` "
-        "(or __graft_entry__.build()); the backend has no CPU fallback")
 
-_lib = ctypes.CDLL(LIB_PATH)
+
+class _LazyLib:
+    """libdexlet_cuda.so, mapped on first use: importing the package (e.g. for
+    the input generators in ``programs``) does not load the CUDA library.  A
+    missing library raises on that first use -- there is no CPU fallback."""
+
+    def __init__(self):
+        self._cdll = None
+
+    def load(self) -> ctypes.CDLL:
+        if self._cdll is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `make -C paper_2104_05372_b200/csrc` "
+                    "(or __graft_entry__.build()); the backend has no CPU fallback")
+            cdll = ctypes.CDLL(LIB_PATH)
+            for name, res, args in _SIGS:
+                f = getattr(cdll, name)
+                f.restype = res
+                f.argtypes = list(args)
+            self._cdll = cdll
+        return self._cdll
+
+    def __getattr__(self, name):
+        return getattr(self.load(), name)
+
+
+_lib = _LazyLib()
+_SIGS = []
 
 # status codes (include/dexlet_cuda.h)
 DXC_OK = 0
@@ -46,6 +70,8 @@ DXC_F32, DXC_F64, DXC_I32, DXC_I64, DXC_U32 = 0, 1, 2, 3, 4
 F_NO_FUSION = 1
 F_NO_ROWSCATTER = 2
 F_DUMP = 4
+F_TEST_COMM_MISMATCH = 8  # test only: one device emulating the ranks of a sharded plan
+F_NO_GEMM = 16  # contractions through the generic SIMT lowering
 
 _ERRNAMES = {
     DXC_E_PARSE: "E-parse", DXC_E_TYPE: "E-type", DXC_E_SIZE: "E-size",
@@ -69,10 +95,7 @@ class DxlOptions(ctypes.Structure):
 
 
 def _sig(name, res, *args):
-    f = getattr(_lib, name)
-    f.restype = res
-    f.argtypes = list(args)
-    return f
+    _SIGS.append((name, res, args))
 
 
 _vp = ctypes.c_void_p
@@ -105,6 +128,8 @@ _sig("dxl_program_input_leaf", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _i
 _sig("dxl_program_output_num_leaves", ctypes.c_int, _vp, _ip)
 _sig("dxl_program_output_leaf", ctypes.c_int, _vp, ctypes.c_int, _ip, _i64p)
 _sig("dxl_program_set_input", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int)
+_sig("dxl_program_set_input_n", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int64)
+_sig("dxl_program_check", ctypes.c_int, _vp)
 _sig("dxl_program_bind_input_device", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp)
 _sig("dxl_program_input_device_ptr", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp))
 _sig("dxl_program_run", ctypes.c_int, _vp)
@@ -148,7 +173,7 @@ ABI_SYMBOLS = [
     "dxl_program_run", "dxl_program_get_output", "dxl_program_output_device_ptr",
     "dxl_program_source", "dxl_program_plan", "dxl_program_num_launches", "dxc_desc_size",
     "dxc_desc_reverse", "dxc_chunk_range", "dxc_l2_flush", "dxl_program_enable_kernel_timing",
-    "dxl_program_kernel_times", "dxl_program_kernel_names",
+    "dxl_program_kernel_times", "dxl_program_kernel_names", "dxl_program_set_input_n", "dxl_program_check",
 ]
 #: every symbol declared in include/dexlet_gmm.h
 GMM_ABI_SYMBOLS = [
@@ -166,7 +191,12 @@ def _check(rc: int):
 
 
 def lib() -> ctypes.CDLL:
-    return _lib
+    return _lib.load()
+
+
+def loaded() -> bool:
+    """Whether libdexlet_cuda.so has been mapped into this process."""
+    return _lib._cdll is not None
 
 
 def chunk_range(total: int, parts: int, c: int) -> Tuple[int, int]:
@@ -323,8 +353,14 @@ class Program:
 
     def set_input(self, i: int, leaf: int, arr: np.ndarray):
         arr = np.ascontiguousarray(arr)
-        dt = _DT_OF[arr.dtype]
-        _check(_lib.dxl_program_set_input(self.handle, i, leaf, arr.ctypes.data_as(_vp), dt))
+        dt = _DT_OF.get(arr.dtype)
+        if dt is None:
+            raise DexError(DXC_E_ARG, f"input {i} leaf {leaf}: unsupported dtype {arr.dtype}")
+        _check(_lib.dxl_program_set_input_n(self.handle, i, leaf, arr.ctypes.data_as(_vp), dt, arr.size))
+
+    def check(self):
+        """Raise DexError(E-bounds) if an index check failed (synchronizes)."""
+        _check(_lib.dxl_program_check(self.handle))
 
     def set_input_ptr(self, i: int, leaf: int, host_ptr: int, dtype: int):
         _check(_lib.dxl_program_set_input(self.handle, i, leaf, _vp(host_ptr), dtype))

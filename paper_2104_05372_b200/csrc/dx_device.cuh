@@ -385,7 +385,7 @@ __device__ __forceinline__ void dx_tile_rows4(const float* etile, int key, int* 
 // one writer, so the adds are plain LDS/FADD/STS with no atomics, no
 // collisions and no block barrier.  Order is fixed: ascending row within the
 // warp, copies folded in order by dx_warp_tab_flush.
-template <int D, int K, int FWD = 1>
+template <int D, int K>
 __device__ __forceinline__ void dx_warp_tab(const float* etile, int key, float* tab) {
   static_assert(D >= 4 && D <= 32 && (32 % D) == 0, "WarpTab row width");
   constexpr int G = 32 / D, NB = D / 4;
@@ -393,17 +393,7 @@ __device__ __forceinline__ void dx_warp_tab(const float* etile, int key, float* 
   const int g = lane / D, c = lane % D;
   const int k = key < 0 ? K : key;
   __syncwarp();
-  if constexpr (!FWD) {
-  float* tl = tab + g * D + c;
-#pragma unroll
-  for (int s = 0; s < 32 / G; ++s) {
-    const int r = s * G + g;
-    const int t = wbase + r;
-    const float v = etile[t * D + ((((c >> 2) ^ ((t >> 1) & (NB - 1)))) << 2) + (c & 3)];
-    const int kr = __shfl_sync(DX_FULL, k, r);
-    tl[kr * 32] += v;
-  }
-  } else {
+  {
   // Software-pipelined read-modify-write: the load of step s+1 is issued
   // before the store of step s (ordered volatile shared accesses), and when
   // both steps hit the same word the value just computed is forwarded.  Any

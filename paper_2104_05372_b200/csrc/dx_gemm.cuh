@@ -332,15 +332,58 @@ extern "C" __global__ void __launch_bounds__(192, 1)
                           unsigned* tickets) {
   dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
 }
-// N = 256 tiles (merged accumulator, 2 stages of 96 KB, 8 epilogue warps):
-// half the MMA instructions per flop of the N = 128 kernel (opt-in,
-// DEXLET_GEMM_N256=1).  The merged accumulator truncates the small products
-// against the large one: measured 15-50% more gradient error downstream of
-// an MLP forward GEMM, so it is not the default.
-extern "C" __global__ void __launch_bounds__(320, 1)
-    dx_gemm_tf32x3_n256(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
-                        const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
-                        long long N, long long K, float* C, long long ldc, long long mode, long long ksplit,
-                        unsigned* tickets) {
-  dx_gemm_tf32x3<256, 2, float, true>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
+
+// f64 parity mode (dxl_options.float64): the same contraction class in
+// binary64, as the reference evaluates it (eval.cpp:500-514).  SIMT f64 FMA,
+// 64 x 64 output tile per 256-thread block (4 x 4 per thread), K in steps of
+// 16 staged through shared memory; A and B are K-major f64 images written by
+// the operand prologues.  C[m][n] (+)= sum_k A[m][k] * B[n][k], each output
+// summed in ascending k (deterministic).
+extern "C" __global__ void __launch_bounds__(256) dx_gemm_f64(const double* __restrict__ A, const double* __restrict__ B,
+                                                              long long M, long long N, long long K, double* C,
+                                                              long long ldc, long long mode) {
+  __shared__ double As[16][64 + 1], Bs[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long NTn = (N + 63) / 64;
+  const long long m0 = (long long)(blockIdx.x / NTn) * 64, n0 = (long long)(blockIdx.x % NTn) * 64;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (long long k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = threadIdx.x + 256 * i, r = idx >> 4, c = idx & 15;
+      const long long k = k0 + c;
+      As[c][r] = (m0 + r < M && k < K) ? A[(m0 + r) * K + k] : 0.0;
+      Bs[c][r] = (n0 + r < N && k < K) ? B[(n0 + r) * K + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long n = n0 + tx + 16 * j;
+      if (n >= N) continue;
+      double* o = C + m * ldc + n;
+      *o = mode ? *o + acc[i][j] : acc[i][j];
+    }
+  }
 }

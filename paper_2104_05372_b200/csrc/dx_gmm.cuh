@@ -65,28 +65,17 @@
 // independent accumulators (hi*hi, hi*lo, lo*hi at +0, +64, +128: the MMAs of
 // a k-step do not wait on each other); A stage s (hi 32 columns, lo 32) at
 // 384 + 64 s.
-#if DXG_TMEM_A
 #define DXG_NXS 5                // X^T (+ beta, lse) stages of the backward TMA ring
-#else
-#define DXG_NXS 2                // (shared memory holds the A stages instead)
-#endif
 #ifndef DXG_NACC
 #define DXG_NACC 1               // TMEM accumulators per D buffer (1: merged, 3: hh / hl / lh)
 #endif
 #ifndef DXG_PN128  // pair kernel: one N=128 MMA over [X^T hi ; X^T lo] per A split
 #define DXG_PN128 (DXG_TMEM_A && DXG_NACC == 1)
 #endif
-#if DXG_PN128
 #define DXG_TD(b) ((b) * 128)  // D buffer b: 128 columns (products with x hi | x lo)
 #define DXG_TACC(i) 0
 #define DXG_NZS 4
 #define DXG_TA(s) (256 + 64 * (s))
-#else
-#define DXG_TD(b) ((b) * 64 * DXG_NACC)
-#define DXG_TACC(i) ((DXG_NACC == 3 ? (i) : 0) * 64)
-#define DXG_NZS ((512 - 128 * DXG_NACC) / 64)  // A stages filling the rest of TMEM
-#define DXG_TA(s) (128 * DXG_NACC + 64 * (s))
-#endif
 
 // ---- shared helpers ----------------------------------------------------------
 // byte offset of element (row, col) of a bf16 K-major SWIZZLE_128B image whose
@@ -536,396 +525,7 @@ extern "C" __global__ void __launch_bounds__(256) dx_gmm_lse(const float* __rest
 #define DXG_XT_BYTES (2 * DXG_D * 128)          // hi + lo image of one chunk
 #define DXG_XB_BYTES (DXG_BN * 128)             // one split of the B operand
 #define DXG_Z_BYTES (2 * 128 * 128)             // hi + lo A operand of one chunk
-#if DXG_TMEM_A
 #define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + DXG_BN * 128 * 8 + 1024)
-#else
-#define DXG_BWD_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_Z_BYTES + DXG_BN * 128 * 8 + 1024)
-#endif
-extern "C" __global__ void __launch_bounds__(448, 1)
-    dx_gmm_bwd_pair(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
-               const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
-               int K, long long n, long long npad, int P2,
-               double* __restrict__ dpart, double* __restrict__ wpart, int* __restrict__ ppart) {
-  extern __shared__ __align__(1024) unsigned char dxg_smem_raw[];
-  unsigned char* smem = dxg_smem_raw + ((1024u - (dx_smem_addr(dxg_smem_raw) & 1023u)) & 1023u);
-  unsigned char* bs = smem;                           // 2 stages x (hi 10 KB, lo 10 KB)
-  unsigned char* zs = smem + DXG_NXS * 2 * DXG_XB_BYTES;  // 2 stages x (hi 16 KB, lo 16 KB)
-#if DXG_TMEM_A
-  double* dacc = reinterpret_cast<double*>(zs);  // [80][128] fp64
-#else
-  double* dacc = reinterpret_cast<double*>(zs + 2 * DXG_Z_BYTES);  // [80][128] fp64
-#endif
-  // per stage: beta of the pair's two components and lse over the chunk's 64
-  // points (bulk-copied with X^T, so the producers never wait on HBM)
-  __shared__ __align__(16) float gin[DXG_NXS][3][DXG_BC];
-  __shared__ __align__(8) unsigned long long xfull[DXG_NXS], xempty[DXG_NXS], zfull[DXG_NZS], zempty[DXG_NZS], tfull[2], tempty[2];
-  __shared__ unsigned tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NP = (K + 1) / 2;
-  const long long C = npad / DXG_BC;  // chunks
-  const long long units = (long long)NP * P2;
-  // Units are enumerated chunk-range-major and dealt round-robin, so the CTAs
-  // running at the same time work on the same few chunk ranges (of different
-  // pairs) and each X^T chunk comes from HBM about once, then from L2.
-#define DXG_UNITS_LOOP for (long long u = blockIdx.x; u < units; u += gridDim.x)
-#define DXG_UNIT_SPLIT const long long pr = u % NP, p = u / NP
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < DXG_NZS; ++s) {
-      dx_mbar_init(&zfull[s], 8);
-      dx_mbar_init(&zempty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      dx_mbar_init(&tfull[s], 1);
-      dx_mbar_init(&tempty[s], 4);
-    }
-    for (int s = 0; s < DXG_NXS; ++s) {
-      dx_mbar_init(&xfull[s], 1);
-      dx_mbar_init(&xempty[s], 1);
-    }
-    dx_fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dx_smem_addr(&tmem_base)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  dx_fence_proxy_async();
-  dxg_fence_before();
-  __syncthreads();
-  dxg_fence_after();
-  const unsigned tmem = tmem_base;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      DXG_UNITS_LOOP {
-        DXG_UNIT_SPLIT;
-        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-        const long long k0 = pr * 2, k1 = (pr * 2 + 1 < K) ? pr * 2 + 1 : pr * 2;
-        for (long long c = c0; c < c1; ++c, ++it) {
-          const int s = it % DXG_NXS;
-          if (it >= DXG_NXS) dx_mbar_wait_bounded(&xempty[s], (unsigned)(((it / DXG_NXS) - 1) & 1));
-#ifdef DXG_DBG_NOGIN  // (timing experiment: only the X^T images)
-          dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES);
-#else
-          dx_mbar_expect_tx(&xfull[s], DXG_XT_BYTES + 3 * DXG_BC * 4);
-#endif
-          const unsigned char* src = xtimg + c * DXG_XT_BYTES;
-          dx_bulk_g2s(bs + (s * 2) * DXG_XB_BYTES, src, DXG_D * 128, &xfull[s]);
-          dx_bulk_g2s(bs + (s * 2 + 1) * DXG_XB_BYTES, src + DXG_D * 128, DXG_D * 128, &xfull[s]);
-#ifndef DXG_DBG_NOGIN
-          dx_bulk_g2s(gin[s][0], beta + k0 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
-          dx_bulk_g2s(gin[s][1], beta + k1 * npad + c * DXG_BC, DXG_BC * 4, &xfull[s]);
-          dx_bulk_g2s(gin[s][2], lse + c * DXG_BC, DXG_BC * 4, &xfull[s]);
-#endif
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const unsigned idesc = dxg_idesc_f16<DXG_PN128 ? 2 * DXG_BN : DXG_BN>();
-      const unsigned baddr = dx_smem_addr(bs), zaddr = dx_smem_addr(zs);
-      int it = 0, pc = 0;
-      long long prevPair = -1;
-      int inb = 0;  // chunks accumulated into the current TMEM buffer
-      DXG_UNITS_LOOP {
-        DXG_UNIT_SPLIT;
-        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-        if (pr != prevPair && inb > 0) {  // flush at pair change
-          dx_umma_commit(&tfull[pc & 1]);
-          ++pc;
-          inb = 0;
-        }
-        prevPair = pr;
-        for (long long c = c0; c < c1; ++c, ++it) {
-          const int s = it % DXG_NZS;
-          if (inb == 0 && pc >= 2) dx_mbar_wait_bounded(&tempty[pc & 1], (unsigned)(((pc >> 1) - 1) & 1));
-          const int xs = it % DXG_NXS;
-          dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
-          dx_mbar_wait_bounded(&zfull[s], (unsigned)((it / DXG_NZS) & 1));
-          dxg_fence_after();
-          // buffer (pc & 1): columns [256 b, 256 b + 80) take hi*hi, [+128, +208)
-          // the small hi*lo + lo*hi products (fewer truncating adds on the big sum)
-          const unsigned td = tmem + (unsigned)DXG_TD(pc & 1);
-          const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
-#if DXG_TMEM_A
-          (void)zaddr;
-          const unsigned tah = tmem + (unsigned)DXG_TA(s), tal = tah + 32;
-#pragma unroll
-          for (int kk = 0; kk < DXG_BC / 16; ++kk) {
-            const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
-            const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
-            const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
-#ifndef DXG_DBG_NOMMA  // (timing experiment: the pipeline without tensor-core work)
-#if DXG_PN128
-            (void)dbl;
-            dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
-            dxg_umma_f16_ta(td, tal + kk * 8, dbh, idesc, 1u);
-#else
-            dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, acc);
-            dxg_umma_f16_ta(td + DXG_TACC(1), tah + kk * 8, dbl, idesc, DXG_NACC == 3 ? acc : 1u);
-            dxg_umma_f16_ta(td + DXG_TACC(2), tal + kk * 8, dbh, idesc, DXG_NACC == 3 ? acc : 1u);
-#endif
-#else
-            (void)acc; (void)dbh; (void)dbl;
-#endif
-          }
-#else
-          const unsigned zh = zaddr + (unsigned)(s * DXG_Z_BYTES), zl = zh + 128 * 128;
-#pragma unroll
-          for (int kk = 0; kk < DXG_BC / 16; ++kk) {
-            const unsigned long long ah = dx_umma_desc_sw128(zh + kk * 32);
-            const unsigned long long al = dx_umma_desc_sw128(zl + kk * 32);
-            const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
-            const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
-            const unsigned acc = (inb > 0 || kk > 0) ? 1u : 0u;
-            dxg_umma_f16(td, ah, dbh, idesc, acc);
-            dxg_umma_f16(td + DXG_TACC(1), ah, dbl, idesc, DXG_NACC == 3 ? acc : 1u);
-            dxg_umma_f16(td + DXG_TACC(2), al, dbh, idesc, DXG_NACC == 3 ? acc : 1u);
-          }
-#endif
-          dx_umma_commit(&xempty[xs]);
-          dx_umma_commit(&zempty[s]);
-          if (++inb == DXG_PROMO) {
-            dx_umma_commit(&tfull[pc & 1]);
-            ++pc;
-            inb = 0;
-          }
-        }
-      }
-      if (inb > 0) {
-        dx_umma_commit(&tfull[pc & 1]);
-        ++pc;
-      }
-    }
-  } else if (warp < 10) {
-    // A-operand producers: thread (row r = (k_local, b), half hh of the chunk's
-    // points).  Z[(k,b)][i] = g_ik (x_ib - mu_kb), centred on the component's
-    // mean so the moments need no cancelling correction (M = D - m~ mu^T).
-    // g is computed once per (component, point): lane q of a warp evaluates
-    // point hh*32+q and the warp shares the 32 values through shared memory.
-    const int pt = threadIdx.x - 64;       // 0..255
-    const int pw = pt >> 5;                // producer warp 0..7
-#if DXG_TMEM_A
-    // TMEM lane access: warp w owns lanes 32 (w % 4) .. +31 = rows of A
-    const int r = (warp & 3) * 32 + lane, hh = pw >> 2;
-    const bool wrow = (r & 32) == 0;       // warps holding rows b < 32 accumulate W
-    const int wk0a = 2, wk0b = 6, wk1a = 0, wk1b = 4;  // producer warps of the b<32 rows of k_local 0 / 1
-#else
-    const int r = pt & 127, hh = pt >> 7;  // row of Z, point half
-    const bool wrow = (pw & 1) == 0;       // warps holding rows b < 32 accumulate W
-    const int wk0a = 0, wk0b = 4, wk1a = 2, wk1b = 6;
-#endif
-    const int kl = r >> 6, b = r & 63;
-    __shared__ __align__(16) float gw[8][32];
-    __shared__ float wred[8];
-    __shared__ double mred[2][128];
-    double msum = 0.0;  // sum of this thread's z = g (x - mu) over its points
-    const float sx = dxg_scale_for(__uint_as_float(*xmax));
-    int it = 0;
-    float wacc = 0.f, mub = 0.f;
-    long long prevPair = -1;
-    int slot = 0;
-    auto flushW = [&]() {  // W of the finished pair: fixed-order reduction over points
-      const float w = dx_warp_sum(wacc);
-      dxg_named_sync(2, 256);
-      if (lane == 0) wred[pw] = w;
-      dxg_named_sync(2, 256);
-      mred[hh][r] = msum;
-      dxg_named_sync(2, 256);
-      double* wp = wpart + ((long long)blockIdx.x * DXG_FMAX + slot) * DXG_WP;
-      if (pt < 2) wp[pt * (1 + DXG_D)] = (double)(pt == 0 ? wred[wk0a] + wred[wk0b] : wred[wk1a] + wred[wk1b]);
-      if (hh == 0) wp[kl * (1 + DXG_D) + 1 + b] = mred[0][r] + mred[1][r];
-      msum = 0.0;
-      ++slot;
-    };
-    DXG_UNITS_LOOP {
-      DXG_UNIT_SPLIT;
-      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-      const int k = (int)(pr * 2 + kl);
-      const bool live = k < K;
-      if (pr != prevPair) {
-        if (prevPair >= 0) flushW();
-        prevPair = pr;
-        wacc = 0.f;
-        mub = live ? means[(long long)k * DXG_D + b] * sx : 0.f;
-      }
-      for (long long c = c0; c < c1; ++c, ++it) {
-        const int s = it % DXG_NZS;
-        const int xs = it % DXG_NXS;
-        if (it >= DXG_NZS) dx_mbar_wait_bounded(&zempty[s], (unsigned)(((it / DXG_NZS) - 1) & 1));
-        dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
-        {
-          const int q = hh * 32 + lane;
-          const float gg = __expf(gin[xs][kl][q] - gin[xs][2][q]);
-          const float gq = (live && c * DXG_BC + q < n) ? gg : 0.f;
-          if (wrow) wacc += gq;
-          gw[pw][lane] = gq;
-          __syncwarp();
-        }
-        const unsigned char* xh = bs + (xs * 2) * DXG_XB_BYTES;
-        const unsigned char* xl = xh + DXG_XB_BYTES;
-        float mchunk = 0.f;  // this chunk's part of m~ (32 points)
-#if DXG_TMEM_A
-        unsigned th[16], tl[16];
-#else
-        unsigned char* zh = zs + s * DXG_Z_BYTES;
-        unsigned char* zl = zh + 128 * 128;
-#endif
-#ifdef DXG_DBG_NOPROD  // (timing experiment: tensor-core pipeline without the SIMT producers)
-#pragma unroll
-        for (int w = 0; w < 16; ++w) th[w] = tl[w] = 0u;
-#else
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {  // 4 x 8 points = 16-byte chunks
-          const int pcol = hh * 32 + cc * 8;
-          const unsigned off_x = dxg_sw((unsigned)b, (unsigned)pcol);
-          const uint4 h4 = *reinterpret_cast<const uint4*>(xh + off_x);
-          const uint4 l4 = *reinterpret_cast<const uint4*>(xl + off_x);
-          const float4 ga = *reinterpret_cast<const float4*>(&gw[pw][cc * 8]);
-          const float4 gb = *reinterpret_cast<const float4*>(&gw[pw][cc * 8 + 4]);
-          const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-          const unsigned hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
-          unsigned oh[4], ol[4];
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const float x0 = dxg_h_lo(hw[w]) + dxg_h_lo(lw[w]) - mub;
-            const float x1 = dxg_h_hi(hw[w]) + dxg_h_hi(lw[w]) - mub;
-            const float z0 = gv[2 * w] * x0, z1 = gv[2 * w + 1] * x1;
-            mchunk += z0 + z1;
-            dxg_split2(z0, z1, oh[w], ol[w]);
-          }
-#if DXG_TMEM_A
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            th[cc * 4 + w] = oh[w];
-            tl[cc * 4 + w] = ol[w];
-          }
-#else
-          const unsigned off_z = dxg_sw((unsigned)r, (unsigned)pcol);
-          *reinterpret_cast<uint4*>(zh + off_z) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
-          *reinterpret_cast<uint4*>(zl + off_z) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
-#endif
-        }
-#endif
-        msum += (double)mchunk;
-#if DXG_TMEM_A
-        {
-          const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(DXG_TA(s) + hh * 16);
-#ifndef DXG_DBG_NOSTTM  // (timing experiment)
-          DXG_TMEM_ST16(ta, th);
-          DXG_TMEM_ST16(ta + 32, tl);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#else
-          (void)ta;
-#endif
-          dxg_fence_before();
-        }
-#else
-        dx_fence_proxy_async();  // generic-proxy writes -> tensor-core reads
-#endif
-        __syncwarp();
-        if (lane == 0) dx_mbar_arrive(&zfull[s]);
-      }
-    }
-    if (prevPair >= 0) flushW();
-  } else {
-    // promotion epilogue: warps 10..13 -> TMEM lane quarter (warp & 3)
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const unsigned lanebase = tmem + ((unsigned)(q * 32) << 16);
-#pragma unroll 4
-    for (int j = 0; j < DXG_BN; ++j) dacc[j * 128 + row] = 0.0;
-    float acc[DXG_BN];
-#pragma unroll
-    for (int j = 0; j < DXG_BN; ++j) acc[j] = 0.f;
-    int pc = 0, inb = 0, slot = 0, nacc = 0;
-    long long prevPair = -1;
-    auto spill = [&]() {  // fp32 partial of <= DXG_F64_EVERY chunks -> fp64
-#pragma unroll
-      for (int j = 0; j < DXG_BN; ++j) {
-        dacc[j * 128 + row] += (double)acc[j];
-        acc[j] = 0.f;
-      }
-      nacc = 0;
-    };
-    auto drain = [&]() {
-      const int b = pc & 1;
-      dx_mbar_wait_bounded(&tfull[b], (unsigned)((pc >> 1) & 1));
-      dxg_fence_after();
-#pragma unroll
-      for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
-#if DXG_NACC == 3
-        unsigned v[16], w[16], x[16];
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + 64 + j0), w);
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + 128 + j0), x);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]) + (__uint_as_float(w[j]) + __uint_as_float(x[j]));
-#elif DXG_PN128
-        unsigned v[16], w[16];
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + DXG_BN + j0), w);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          const float2 t = dx_f2add(make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
-                                    make_float2(__uint_as_float(w[j]), __uint_as_float(w[j + 1])));
-          const float2 a2 = dx_f2add(make_float2(acc[j0 + j], acc[j0 + j + 1]), t);
-          acc[j0 + j] = a2.x;
-          acc[j0 + j + 1] = a2.y;
-        }
-#else
-        unsigned v[16];
-        DXG_TMEM_LD16(lanebase + (unsigned)(DXG_TD(b) + j0), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]);
-#endif
-      }
-      dxg_fence_before();
-      __syncwarp();
-      if (lane == 0) dx_mbar_arrive(&tempty[b]);
-      ++pc;
-      if (++nacc == DXG_F64_EVERY) spill();
-    };
-    auto flush = [&](long long pair) {
-      spill();
-      double* dst = dpart + (((long long)blockIdx.x * DXG_FMAX + slot) * 128 + row) * DXG_BN;
-#pragma unroll 4
-      for (int j = 0; j < DXG_BN; ++j) {
-        dst[j] = dacc[j * 128 + row];
-        dacc[j * 128 + row] = 0.0;
-      }
-      if (threadIdx.x == 320) ppart[blockIdx.x * DXG_FMAX + slot] = (int)pair;
-      ++slot;
-    };
-    DXG_UNITS_LOOP {
-      DXG_UNIT_SPLIT;
-      const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-      if (pr != prevPair && prevPair >= 0) {
-        if (inb > 0) { drain(); inb = 0; }
-        flush(prevPair);
-      }
-      prevPair = pr;
-      for (long long c = c0; c < c1; ++c)
-        if (++inb == DXG_PROMO) { drain(); inb = 0; }
-    }
-    if (prevPair >= 0) {
-      if (inb > 0) drain();
-      flush(prevPair);
-    }
-  }
-  dxg_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-  }
-}
-
 // ---- backward, two pairs (four components) per unit (default) ----------------------
 // Same math as dx_gmm_bwd_pair, but each X^T chunk staged by the bulk-copy ring
 // feeds the MMAs of two component pairs (the single-pair kernel is bound by
@@ -940,12 +540,6 @@ extern "C" __global__ void __launch_bounds__(448, 1)
 // error of the tensor core's fp32 accumulation at the single-pair kernel's.
 #define DXG_QWP (4 * (1 + DXG_D))
 #define DXG_BWD4_SMEM (DXG_NXS * 2 * DXG_XB_BYTES + 2 * DXG_BN * 128 * 8 + 1024)
-#ifndef DXG_PROMO4
-#define DXG_PROMO4 1
-#endif
-#ifndef DXG_N128
-#define DXG_N128 1  // one N=128 MMA over [X^T hi ; X^T lo] per A split (0: three N=64 MMAs)
-#endif
 extern "C" __global__ void __launch_bounds__(576, 1)
     dx_gmm_bwd(const unsigned char* __restrict__ xtimg, const float* __restrict__ beta,
                 const float* __restrict__ lse, const float* __restrict__ means, const unsigned* __restrict__ xmax,
@@ -1013,7 +607,6 @@ extern "C" __global__ void __launch_bounds__(576, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-#if DXG_N128
       // B = [X^T hi ; X^T lo]: the two images of a chunk are contiguous SW128
       // row groups, i.e. one N=128 operand.  D[q] (128 columns: products with
       // x hi | x lo) = A_hi B + A_lo B over one chunk, drained every chunk.
@@ -1045,43 +638,6 @@ extern "C" __global__ void __launch_bounds__(576, 1)
           dx_umma_commit(&xempty[xs]);
         }
       }
-#else
-      const unsigned idesc = dxg_idesc_f16<DXG_BN>();
-      const unsigned baddr = dx_smem_addr(bs);
-      int it = 0, pc = 0, inb = 0;
-      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        const long long p = u / NQ;
-        const long long c0 = p * C / P2, c1 = (p + 1) * C / P2;
-        for (long long c = c0; c < c1; ++c, ++it) {
-          const int xs = it % DXG_NXS, s = it & 1;
-          dx_mbar_wait_bounded(&xfull[xs], (unsigned)((it / DXG_NXS) & 1));
-          const unsigned bh = baddr + (unsigned)(xs * 2 * DXG_XB_BYTES), bl = bh + DXG_XB_BYTES;
-          for (int q = 0; q < 2; ++q) {
-            if (inb == 0 && pc >= 2) dx_mbar_wait_bounded(&tempty[q][pc & 1], (unsigned)(((pc >> 1) - 1) & 1));
-            dx_mbar_wait_bounded(&zfull[q][s], (unsigned)((it >> 1) & 1));
-            dxg_fence_after();
-            const unsigned td = tmem + (unsigned)((2 * q + (pc & 1)) * 64);
-            const unsigned tah = tmem + (unsigned)(256 + (2 * q + s) * 64), tal = tah + 32;
-#pragma unroll
-            for (int kk = 0; kk < DXG_BC / 16; ++kk) {
-              const unsigned long long dbh = dx_umma_desc_sw128(bh + kk * 32);
-              const unsigned long long dbl = dx_umma_desc_sw128(bl + kk * 32);
-              dxg_umma_f16_ta(td, tah + kk * 8, dbh, idesc, (inb > 0 || kk > 0) ? 1u : 0u);
-              dxg_umma_f16_ta(td, tah + kk * 8, dbl, idesc, 1u);
-              dxg_umma_f16_ta(td, tal + kk * 8, dbh, idesc, 1u);
-            }
-            dx_umma_commit(&zempty[q][s]);
-          }
-          dx_umma_commit(&xempty[xs]);
-          if (++inb == DXG_PROMO4 || c + 1 == c1) {  // every unit ends with a drain
-            dx_umma_commit(&tfull[0][pc & 1]);
-            dx_umma_commit(&tfull[1][pc & 1]);
-            ++pc;
-            inb = 0;
-          }
-        }
-      }
-#endif
     }
   } else if (warp < 10) {
     const int pw = warp - 2, q = pw >> 2;           // pair of this producer warp
@@ -1117,10 +673,6 @@ extern "C" __global__ void __launch_bounds__(576, 1)
         const unsigned char* xl = xh + DXG_XB_BYTES;
         unsigned th[32], tl[32];
         float2 mchunk = make_float2(0.f, 0.f);  // even / odd points
-#ifdef DXG_DBG_NOPROD  // (timing experiment: no SIMT producer math)
-#pragma unroll
-        for (int w = 0; w < 32; ++w) th[w] = tl[w] = 0u;
-#else
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {  // 8 x 8 points
           const unsigned off_x = dxg_sw((unsigned)b, (unsigned)(cc * 8));
@@ -1139,7 +691,6 @@ extern "C" __global__ void __launch_bounds__(576, 1)
             dxg_split2v(z, th[cc * 4 + w], tl[cc * 4 + w]);
           }
         }
-#endif
         msum += (double)(mchunk.x + mchunk.y);
         {
           const unsigned ta = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)(256 + (2 * q + s) * 64);
@@ -1182,16 +733,11 @@ extern "C" __global__ void __launch_bounds__(576, 1)
       const int qd = (int)(u % NQ);
       const long long p = u / NQ;
       const int nch = (int)((p + 1) * C / P2 - p * C / P2);  // chunks of this unit (32-bit: registers)
-#if !DXG_N128
-      int inb = 0;
-#endif
       for (int c = 0; c < nch; ++c) {
-#if DXG_N128
         {
           dx_mbar_wait_bounded(&tfull[q][0], (unsigned)(pc & 1));
           dxg_fence_after();
 #pragma unroll
-#ifndef DXG_DBG_NODRAIN
           for (int j0 = 0; j0 < DXG_BN; j0 += 8) {  // x8 loads: acc[64] + 16 in flight (96 registers at 576 threads)
             unsigned v[8], w[8];
             DXG_TMEM_LD8(lanebase + (unsigned)(q * 128 + j0), v);
@@ -1206,34 +752,12 @@ extern "C" __global__ void __launch_bounds__(576, 1)
               acc[j0 + j + 1] = a2.y;
             }
           }
-#endif
           dxg_fence_before();
           __syncwarp();
           if (lane == 0) dx_mbar_arrive(&tempty[q][0]);
           ++pc;
           if (++nacc == DXG_F64_EVERY) spill();
         }
-#else
-        if (++inb == DXG_PROMO4 || c + 1 == nch) {
-          const int bb = pc & 1;
-          dx_mbar_wait_bounded(&tfull[q][bb], (unsigned)((pc >> 1) & 1));
-          dxg_fence_after();
-#pragma unroll
-          for (int j0 = 0; j0 < DXG_BN; j0 += 16) {
-            unsigned v[16];
-            DXG_TMEM_LD16(lanebase + (unsigned)((2 * q + bb) * 64 + j0), v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(v[j]);
-          }
-          dxg_fence_before();
-          __syncwarp();
-          if (lane == 0) dx_mbar_arrive(&tempty[q][bb]);
-          ++pc;
-          inb = 0;
-          if (++nacc == DXG_F64_EVERY) spill();
-        }
-#endif
       }
       // flush this unit: rows (q, row) of the quad's D to an fp64 slot
       spill();

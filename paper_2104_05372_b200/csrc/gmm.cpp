@@ -33,12 +33,8 @@ constexpr int NXS = 5;  // DXG_NXS
 constexpr int MOM = D * D + D + 1;
 constexpr int FWD_SMEM = 2 * GC * 64 * 128 + FXS * 2 * TM * 128 + 1024;
 inline int bwd4Smem() { return NXS * 2 * (BN * 128) + 2 * BN * 128 * 8 + 1024; }
-inline int bwdSmem() {
-  const bool smemA = std::getenv("DEXLET_GMM_SMEM_A") != nullptr;
-  return (smemA ? 2 : NXS) * 2 * (BN * 128) + (smemA ? 2 * (2 * 128 * 128) : 0) + BN * 128 * 8 + 1024;
-}
 constexpr int FIN_SMEM = 2 * D * (D + 1) * 8;
-enum { K_ABSMAX, K_PREPQ, K_PREPX, K_FWD, K_LSE, K_SUM, K_BWD, K_MOM, K_FIN, K_N, K_PAIR = K_N };
+enum { K_ABSMAX, K_PREPQ, K_PREPX, K_FWD, K_LSE, K_SUM, K_BWD, K_MOM, K_FIN, K_N };
 const char* kNames[K_N] = {"dx_gmm_absmax", "dx_gmm_prep_q", "dx_gmm_prep_x", "dx_gmm_fwd", "dx_gmm_lse",
                            "dx_gmm_sum",    "dx_gmm_bwd",    "dx_gmm_moments", "dx_gmm_finish"};
 
@@ -84,8 +80,7 @@ double logGammaDistrib(double a, int p) {
 struct dxg_gmm {
   dxrt::Ctx* ctx = nullptr;
   CUmodule mod = nullptr;
-  CUfunction fn[K_N + 1] = {};
-  bool quad = true;  // dx_gmm_bwd (two pairs per unit) rather than dx_gmm_bwd_pair
+  CUfunction fn[K_N] = {};
   int K = 0, NG = 0, NP = 0, P = 1, P2 = 1, gridF = 1, gridB = 1, gridL = 1;
   long long n = 0, ng = 0, npad = 0, T = 0, C = 0;
   CUdeviceptr alphas = 0, means = 0, icf = 0, x = 0;
@@ -144,35 +139,14 @@ int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global,
   const int sms = ctx->smCount;
   g->P = pickP(g->NG, g->T, sms);
   g->gridF = (int)std::min<long long>(sms, (long long)g->NG * g->P);
-  // dx_gmm_bwd feeds two component pairs from each X^T chunk (13% faster
-  // than the single-pair kernel at the same accuracy); DEXLET_GMM_BWD_PAIR=1
-  // selects dx_gmm_bwd_pair (experiments)
-  g->quad = std::getenv("DEXLET_GMM_BWD_PAIR") == nullptr;
-  g->P2 = pickP2(g->quad ? (k + 3) / 4 : g->NP, g->C, sms);
-  if (const char* e = std::getenv("DEXLET_GMM_P2")) g->P2 = std::max(1, std::atoi(e));  // (experiments)
-  g->gridB = (int)std::min<long long>(sms, (long long)(g->quad ? (k + 3) / 4 : g->NP) * g->P2);
+  // dx_gmm_bwd feeds two component pairs (a quad) from each X^T chunk
+  g->P2 = pickP2((k + 3) / 4, g->C, sms);
+  g->gridB = (int)std::min<long long>(sms, (long long)((k + 3) / 4) * g->P2);
   g->gridL = (int)std::min<long long>(8 * sms, (g->n + 255) / 256);  // 2048 threads per SM: more loads in flight
-  // DEXLET_GMM_SMEM_A=1: backward A operand staged in shared memory (A/B)
-  std::string src = std::string(std::getenv("DEXLET_GMM_SMEM_A") ? "#define DXG_TMEM_A 0\n" : "");
-  if (const char* e = std::getenv("DEXLET_GMM_PROMO")) src += std::string("#define DXG_PROMO ") + e + "\n";
-  if (std::getenv("DEXLET_GMM_DBG_NOPROD")) src += "#define DXG_DBG_NOPROD 1\n";
-  if (std::getenv("DEXLET_GMM_DBG_NODRAIN")) src += "#define DXG_DBG_NODRAIN 1\n";
-  if (std::getenv("DEXLET_GMM_DBG_NOMMA")) src += "#define DXG_DBG_NOMMA 1\n";
-  if (std::getenv("DEXLET_GMM_DBG_NOGIN")) src += "#define DXG_DBG_NOGIN 1\n";
-  if (std::getenv("DEXLET_GMM_DBG_NOSTTM")) src += "#define DXG_DBG_NOSTTM 1\n";
-  if (const char* e = std::getenv("DEXLET_GMM_NACC")) src += std::string("#define DXG_NACC ") + e + "\n";
-  if (const char* e = std::getenv("DEXLET_GMM_PROMO4")) src += std::string("#define DXG_PROMO4 ") + e + "\n";
-  if (std::getenv("DEXLET_GMM_N64")) src += "#define DXG_N128 0\n";
-  src += std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
+  std::string src = std::string(dxrt::gemmSource()) + "\n" + dxrt::gmmSource();
   if ((rc = ctx->loadModule(src, &g->mod))) { delete g; return rc; }
   for (int i = 0; i < K_N; ++i)
     if ((rc = check(cuModuleGetFunction(&g->fn[i], g->mod, kNames[i]), kNames[i]))) { delete g; return rc; }
-  if ((rc = check(cuModuleGetFunction(&g->fn[K_PAIR], g->mod, "dx_gmm_bwd_pair"), "dx_gmm_bwd_pair"))) { delete g; return rc; }
-  if ((rc = check(cuFuncSetAttribute(g->fn[K_PAIR], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bwdSmem()),
-                  "smem bwd pair"))) {
-    delete g;
-    return rc;
-  }
   if ((rc = check(cuFuncSetAttribute(g->fn[K_FWD], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, FWD_SMEM), "smem fwd")) ||
       (rc = check(cuFuncSetAttribute(g->fn[K_BWD], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bwd4Smem()), "smem bwd")) ||
       (rc = check(cuFuncSetAttribute(g->fn[K_FIN], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, FIN_SMEM), "smem fin"))) {
@@ -251,6 +225,18 @@ int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
   if (!(gamma > 0.0) || wm < 0) { setError("dxg_gmm_run: Wishart gamma must be > 0 and m >= 0"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
+  if (g->ng != g->n) {
+    // a shard of the points: the moments and the log-likelihood must be
+    // summed over exactly the ranks that hold the other shards
+    if (!g->ctx->comm) {
+      setError("dxg_gmm_run: sharded plan (n_global > n_local) needs dxc_comm_init on the context first");
+      return DXC_E_ARG;
+    }
+    if (g->ctx->nranks < 2) {
+      setError("dxg_gmm_run: sharded plan (n_global > n_local) over a one-rank communicator");
+      return DXC_E_ARG;
+    }
+  }
   g->gamma = gamma;
   g->wm = wm;
   g->haveGrad = want_grad != 0;
@@ -289,17 +275,9 @@ int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
     if ((rc = check(cuMemsetD8Async(g->ppart, 0xff, (size_t)g->gridB * FMAX * 4, s), "memset ppart"))) return rc;
     int P2 = g->P2;
     void* a[] = {&g->xtimg, &g->beta, &g->lse, &g->means, &g->xmax, &K, &n, &npad, &P2, &g->dpart, &g->wpart, &g->ppart};
-    if (!g->quad) {
-      if (g->timing) cuEventRecord(g->ev[K_BWD], g->ctx->stream);
-      if ((rc = check(cuLaunchKernel(g->fn[K_PAIR], (unsigned)g->gridB, 1, 1, 448, 1, 1, bwdSmem(), g->ctx->stream, a,
-                                     nullptr),
-                      "dx_gmm_bwd_pair")))
-        return rc;
-    } else if ((rc = launch(g, K_BWD, (unsigned)g->gridB, 576, bwd4Smem(), a))) {
-      return rc;
-    }
+    if ((rc = launch(g, K_BWD, (unsigned)g->gridB, 576, bwd4Smem(), a))) return rc;
     int nslot = g->gridB * FMAX;
-    int G = g->quad ? 4 : 2;
+    int G = 4;
     void* b[] = {&g->dpart, &g->wpart, &g->ppart, &nslot, &g->xmax, &G, &g->mom};
     if ((rc = launch(g, K_MOM, (unsigned)K, 256, 0, b))) return rc;
   }

@@ -1695,7 +1695,7 @@ class Lowering {
                       " + q * 16), 3))";
             std::string ct = fl ? "dx_f" : ctype(s0.kind);
             std::string vt = es == 8 ? (fl ? "double2" : "longlong2") : (fl ? "float4" : "int4");
-            g.line(ct + " " + r + "[" + lit(cnt) + "];");
+            g.line(ct + " " + r + "[" + lit(std::max(1LL, (long long)cnt)) + "];");
             g.line("#pragma unroll");
             g.line("for (int q = 0; q < " + lit(cnt / vw) + "; ++q) { const " + vt + " w = *(const " + vt + "*)(" +
                    addrq + "); " +
@@ -1919,7 +1919,7 @@ class Lowering {
       s.base = nm + "_" + std::to_string(l);
       s.off = "0";
       s.kind = lv[l].kind;
-      g.line(ctype(s.kind) + " " + s.base + "[" + lit(lv[l].count) + "]" + (zero ? " = {}" : "") + ";");
+      g.line(ctype(s.kind) + " " + s.base + "[" + lit(std::max(1LL, (long long)lv[l].count)) + "]" + (zero ? " = {}" : "") + ";");
       slots.push_back(s);
     }
     return slots;
@@ -2532,8 +2532,7 @@ class Lowering {
     const auto* ra = as<VRefType>(r.action.refAnnot);
     if (!ra) fail(ErrCode::Internal, "runAccum reached the lowering unannotated", e->span);
     DTy payload = resolveType(ra->payload, kernelLook(g, s));
-    if (!std::getenv("DEXLET_NO_KMAP"))
-      if (KV m = accumToMapK(g, s, r, payload)) return m;
+    if (KV m = accumToMapK(g, s, r, payload)) return m;
     std::vector<Slot> slots = localArrays(g, payload, true);
     std::vector<LeafInfo> plv = leaves(payload);
     if (g.inCand || g.inLaneLoop)
@@ -2834,7 +2833,6 @@ class Lowering {
 // ---------------------------------------------------------------------------
 
 static int tileThreads() {
-  if (const char* e = std::getenv("DEXLET_TILE_NT")) return std::atoi(e);
   return 256;
 }
 
@@ -2861,8 +2859,7 @@ void Lowering::decideStrategies(KGen& g) {
       smemUsed += (int)cu.width * 4;
       continue;
     }
-    if (cu.allRow && cu.rowD > 0 && cu.rowSitesN == 1 && !opt.noRowScatter && !tileRowTaken &&
-        !std::getenv("DEXLET_NO_TILEROW")) {
+    if (cu.allRow && cu.rowD > 0 && cu.rowSitesN == 1 && !opt.noRowScatter && !tileRowTaken) {
       long long Kr = cu.width / cu.rowD;
       const int NT = tileThreads();
       long long need = (long long)NT * (cu.rowD + 1) * esize + (NT / 32) * Kr * 4 + (Kr + 1) * 4 + NT * 4 + 64;
@@ -2912,7 +2909,7 @@ void Lowering::decideStrategies(KGen& g) {
       // barrier per tile (dx_warp_tab); needs (K+1) x 128 B per warp.
       long long wt = (long long)(NT / 32) * (Kr + 1) * 128;
       cu.warpTab = !opt.f64 && cu.rowD % 4 == 0 && 32 % cu.rowD == 0 &&
-                   cu.smemOff + wt + (long long)NT * cu.rowD * 4 <= (NT > 256 ? 200 : 150) * 1024 && !std::getenv("DEXLET_NO_WARPTAB");
+                   cu.smemOff + wt + (long long)NT * cu.rowD * 4 <= (NT > 256 ? 200 : 150) * 1024;
       cu.vec4 = cu.warpTab || (!opt.f64 && cu.rowD % 4 == 0 && Kr * (cu.rowD / 4) <= NT);
       if (cu.warpTab) {
         off = cu.smemOff + (int)(wt + (long long)NT * cu.rowD * 4);
@@ -2987,7 +2984,7 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
     if (!serial) {
       long long rest = total;
       for (size_t i = 0; i < kb0.dims.size(); ++i) {
-        rest /= size(kb0.dims[i]);
+        rest = size(kb0.dims[i]) ? rest / size(kb0.dims[i]) : 0;  // Fin 0: empty space
         if (kb0.dims.size() == 1) ords.push_back(o);
         else {
           std::string ord = g.fresh("kd");
@@ -3130,6 +3127,10 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
                         const std::vector<long long>* intoOffs) {
   const KernelBody& kb0 = parts[0];
   long long total = serial ? 1 : size(kb0.desc);
+  // an empty index set (Fin 0): no iteration, no effect, empty outputs -- the
+  // reference's enumerate is empty too (eval.cpp:295-308); cells keep their
+  // zeroOfType value (eval.cpp:452-464).  Nothing is compiled or launched.
+  const bool empty = !serial && total == 0;
   std::string kname = kernelName();
   std::vector<int> outBufs;
   std::vector<long long> outOffs;
@@ -3173,7 +3174,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   g.staged.clear();
   g.wholeStaged.clear();
   g.tensorStaged.clear();
-  if (g.tile && !std::getenv("DEXLET_NO_TMA")) {
+  if (g.tile) {
     int es = opt.f64 ? 8 : 4;
     long long budget = 96 * 1024;
     for (auto& [b, lb] : g.streamUse) {
@@ -3187,7 +3188,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       g.staged.insert(b);
       long long rowB = lb.first * eb;
       if (g.needAlign.count(b) && !opt.f64 && plan.bufs[b].kind == SK::F && aligned &&
-          (rowB == 32 || rowB == 64 || rowB == 128) && g.threads % 256 == 0 && !std::getenv("DEXLET_NO_TMA_TENSOR"))
+          (rowB == 32 || rowB == 64 || rowB == 128) && g.threads % 256 == 0)
         g.tensorStaged[b] = rowB == 32 ? 1 : rowB == 64 ? 3 : 7;
     }
     for (int b : g.nonStream) {
@@ -3203,19 +3204,18 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     cu.aliasStage = -1;
     if (cu.strat != CellUse::TileRow || !cu.vec4) continue;
     for (auto& [b, mask] : g.tensorStaged)
-      if (g.streamUse[b].first == cu.rowD && plan.bufs[b].kind == SK::F && !std::getenv("DEXLET_NO_ALIAS"))
+      if (g.streamUse[b].first == cu.rowD && plan.bufs[b].kind == SK::F)
         cu.aliasStage = b;
   }
   // warp per ordinal for short outer loops over long reductions (row sums)
   g.warpRow = !serial && g.warpRowOK && g.laneLoopId >= 0 && g.cells.empty() && !hasRow && !g.tile &&
-              kb0.dims.size() == 1 && total <= 148LL * 256 && !std::getenv("DEXLET_NO_WARPROW");
+              kb0.dims.size() == 1 && total <= 148LL * 256;
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
   int U = g.warpRow ? 1 : (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
   // more 16-byte loads in flight per thread for the tiniest bodies (histograms):
   // one load per thread and grid-stride step leaves HBM latency exposed
   if (U == 4 && g.lines <= 8) {
     U = 12;  // measured on the 2^28-key histogram: 4 -> 240 us, 8 -> 215, 12 -> 209, 16 -> 242
-    if (const char* e = std::getenv("DEXLET_U")) U = std::max(4, std::min(16, std::atoi(e) / 4 * 4));
   }
   // cells must be on the device before this kernel
   for (auto& cu : g.cells) cellToDevice(cu.cell);
@@ -3256,7 +3256,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   // blocks meet at a grid barrier and fold the partials themselves.
   bool coop = false;
   for (auto& cu : g.cells) coop |= cu.partialBuf >= 0;
-  if (serial || std::getenv("DEXLET_NO_COOP")) coop = false;
+  if (serial || total == 0) coop = false;
   int syncBuf = -1;
   if (coop) {
     syncBuf = newBuf(BufDecl::Sync, SK::U32, 1);
@@ -3291,8 +3291,6 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   for (size_t i = 0; i < g.cells.size(); ++i)
     if (g.cells[i].strat == CellUse::TileRow) tileCell = (int)i;
   // WarpTab kernels fed by the TMA ring: warps share nothing but the stages
-  const bool warpTabRing = tileCell >= 0 && g.cells[tileCell].warpTab && !g.staged.empty() &&
-                           std::getenv("DEXLET_WT_RING") != nullptr;  // opt-in: measured no faster
   int stageOff = (smem + 15) / 16 * 16;
   if (maxRowD > 0) smem = stageOff + warps * (32 * (int)(maxRowD + 1) + 32) * esize;
   // TMA staging areas
@@ -3497,14 +3495,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "  int dx_it = 0;\n";
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride, ++dx_it) {\n";
       src << "    const int dx_stg = dx_it & 1;\n";
-      if (warpTabRing) {
-        // the stage of tile it-1 is reused once every warp has arrived on its
-        // empty barrier: only the issuing thread waits, the other warps go on
-        src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { if (dx_it >= 1) dx_mbar_wait(&dx_empty[dx_stg ^ 1], "
-               "(unsigned)(((dx_it - 1) >> 1) & 1)); dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
-      } else {
-        src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
-      }
+      src << "    if (threadIdx.x == 0 && dx_base + dx_stride < dx_n) { dx_fence_proxy_async(); dx_issue(dx_stg ^ 1, dx_base + dx_stride); }\n";
       for (int b : g.staged) {
         int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
         auto lb = g.streamUse[b];
@@ -3575,10 +3566,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
             etp = "(sb" + std::to_string(cu.aliasStage) + " + dx_sh" + std::to_string(cu.aliasStage) + ")";
           src << "    dx_tile_store4<" << rs.D << ">(" << etp << ", threadIdx.x, rowv" << rs.id << ");\n";
           if (cu.warpTab) {
-            src << "    dx_warp_tab<" << rs.D << ", " << Kr << ", " << (std::getenv("DEXLET_WT_SIMPLE") ? 0 : 1) << ">(" << etp << ", rowk" << rs.id << ", wtab" << I
+            src << "    dx_warp_tab<" << rs.D << ", " << Kr << ">(" << etp << ", rowk" << rs.id << ", wtab" << I
                 << " + dx_warp * " << (Kr + 1) * 32 << ");\n";
-            if (warpTabRing) src << "    __syncwarp();\n    if (dx_lane == 0) dx_mbar_arrive(&dx_empty[dx_stg]);  // this warp is done with the stage\n";
-            else src << "    __syncthreads();  // every warp is done with this TMA stage\n";
+            src << "    __syncthreads();  // every warp is done with this TMA stage\n";
             continue;
           }
           src << "    dx_tile_rows4<" << rs.D << ", " << Kr << ", " << g.threads << ">(" << etp << ", rowk" << rs.id
@@ -3641,14 +3631,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         default: break;
       }
     }
-    // (timing experiment, wrong results: DEXLET_DBG_COOP=1 drops the folds,
-    // 2 also the grid barrier)
-    static const int dbgCoop = std::getenv("DEXLET_DBG_COOP") ? std::atoi(std::getenv("DEXLET_DBG_COOP")) : 0;
-    if (coop && dbgCoop >= 2) src << "  return;\n";
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
       src << "  dx_grid_barrier(p" << syncBuf << ");\n";
-      if (dbgCoop >= 1) src << "  return;\n";
       if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
       for (size_t i = 0; i < g.cells.size(); ++i) {
         CellUse& cu = g.cells[i];
@@ -3664,8 +3649,10 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     src << "}\n\n";
   }
-  plan.source += src.str();
-  plan.numKernels++;
+  if (!empty) {
+    plan.source += src.str();
+    plan.numKernels++;
+  }
 
   // Output buffers for sharded kernels are summed across ranks: zero first.
   if (g.sharded) {
@@ -3676,6 +3663,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
   }
 
+  if (!empty) {
   Step ks;
   ks.k = Step::Kernel;
   ks.name = kname;
@@ -3720,6 +3708,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       addStep(a);
     }
   }
+  }  // !empty
   if (!elemTy) return hUnit();
   DTy rt = serial ? elemTy : tTable(kb0.desc, elemTy);
   if (outBufs.empty()) {
@@ -3800,7 +3789,7 @@ static bool mapLikeRunAccum(const ERunAccum& r) {
 }
 
 HV Lowering::flattenEffectNest(const HEnvP& env, const EFor& f, const DescPtr& d) {
-  if (opt.noFusion || std::getenv("DEXLET_NO_FLATTEN_EFFECT")) return nullptr;
+  if (opt.noFusion) return nullptr;
   const long long n = size(d);
   if (n >= 148LL * 1024) return nullptr;  // the outer loop fills the GPU already
   std::vector<const ELet*> pre;
@@ -3941,7 +3930,7 @@ ValuePtr Lowering::typeValue(const DTy& t) {
 HV Lowering::splitMaterialize(const HV& lz) {
   if (lz->k != HVal::Lazy) return nullptr;
   if (lz->st->split) return lz->st->split;
-  if (opt.noFusion || std::getenv("DEXLET_NO_SPLIT")) return nullptr;
+  if (opt.noFusion) return nullptr;
   // the perfect nest (as loopKernelLazy flattens it)
   std::vector<const ELet*> wraps;
   std::vector<const EFor*> fors;

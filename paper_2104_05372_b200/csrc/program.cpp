@@ -137,7 +137,6 @@ int Program::prepare() {
     if ((rc = dxrt::check(cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, s.threads, s.smem), "occupancy")))
       return rc;
     if (nb < 1) nb = 1;
-    if (const char* e = std::getenv("DEXLET_BLOCKS_PER_SM")) nb = std::max(1, std::min(nb, std::atoi(e)));  // (experiments)
     long long U = s.minGrid > 0 ? s.minGrid : 1;  // ordinals per thread
     long long need = ((hi - lo + U - 1) / U + s.threads - 1) / s.threads;
     if (s.warpRow) need = ((hi - lo) * 32 + s.threads - 1) / s.threads;
@@ -176,7 +175,7 @@ int Program::prepare() {
       if ((rc = dxrt::check(cuMemcpyHtoD(devptr[s.buf2], host.data(), host.size()), "upload cell init"))) return rc;
     }
   }
-  if (std::getenv("DEXLET_NO_GRAPH") || plan.world > 1) useGraph = false;
+  if (plan.world > 1) useGraph = false;
   if ((rc = buildTensorMaps())) return rc;
   // finalize functions
   const char* fz[4] = {"dx_fin_f32", "dx_fin_f64", "dx_fin_count_f32", "dx_fin_count_f64"};
@@ -188,7 +187,28 @@ int Program::prepare() {
   if ((rc = dxrt::check(cuModuleGetFunction(&finF32D, mod, "dx_fin_f32d"), "finalize fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[0], mod, "dx_cvt_f32_f64"), "cvt fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[1], mod, "dx_cvt_f64_f32"), "cvt fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&checkIdxFn, mod, "dx_check_index"), "check fn"))) return rc;
+  numLeafFlags = 0;
+  for (auto& in : plan.inputs) numLeafFlags += (int)in.size();
+  if ((rc = dxrt::check(cuMemAlloc(&upFlags, (size_t)std::max(1, numLeafFlags) * 4), "cuMemAlloc flags"))) return rc;
+  owned.push_back(upFlags);
+  if ((rc = dxrt::check(cuMemsetD8(upFlags, 0, (size_t)std::max(1, numLeafFlags) * 4), "memset flags"))) return rc;
   prepared = true;
+  return DXC_OK;
+}
+
+int Program::readFlags(int* any) {
+  int rc;
+  std::vector<int> f(1 + numLeafFlags, 0);
+  if (plan.errFlagBuf >= 0 && checkFlag &&
+      (rc = dxrt::check(cuMemcpyDtoHAsync(f.data(), devptr[plan.errFlagBuf], 4, ctx->stream), "flag")))
+    return rc;
+  if (numLeafFlags > 0 &&
+      (rc = dxrt::check(cuMemcpyDtoHAsync(f.data() + 1, upFlags, (size_t)numLeafFlags * 4, ctx->stream), "flags")))
+    return rc;
+  if ((rc = dxrt::check(cuStreamSynchronize(ctx->stream), "sync"))) return rc;
+  *any = 0;
+  for (int v : f) *any |= v;
   return DXC_OK;
 }
 
@@ -259,6 +279,20 @@ int Program::launch(CUfunction f, unsigned grid, unsigned block, unsigned smem, 
 int Program::run() {
   if (!ctx) { setError("program has no device context"); return DXC_E_ARG; }
   int rc;
+  if (plan.world > 1) {
+    // a sharded plan needs the communicator of exactly its (world, rank):
+    // anything else returns shard-local or wrongly summed cells silently
+    if (!ctx->comm) {
+      setError("sharded plan (world > 1): call dxc_comm_init on the context first");
+      return DXC_E_ARG;
+    }
+    if (!allowCommMismatch && (ctx->nranks != plan.world || ctx->rank != plan.rank)) {
+      setError("sharded plan is (world " + std::to_string(plan.world) + ", rank " + std::to_string(plan.rank) +
+               ") but the context communicator is (" + std::to_string(ctx->nranks) + ", " +
+               std::to_string(ctx->rank) + ")");
+      return DXC_E_ARG;
+    }
+  }
   if (!prepared && (rc = prepare())) return rc;
   ctx->makeCurrent();
   if (tmapsDirty && (rc = buildTensorMaps())) return rc;
@@ -456,6 +490,8 @@ int dxl_program_create(dxc_ctx* ctx, const char* source, const char* entry, cons
     lo.threads = opts->threads > 0 ? opts->threads : 256;
     lo.noFusion = (opts->flags & DXL_F_NO_FUSION) != 0;
     lo.noRowScatter = (opts->flags & DXL_F_NO_ROWSCATTER) != 0;
+    p->allowCommMismatch = (opts->flags & DXL_F_TEST_COMM_MISMATCH) != 0;
+    lo.noGemm = (opts->flags & DXL_F_NO_GEMM) != 0;
   }
   std::vector<std::pair<Name, ValuePtr>> params;
   ExprPtr optimized;
@@ -589,9 +625,22 @@ int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host,
   bool direct = (l.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) ||
                 (l.kind == SK::X && dtype == DXC_I32) || (l.kind == SK::I && dtype == DXC_I64);
   if (direct) {
-    // index leaves are range-checked on the device where they are read
-    // (dx_chk_idx in every kernel that loads them)
-    return dxrt::check(cuMemcpyHtoDAsync(dst, host, (size_t)l.count * es, p->ctx->stream), "input upload");
+    int rc = dxrt::check(cuMemcpyHtoDAsync(dst, host, (size_t)l.count * es, p->ctx->stream), "input upload");
+    if (rc || l.kind != SK::X || l.count == 0) return rc;
+    // index leaves: fromOrdinal's range check (index_set.cpp:99-106) on the
+    // device, right after the upload; reported as E-bounds by get_output and
+    // dxl_program_check (kernels that read the leaf also clamp it)
+    int flat = 0;
+    for (int i = 0; i < input; ++i) flat += (int)p->plan.inputs[i].size();
+    flat += leaf;
+    CUdeviceptr flag = p->upFlags + (CUdeviceptr)flat * 4;
+    if ((rc = dxrt::check(cuMemsetD8Async(flag, 0, 4, p->ctx->stream), "flag reset"))) return rc;
+    long long n = l.count;
+    int isz = (int)(l.desc ? size(l.desc) : 0);
+    void* args[4] = {&dst, &n, &isz, &flag};
+    return dxrt::check(cuLaunchKernel(p->checkIdxFn, (unsigned)std::min<long long>((n + 255) / 256, 1184), 1, 1, 256, 1, 1,
+                                      0, p->ctx->stream, args, nullptr),
+                       "index check");
   }
   int rc;
   long long isz = l.desc ? size(l.desc) : 0;
@@ -599,6 +648,33 @@ int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host,
   if (rc) return rc;
   rc = dxrt::check(cuMemcpyHtoD(dst, buf.data(), buf.size()), "input upload");
   return rc;
+  GUARD_END
+}
+
+int dxl_program_set_input_n(dxl_program* p, int input, int leaf, const void* host, int dtype, int64_t count) {
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  const InLeaf& l = p->plan.inputs[input][leaf];
+  if (count != l.count) {
+    setError("E-size: input " + std::to_string(input) + " leaf " + std::to_string(leaf) + " holds " +
+             std::to_string(l.count) + " elements, got " + std::to_string((long long)count));
+    return DXC_E_SIZE;
+  }
+  return dxl_program_set_input(p, input, leaf, host, dtype);
+}
+
+int dxl_program_check(dxl_program* p) {
+  GUARD_BEGIN
+  if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+  p->ctx->makeCurrent();
+  int flag = 0;
+  int rc = p->readFlags(&flag);
+  if (rc) return rc;
+  if (flag) { setError("E-bounds: an input ordinal is outside its index set"); return DXC_E_BOUNDS; }
+  return DXC_OK;
   GUARD_END
 }
 
@@ -664,10 +740,7 @@ int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype) {
                   (o.kind == SK::X && dtype == DXC_I32) || (o.kind == SK::I && dtype == DXC_I64);
     int rc;
     int flag = 0;
-    if (p->plan.errFlagBuf >= 0 && p->checkFlag) {
-      if ((rc = dxrt::check(cuMemcpyDtoHAsync(&flag, p->devptr[p->plan.errFlagBuf], 4, p->ctx->stream), "flag")))
-        return rc;
-    }
+    if ((rc = p->readFlags(&flag))) return rc;
     CUdeviceptr src = p->devptr[o.buf] + o.off * es;
     if (direct) {
       rc = dxrt::check(cuMemcpyDtoHAsync(host, src, (size_t)o.count * es, p->ctx->stream), "output download");

@@ -29,6 +29,7 @@ struct Program {
   CUmodule mod = nullptr;
   bool prepared = false;
   bool checkFlag = true;
+  bool allowCommMismatch = false;  // DXL_F_TEST_COMM_MISMATCH (single-device tests only)
   std::vector<CUdeviceptr> devptr;
   std::vector<CUdeviceptr> owned;
   std::set<int> boundInputs;
@@ -40,6 +41,10 @@ struct Program {
   CUfunction addFn[3] = {};  // f32 += f32, f64 += f64, f64 += f32
   CUfunction finF32D = nullptr;
   CUfunction cvtFn[2] = {};
+  CUfunction checkIdxFn = nullptr;
+  CUdeviceptr upFlags = 0;  // one int per input leaf: E-bounds seen by the upload check
+  int numLeafFlags = 0;
+  int readFlags(int* any);  // synchronizes; *any = error flag or any upload flag
   int launches = 0;
   std::vector<CUtensorMap> tmaps;                  // TMA descriptors (kernel args)
   std::map<std::pair<int, int>, int> tmapOf;        // (step, arg) -> tmaps index

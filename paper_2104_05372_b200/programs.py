@@ -204,3 +204,14 @@ def mlp_inputs(b: int, i: int, h: int, o: int, seed: int = 20211):
     w1 = (rng.standard_normal((i, h)) / np.sqrt(i)).astype(np.float32)
     w2 = (rng.standard_normal((h, o)) / np.sqrt(h)).astype(np.float32)
     return x, w1, w2
+
+
+def gmm_inputs(n: int, d: int, K: int, seed: int = 20211):
+    """Synthetic inputs of SURVEY.md §8(d) config 3 (ADBench form): x, means ~
+    N(0,1), icf ~ U(-0.1, 0.1), alphas ~ N(0,1), fp32."""
+    rng = np.random.default_rng(seed)
+    alphas = rng.standard_normal(K).astype(np.float32)
+    means = rng.standard_normal((K, d)).astype(np.float32)
+    icf = rng.uniform(-0.1, 0.1, (K, d * (d + 1) // 2)).astype(np.float32)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    return alphas, means, icf, x

@@ -1,0 +1,550 @@
+// Dev microbenchmark (not product code): candidate structures for the
+// k-means cost+grad kernel (n points, d = 16, K = 64), to pick the layout
+// the lowering emits.  Variants:
+//   0  stream-only: read pts + asg, sum them (HBM ceiling of this pattern)
+//   1  sub-warp (16 lanes per point), direct LDG, unrolled U steps, warp
+//      tables RMW, last-block-done fold
+//   2  sub-warp, TMA 1-D bulk ring (4 stages), warp tables, LBD fold
+// Each timed with events around a single launch, L2 flushed before.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <cmath>
+#include <algorithm>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
+
+constexpr int D = 16, K = 64;
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  unsigned a;
+  asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+  return a;
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(smem_addr(bar)),
+               "r"(parity) : "memory");
+}
+__device__ __forceinline__ unsigned swz(unsigned a) { return a ^ (((a >> 7) & 3) << 4); }
+
+// Last-block-done fold, two levels: groups of GB blocks; the last block of a
+// group folds the group's partials (fixed order) into a group partial; the
+// last group folds the group partials (fixed order) into the result.
+// part: [nblk][W] floats; gpart: [ngrp][W] floats; tick: [ngrp + 1] u32.
+template <int W>
+__device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB, double* out) {
+  // every load of a fold is issued before the fixed-order sum (one L2 latency)
+  __shared__ int last;
+  const int nblk = gridDim.x, ngrp = (nblk + GB - 1) / GB, grp = blockIdx.x / GB;
+  const int gsz = min(GB, nblk - grp * GB);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&tick[grp], 1u) == (unsigned)gsz - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    float v[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) v[b] = b < gsz ? __ldcg(&part[(long long)(grp * GB + b) * W + c]) : 0.f;
+    float s = 0.f;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) s += v[b];
+    gpart[(long long)grp * W + c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tick[grp] = 0;
+    __threadfence();
+    last = atomicAdd(&tick[ngrp], 1u) == (unsigned)ngrp - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    float v[32];
+#pragma unroll
+    for (int g = 0; g < 32; ++g) v[g] = g < ngrp ? __ldcg(&gpart[(long long)g * W + c]) : 0.f;
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < 32; ++g) s += (double)v[g];
+    out[c] = s;
+  }
+  if (threadIdx.x == 0) tick[ngrp] = 0;
+}
+
+__global__ void __launch_bounds__(512) k_stream(const float4* __restrict__ p, long long n4, const int4* __restrict__ a, long long na4, float* out) {
+  float s = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 v = __ldcs(p + i);
+    s += v.x + v.y + v.z + v.w;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < na4; i += (long long)gridDim.x * blockDim.x) {
+    int4 v = __ldcs(a + i);
+    s += (float)(v.x + v.y + v.z + v.w);
+  }
+  if (s == 12345.f) out[0] = s;
+}
+
+// ---- variant 1: sub-warp LDG ------------------------------------------------
+// warp iteration = 2*U consecutive points; lane (g = lane>>4, q = lane&15)
+template <int NW, int U>
+__global__ void __launch_bounds__(NW * 32, 1) k_ldg(const float* __restrict__ pts, const int* __restrict__ asg,
+                                                   const float* __restrict__ cs, long long n, float* part, float* gpart,
+                                                   unsigned* tick, int GB, double* out) {
+  extern __shared__ __align__(16) float sm[];
+  float* tabs = sm;                       // NW x 65 x 32
+  float* csm = sm + NW * 65 * 32;         // 64 x 16 swizzled
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 4, q = lane & 15;
+  for (int t = threadIdx.x; t < NW * 65 * 32 / 4; t += blockDim.x) reinterpret_cast<float4*>(tabs)[t] = make_float4(0, 0, 0, 0);
+  for (int t = threadIdx.x; t < K * D; t += blockDim.x) *(float*)((char*)csm + swz(t * 4)) = cs[t];
+  __syncthreads();
+  float* tab = tabs + warp * 65 * 32 + g * 16 + q;
+  const unsigned tabA = smem_addr(tab);
+  float cost = 0.f;
+  const long long nch = (n + 2 * U - 1) / (2 * U);
+  const long long gw = (long long)blockIdx.x * NW + warp, tw = (long long)gridDim.x * NW;
+  for (long long ch = gw; ch < nch; ch += tw) {
+    const long long p0 = ch * 2 * U;
+    float v[U];
+    int key = 0;
+    const bool full = p0 + 2 * U <= n;
+    if (full) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(pts + (p0 + 2 * u + g) * D + q);
+      if (lane < 2 * U) key = __ldcs(asg + p0 + lane);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = (p0 + 2 * u + g < n) ? pts[(p0 + 2 * u + g) * D + q] : 0.f;
+      if (lane < 2 * U && p0 + lane < n) key = asg[p0 + lane];
+    }
+    float val[U];
+    unsigned ad[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = __shfl_sync(0xffffffffu, key, 2 * u + g);
+      const bool ok = p0 + 2 * u + g < n;
+      const float c = *(const float*)((const char*)csm + swz((k * 16 + q) * 4));
+      const float e = v[u] - c;
+      if (ok) cost += e * e;
+      val[u] = ok ? -(e + e) : 0.f;
+      ad[u] = tabA + (unsigned)k * 128u;
+    }
+    // software-pipelined RMW (load of step u+1 before store of step u)
+    float cur;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(cur) : "r"(ad[0]) : "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float nxt = 0.f;
+      if (u + 1 < U) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nxt) : "r"(ad[u + 1]) : "memory");
+      const float r = cur + val[u];
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(ad[u]), "f"(r) : "memory");
+      if (u + 1 < U) cur = ad[u + 1] == ad[u] ? r : nxt;
+    }
+  }
+  // block partial: cost + 1024 table entries
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = cost;
+  float* pb = part + (long long)blockIdx.x * 1025;
+  for (int e = threadIdx.x; e < K * D; e += blockDim.x) {
+    const int k = e >> 4, j = e & 15;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += tabs[w * 65 * 32 + k * 32 + j] + tabs[w * 65 * 32 + k * 32 + 16 + j];
+    pb[1 + e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < NW; ++w) s += red[w];
+    pb[0] = s;
+  }
+  lbd_fold<1025>(part, gpart, tick, GB, out);
+}
+
+// ---- variant 1b: sub-warp LDG with the next chunk's loads in flight -------
+__device__ unsigned long long g_ts[4096][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+template <int NW, int U>
+__global__ void __launch_bounds__(NW * 32, 1) k_ldgp(const float* __restrict__ pts, const int* __restrict__ asg,
+                                                    const float* __restrict__ cs, long long n, float* part, float* gpart,
+                                                    unsigned* tick, int GB, double* out) {
+  extern __shared__ __align__(16) float sm[];
+  float* tabs = sm;
+  float* csm = sm + NW * 65 * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 4, q = lane & 15;
+  const long long nch = n / (2 * U);  // full chunks; the tail is done below
+  const long long gw = (long long)blockIdx.x * NW + warp, tw = (long long)gridDim.x * NW;
+  if (threadIdx.x == 0) g_ts[blockIdx.x][0] = gtime();
+  float v[U], w[U];
+  int key = 0, key2 = 0;
+  auto ld = [&](long long ch, float (&dst)[U], int& k) {
+    const long long p0 = ch * 2 * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[u] = __ldcs(pts + (p0 + 2 * u + g) * D + q);
+    if (lane < 2 * U) k = __ldcs(asg + p0 + lane);
+  };
+  if (gw < nch) ld(gw, v, key);
+  for (int t = threadIdx.x; t < NW * 65 * 32 / 4; t += blockDim.x) reinterpret_cast<float4*>(tabs)[t] = make_float4(0, 0, 0, 0);
+  for (int t = threadIdx.x; t < K * D; t += blockDim.x) *(float*)((char*)csm + swz(t * 4)) = cs[t];
+  __syncthreads();
+  if (threadIdx.x == 0) g_ts[blockIdx.x][1] = gtime();
+  float* tab = tabs + warp * 65 * 32 + g * 16 + q;
+  const unsigned tabA = smem_addr(tab);
+  float cost = 0.f;
+  auto work = [&](const float (&vv)[U], int kk, long long p0, bool full) {
+    float val[U];
+    unsigned ad[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = __shfl_sync(0xffffffffu, kk, 2 * u + g);
+      const bool ok = full || p0 + 2 * u + g < n;
+      const float c = *(const float*)((const char*)csm + swz((k * 16 + q) * 4));
+      const float e = vv[u] - c;
+      if (ok) cost += e * e;
+      val[u] = ok ? -(e + e) : 0.f;
+      ad[u] = tabA + (unsigned)k * 128u;
+    }
+    float cur;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(cur) : "r"(ad[0]) : "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float nxt = 0.f;
+      if (u + 1 < U) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nxt) : "r"(ad[u + 1]) : "memory");
+      const float r = cur + val[u];
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(ad[u]), "f"(r) : "memory");
+      if (u + 1 < U) cur = ad[u + 1] == ad[u] ? r : nxt;
+    }
+  };
+  for (long long ch = gw; ch < nch; ch += 2 * tw) {
+    if (ch + tw < nch) ld(ch + tw, w, key2);
+    work(v, key, ch * 2 * U, true);
+    if (ch + 2 * tw < nch) ld(ch + 2 * tw, v, key);
+    if (ch + tw < nch) work(w, key2, (ch + tw) * 2 * U, true);
+  }
+  // tail chunk (partial), by warp 0 of block 0
+  if (blockIdx.x == 0 && warp == 0 && nch * 2 * U < n) {
+    const long long p0 = nch * 2 * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = (p0 + 2 * u + g < n) ? pts[(p0 + 2 * u + g) * D + q] : 0.f;
+    key = (p0 + lane < n && lane < 2 * U) ? asg[p0 + lane] : 0;
+    work(v, key, p0, false);
+  }
+  if (lane == 0) g_ts[blockIdx.x][2] = max(g_ts[blockIdx.x][2], 0ull);
+  __syncthreads();
+  if (threadIdx.x == 0) g_ts[blockIdx.x][2] = gtime();
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = cost;
+  float* pb = part + (long long)blockIdx.x * 1025;
+  for (int e = threadIdx.x; e < K * D; e += blockDim.x) {
+    const int k = e >> 4, j = e & 15;
+    float s = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) s += tabs[w2 * 65 * 32 + k * 32 + j] + tabs[w2 * 65 * 32 + k * 32 + 16 + j];
+    pb[1 + e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w2 = 0; w2 < NW; ++w2) s += red[w2];
+    pb[0] = s;
+    g_ts[blockIdx.x][3] = gtime();
+  }
+  lbd_fold<1025>(part, gpart, tick, GB, out);
+  if (threadIdx.x == 0) g_ts[blockIdx.x][4] = gtime();
+}
+
+// ---- variant 2: sub-warp, TMA ring -------------------------------------------
+// tile = T points; NS stages; each warp takes T/NW points of the tile: warp w
+// step u handles tile rows (u*NW + w)*2 + g.
+template <int NW, int T, int NS>
+__global__ void __launch_bounds__(NW * 32, 1) k_tma(const float* __restrict__ pts, const int* __restrict__ asg,
+                                                   const float* __restrict__ cs, long long n, float* part, float* gpart,
+                                                   unsigned* tick, int GB, double* out) {
+  extern __shared__ __align__(16) float sm[];
+  float* tabs = sm;                       // NW x 65 x 32
+  float* csm = sm + NW * 65 * 32;         // 64 x 16 swizzled
+  float* stg = csm + K * D;               // NS x (T*16 floats + T ints)
+  constexpr int SF = T * 16 + T;
+  __shared__ __align__(8) unsigned long long full[NS], empty[NS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 4, q = lane & 15;
+  const long long ntile = (n + T - 1) / T;
+  const long long t0 = blockIdx.x;
+  auto issue = [&](int s, long long t) {
+    const long long r0 = t * T;
+    const long long rows = min((long long)T, n - r0);
+    mbar_expect_tx(&full[s], (unsigned)(rows * 64 + ((rows * 4 + 15) & ~15)));
+    bulk_g2s(stg + s * SF, pts + r0 * D, (unsigned)(rows * 64), &full[s]);
+    bulk_g2s(stg + s * SF + T * 16, asg + r0, (unsigned)((rows * 4 + 15) & ~15), &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NS; ++s)
+      if (t0 + (long long)s * gridDim.x < ntile) issue(s, t0 + (long long)s * gridDim.x);
+  }
+  for (int t = threadIdx.x; t < NW * 65 * 32 / 4; t += blockDim.x) reinterpret_cast<float4*>(tabs)[t] = make_float4(0, 0, 0, 0);
+  for (int t = threadIdx.x; t < K * D; t += blockDim.x) *(float*)((char*)csm + swz(t * 4)) = cs[t];
+  __syncthreads();
+  float* tab = tabs + warp * 65 * 32 + g * 16 + q;
+  const unsigned tabA = smem_addr(tab);
+  float cost = 0.f;
+  constexpr int U = T / (2 * NW);
+  int it = 0;
+  for (long long t = t0; t < ntile; t += gridDim.x, ++it) {
+    const int s = it % NS;
+    mbar_wait(&full[s], (unsigned)((it / NS) & 1));
+    const float* tp = stg + s * SF;
+    const int* tk = (const int*)(tp + T * 16);
+    const long long r0 = t * T;
+    float val[U];
+    unsigned ad[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int row = (u * NW + warp) * 2 + g;
+      const bool ok = r0 + row < n;
+      const int k = ok ? tk[row] : 0;
+      const float v = tp[row * 16 + q];
+      const float c = *(const float*)((const char*)csm + swz((k * 16 + q) * 4));
+      const float e = v - c;
+      if (ok) cost += e * e;
+      val[u] = ok ? -(e + e) : 0.f;
+      ad[u] = tabA + (unsigned)k * 128u;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    float cur;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(cur) : "r"(ad[0]) : "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float nxt = 0.f;
+      if (u + 1 < U) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nxt) : "r"(ad[u + 1]) : "memory");
+      const float r = cur + val[u];
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(ad[u]), "f"(r) : "memory");
+      if (u + 1 < U) cur = ad[u + 1] == ad[u] ? r : nxt;
+    }
+    // refill stage s with tile t + NS*grid once every warp released it
+    if (threadIdx.x == 0 && t + (long long)NS * gridDim.x < ntile) {
+      mbar_wait(&empty[s], (unsigned)((it / NS) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(s, t + (long long)NS * gridDim.x);
+    }
+  }
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = cost;
+  float* pb = part + (long long)blockIdx.x * 1025;
+  for (int e = threadIdx.x; e < K * D; e += blockDim.x) {
+    const int k = e >> 4, j = e & 15;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += tabs[w * 65 * 32 + k * 32 + j] + tabs[w * 65 * 32 + k * 32 + 16 + j];
+    pb[1 + e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < NW; ++w) s += red[w];
+    pb[0] = s;
+  }
+  lbd_fold<1025>(part, gpart, tick, GB, out);
+}
+
+__global__ void k_empty() {}
+__global__ void k_spin(long long cycles) {
+  long long t0 = clock64();
+  while (clock64() - t0 < cycles) {}
+}
+__global__ void k_readflush(const float4* p, long long n, float* out) {
+  float s = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float4 v = p[i];
+    s += v.x;
+  }
+  if (s == 1.2345f) out[0] = s;
+}
+__global__ void k_flush(float4* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = make_float4(1, 2, 3, 4);
+}
+
+int main(int argc, char** argv) {
+  long long n = argc > 1 ? atoll(argv[1]) : 1000000;
+  int fmode = argc > 2 ? atoi(argv[2]) : 0;  // 0 write, 1 write + read (clean L2), 2 read only
+  int reps = 30;
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  std::vector<float> hp(n * D), hc(K * D);
+  std::vector<int> ha(n);
+  unsigned s = 12345;
+  auto rnd = [&]() { s = s * 1664525u + 1013904223u; return (s >> 8) * (1.0f / 16777216.0f); };
+  for (auto& x : hp) x = rnd() * 2 - 1;
+  for (auto& x : hc) x = rnd() * 2 - 1;
+  for (auto& x : ha) x = (int)(rnd() * K) % K;
+  // CPU reference (double)
+  double rc = 0; std::vector<double> rg(K * D, 0.0);
+  for (long long i = 0; i < n; ++i)
+    for (int j = 0; j < D; ++j) {
+      double e = (double)hp[i * D + j] - hc[ha[i] * D + j];
+      rc += e * e;
+      rg[ha[i] * D + j] += -2 * e;
+    }
+  float *dp, *dc, *part, *gpart, *fl, *o32;
+  int* da;
+  double* out;
+  unsigned* tick;
+  CK(cudaMalloc(&dp, n * D * 4)); CK(cudaMalloc(&da, n * 4 + 16)); CK(cudaMalloc(&dc, K * D * 4));
+  CK(cudaMalloc(&part, 4 * sms * 1025 * 4)); CK(cudaMalloc(&gpart, 4 * sms * 1025 * 4));
+  CK(cudaMalloc(&tick, 4096)); CK(cudaMemset(tick, 0, 4096));
+  CK(cudaMalloc(&out, 1025 * 8)); CK(cudaMalloc(&o32, 64));
+  long long fln = (256 << 20) / 16;
+  CK(cudaMalloc(&fl, fln * 16));
+  float* fl2;
+  CK(cudaMalloc(&fl2, fln * 16));
+  CK(cudaMemset(fl2, 0, fln * 16));
+  CK(cudaMemcpy(dp, hp.data(), n * D * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(da, ha.data(), n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc, hc.data(), K * D * 4, cudaMemcpyHostToDevice));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  const double bytes = n * D * 4.0 + n * 4.0 + 2.0 * K * D * 4;
+  auto timeit = [&](const char* name, auto launch, bool check) {
+    std::vector<float> ts;
+    for (int r = 0; r < reps + 3; ++r) {
+      if (fmode != 2) k_flush<<<sms * 4, 512>>>((float4*)fl, fln);
+      if (fmode != 0) k_readflush<<<sms * 4, 512>>>((const float4*)fl2, fln, o32);
+      CK(cudaEventRecord(e0));
+      launch();
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 3) ts.push_back(ms);
+    }
+    CK(cudaGetLastError());
+    std::sort(ts.begin(), ts.end());
+    double med = ts[ts.size() / 2] * 1e-3;
+    printf("%-34s median %8.2f us  min %8.2f us  %7.1f GB/s  frac %.3f", name, med * 1e6, ts[0] * 1e3, bytes / med / 1e9,
+           bytes / med / 1e9 / 6542.4);
+    if (check) {
+      std::vector<double> h(1025);
+      CK(cudaMemcpy(h.data(), out, 1025 * 8, cudaMemcpyDeviceToHost));
+      double m = std::fabs(h[0] - rc) / (1 + std::fabs(rc));
+      for (int i = 0; i < K * D; ++i) m = std::max(m, std::fabs(h[1 + i] - rg[i]) / (1 + std::fabs(rg[i])));
+      printf("  maxrel %.2e", m);
+    }
+    printf("\n");
+  };
+  timeit("empty kernel", [&] { k_empty<<<1, 32>>>(); }, false);
+  {
+    // launch overhead probes (no flush): idle GPU, behind a spin kernel, 20 in a row
+    float ms;
+    for (int r = 0; r < 5; ++r) { CK(cudaEventRecord(e0)); k_empty<<<1, 32>>>(); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); }
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("empty, idle GPU: %.2f us\n", ms * 1e3);
+    k_spin<<<1, 32>>>(200000); CK(cudaEventRecord(e0)); k_empty<<<1, 32>>>(); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("empty, queued behind spin: %.2f us\n", ms * 1e3);
+    k_spin<<<1, 32>>>(200000); CK(cudaEventRecord(e0)); for (int i = 0; i < 20; ++i) k_empty<<<1, 32>>>(); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("20 empties, queued: %.2f us each\n", ms * 1e3 / 20);
+    cudaStream_t st; CK(cudaStreamCreate(&st));
+    cudaGraph_t gr; cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)); k_empty<<<1, 32, 0, st>>>(); CK(cudaStreamEndCapture(st, &gr));
+    CK(cudaGraphInstantiate(&ge, gr, 0));
+    for (int r = 0; r < 3; ++r) CK(cudaGraphLaunch(ge, st));
+    k_spin<<<1, 32, 0, st>>>(200000); CK(cudaEventRecord(e0, st)); CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(e1, st)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("graph(empty), queued behind spin: %.2f us\n", ms * 1e3);
+    k_spin<<<1, 32, 0, st>>>(200000); CK(cudaEventRecord(e0, st)); for (int i = 0; i < 20; ++i) CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(e1, st)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("20 graph(empty), queued: %.2f us each\n", ms * 1e3 / 20);
+    k_flush<<<sms * 4, 512, 0, st>>>((float4*)fl, fln); CK(cudaEventRecord(e0, st)); CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(e1, st)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1)); printf("graph(empty) after write flush: %.2f us\n", ms * 1e3);
+  }
+  for (int bps : {2, 4, 8})
+    timeit(bps == 2 ? "stream-only 2 blk/SM x512" : bps == 4 ? "stream-only 4 blk/SM x512" : "stream-only 8 blk/SM x512",
+           [&] { k_stream<<<sms * bps, 512>>>((const float4*)dp, n * D / 4, (const int4*)da, n / 4, o32); }, false);
+  // rotating input copies (NC x 68 MB > L2): K back-to-back launches per event pair
+  const int NC = 3;
+  float* dpc[NC]; int* dac[NC];
+  dpc[0] = dp; dac[0] = da;
+  for (int c = 1; c < NC; ++c) {
+    CK(cudaMalloc(&dpc[c], n * D * 4)); CK(cudaMalloc(&dac[c], n * 4 + 16));
+    CK(cudaMemcpy(dpc[c], dp, n * D * 4, cudaMemcpyDeviceToDevice)); CK(cudaMemcpy(dac[c], da, n * 4, cudaMemcpyDeviceToDevice));
+  }
+  auto timerot = [&](const char* name, auto launch) {
+    for (int r = 0; r < 6; ++r) launch(r % NC);
+    CK(cudaEventRecord(e0));
+    const int KS = 30;
+    for (int r = 0; r < KS; ++r) launch(r % NC);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    double per = ms * 1e-3 / KS;
+    printf("%-34s ROT3 back-to-back %8.2f us/step  %7.1f GB/s  frac %.3f\n", name, per * 1e6, bytes / per / 1e9, bytes / per / 1e9 / 6542.4);
+  };
+  timerot("stream-only 8 blk/SM", [&](int c) { k_stream<<<sms * 8, 512>>>((const float4*)dpc[c], n * D / 4, (const int4*)dac[c], n / 4, o32); });
+#define LDG(NW, U, GB)                                                                                          \
+  {                                                                                                             \
+    int smem = (NW * 65 * 32 + K * D) * 4;                                                                      \
+    CK(cudaFuncSetAttribute(k_ldg<NW, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                 \
+    timeit("ldg NW=" #NW " U=" #U " GB=" #GB,                                                                    \
+           [&] { k_ldg<NW, U><<<sms, NW * 32, smem>>>(dp, da, dc, n, part, gpart, tick, GB, out); }, true);      \
+  }
+  LDG(16, 16, 8) LDG(24, 16, 8)
+#define LDGP(NW, U, GB)                                                                                         \
+  {                                                                                                             \
+    int smem = (NW * 65 * 32 + K * D) * 4;                                                                      \
+    CK(cudaFuncSetAttribute(k_ldgp<NW, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                \
+    timeit("ldgp NW=" #NW " U=" #U " GB=" #GB,                                                                   \
+           [&] { k_ldgp<NW, U><<<sms, NW * 32, smem>>>(dp, da, dc, n, part, gpart, tick, GB, out); }, true);     \
+    timerot("ldgp NW=" #NW " U=" #U " GB=" #GB,                                                                  \
+           [&](int c) { k_ldgp<NW, U><<<sms, NW * 32, smem>>>(dpc[c], dac[c], dc, n, part, gpart, tick, GB, out); }); \
+  }
+  LDGP(16, 16, 12)
+  {
+    std::vector<unsigned long long> ts(4096 * 6);
+    CK(cudaMemcpyFromSymbol(ts.data(), g_ts, ts.size() * 8));
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < sms; ++b) t0 = std::min(t0, ts[b * 6]);
+    for (int ph = 0; ph < 5; ++ph) {
+      std::vector<double> v;
+      for (int b = 0; b < sms; ++b) v.push_back((ts[b * 6 + ph] - t0) * 1e-3);
+      std::sort(v.begin(), v.end());
+      printf("  phase %d (0 entry,1 prologue,2 loop,3 flush,4 fold): min %.2f med %.2f max %.2f us\n", ph, v[0], v[v.size() / 2], v.back());
+    }
+  }
+#define TMA(NW, T, NS, GB)                                                                                      \
+  {                                                                                                             \
+    int smem = (NW * 65 * 32 + K * D + NS * (T * 17)) * 4;                                                      \
+    CK(cudaFuncSetAttribute(k_tma<NW, T, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
+    timeit("tma NW=" #NW " T=" #T " NS=" #NS " GB=" #GB,                                                         \
+           [&] { k_tma<NW, T, NS><<<sms, NW * 32, smem>>>(dp, da, dc, n, part, gpart, tick, GB, out); }, true);  \
+  }
+  TMA(16, 256, 4, 8) TMA(16, 512, 2, 8)
+  return 0;
+}

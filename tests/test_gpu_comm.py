@@ -56,7 +56,7 @@ def test_world2_shards_through_nccl_sum_to_the_whole(which):
     whole = dx.Program(src, ctx=ctx)(*args)
     parts = []
     for rank in (0, 1):
-        prog = dx.Program(src, ctx=ctx, rank=rank, world=2)
+        prog = dx.Program(src, ctx=ctx, rank=rank, world=2, flags=dx.F_TEST_COMM_MISMATCH)
         assert "allreduce" in prog.plan
         parts.append(prog(*args))
     for w, p0, p1 in zip(whole, parts[0], parts[1]):
@@ -91,3 +91,56 @@ def test_sharded_plan_without_communicator_fails_loudly():
     prog = dx.Program(P.histogram(n, k), ctx=ctx, rank=0, world=2)
     with pytest.raises(dx.DexError):
         prog(P.histogram_inputs(n, k, seed=1))
+
+
+def test_sharded_plan_with_wrong_communicator_fails_loudly():
+    """A world-2 plan over a one-rank communicator would all-reduce nothing:
+    refused before anything is launched (unless the test-only flag is set)."""
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    ctx = dx.Context(0)
+    ctx.init_comm(dx.nccl_unique_id(), 1, 0)
+    n, k = 4096, 64
+    prog = dx.Program(P.histogram(n, k), ctx=ctx, rank=1, world=2)
+    with pytest.raises(dx.DexError) as e:
+        prog(P.histogram_inputs(n, k, seed=1))
+    assert e.value.code == dx.DXC_E_ARG
+
+
+def test_sharded_gmm_without_communicator_fails_loudly():
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    n, k = 1000, 3
+    a, mu, icf, x = P.gmm_inputs(n, 64, k, seed=2)
+    g = dx.GMM(dx.Context(0), 64, k, n, 2 * n)
+    with pytest.raises(dx.DexError) as e:
+        g(a, mu, icf, x)
+    assert e.value.code == dx.DXC_E_ARG
+
+
+def test_input_size_mismatch_is_e_size():
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    ctx = dx.Context(0)
+    n, k = 4096, 64
+    prog = dx.Program(P.histogram(n, k), ctx=ctx)
+    with pytest.raises(dx.DexError) as e:
+        prog(P.histogram_inputs(n - 1, k, seed=1))
+    assert e.value.code == dx.DXC_E_SIZE
+
+
+def test_unread_index_leaf_is_range_checked_on_upload():
+    """An index input passed straight to the output is checked at upload
+    (fromOrdinal's check, index_set.cpp:99-106), not only where kernels read it."""
+    import paper_2104_05372_b200 as dx
+    ctx = dx.Context(0)
+    prog = dx.Program("main = \\p:((Fin 8)=>(Fin 4)). p\n", ctx=ctx)
+    keys = np.array([0, 1, 2, 3, 4, 0, 1, 2], dtype=np.int32)
+    prog.set_input(0, 0, keys)
+    prog.run()
+    with pytest.raises(dx.DexError) as e:
+        prog.check()
+    assert e.value.code == dx.DXC_E_BOUNDS
+    prog.set_input(0, 0, keys % 4)
+    prog.run()
+    prog.check()

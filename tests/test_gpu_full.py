@@ -90,6 +90,62 @@ def test_matmul_256_fwd_grad(ctx):
     assert oracle.rel_diff(gx, rg.ravel()) <= 1e-4
 
 
+# Elementwise bar for the f32 MLP gradients at the BASELINE size.  Measured
+# control (scripts/fp32_control.py, profiles/r02_fp32_control.txt): numpy
+# float32 with BLAS sgemm reaches rtMaxRelDiff 2.55e-3 (dW1) / 8.8e-4 (dW2)
+# against the fp64 restatement; even fp32 storage of z, h, y, dz with exactly
+# accumulated GEMMs gives 3.7e-4 (dW1).  The gradients' smallest entries
+# (~0.1) are differences of 8192 terms whose sum magnitude is ~1e3-1e4, so
+# the reference's 1e-4 elementwise bar is out of reach of any fp32 pipeline
+# at this size; the f32 path is held to 2x the sgemm control elementwise and
+# to 1e-5 normwise, and the f64 parity mode (below) meets 1e-4 (in fact 1e-9).
+MLP_F32_ELEMWISE = 5e-3
+MLP_F32_NORMWISE = 1e-5
+
+
+def _normrel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def test_mlp_full_size_f32(ctx):
+    """BASELINE configs[4]: batch 8192, 1024^3, square activation (tcgen05 3xTF32 GEMMs)."""
+    b, i, h, o = 8192, 1024, 1024, 1024
+    x, w1, w2 = P.mlp_inputs(b, i, h, o)
+    prog = dx.Program(P.mlp_grad(b, i, h, o), ctx=ctx)
+    assert "tcgen05 gemm" in prog.plan
+    loss, d1, d2 = prog(x, [w1, w2])
+    rl, r1, r2 = restate.mlp_grad(x, w1, w2)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-4
+    for got, want in ((d1, r1), (d2, r2)):
+        assert _normrel(got, want) <= MLP_F32_NORMWISE
+        assert oracle.rel_diff(got, want.ravel()) <= MLP_F32_ELEMWISE
+
+
+def test_mlp_full_size_f64_mode(ctx):
+    """The same program in the f64 parity mode (float64=True: f64 GEMMs and
+    f64 intermediates, as the reference evaluates) meets the reference's
+    elementwise 1e-4 at the full BASELINE size -- held here to 1e-9."""
+    b, i, h, o = 8192, 1024, 1024, 1024
+    x, w1, w2 = P.mlp_inputs(b, i, h, o)
+    prog = dx.Program(P.mlp_grad(b, i, h, o), ctx=ctx, float64=True)
+    assert "f64 gemm" in prog.plan
+    loss, d1, d2 = prog(x, [w1, w2])
+    rl, r1, r2 = restate.mlp_grad(x, w1, w2)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-9
+    assert oracle.rel_diff(d1, r1.ravel()) <= 1e-9
+    assert oracle.rel_diff(d2, r2.ravel()) <= 1e-9
+
+
+def test_matmul_256_f64_mode(ctx):
+    x, y = P.matmul_inputs(256)
+    loss, gx = dx.Program(P.matmul_grad(256), ctx=ctx, float64=True)(x, y)
+    rl, rg = restate.matmul_grad(x, y)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-9
+    assert oracle.rel_diff(gx, rg.ravel()) <= 1e-9
+
+
 def test_mlp_small_width(ctx):
     x, w1, w2 = P.mlp_inputs(256, 64, 64, 32)
     loss, d1, d2 = dx.Program(P.mlp_grad(256, 64, 64, 32), ctx=ctx)(x, [w1, w2])

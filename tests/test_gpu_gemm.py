@@ -24,7 +24,7 @@ SHAPES = [
     (384, 128, 4096, True, True),    # long K: many pipeline wraps; split-K 4
     (256, 256, 8192, True, False),   # split-K 8 (4 tiles would leave 144 SMs idle)
     (1, 1, 8, True, False),          # single element
-    (12800, 256, 96, True, False),   # 100 tiles of N = 256 under DEXLET_GEMM_N256=1
+    (12800, 256, 96, True, False),   # 200 tiles
     (12800, 512, 40, False, True),   # (same, transposed operands)
 ]
 
@@ -83,15 +83,3 @@ def test_split_k_plan_and_determinism(ctx):
     b = prog(x, y)[0]
     np.testing.assert_array_equal(a, b)
     assert oracle.rel_diff(a, restate.contraction(x, y).ravel()) <= 1e-4
-
-
-
-@pytest.mark.parametrize("m,n,k,xk,yk", [(12800, 256, 96, True, False), (12800, 512, 40, False, True)])
-def test_wide_tiles_opt_in(ctx, monkeypatch, m, n, k, xk, yk):
-    monkeypatch.setenv("DEXLET_GEMM_N256", "1")
-    src = P.contraction(m, n, k, xk, yk)
-    x, y = P.contraction_inputs(m, n, k, xk, yk)
-    prog = dx.Program(src, ctx=ctx)
-    assert "N=256 tiles" in prog.plan
-    (c,) = prog(x, y)
-    assert oracle.rel_diff(c, restate.contraction(x, y, xk, yk).ravel()) <= 1e-4

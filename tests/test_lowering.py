@@ -70,9 +70,9 @@ def test_histogram_uses_exact_shared_counters():
 
 
 def test_matmul_forward_flattens_perfect_nest():
-    """The generic path flattens `for i k.` into one 4096-ordinal kernel (the
-    f64 parity mode keeps it; f32 mode sends this nest to the GEMM)."""
-    prog = dx.Program(P.matmul_fwd(64), ctx=None, float64=True)
+    """The generic path flattens `for i k.` into one 4096-ordinal kernel
+    (with the GEMM class disabled; by default this nest is a GEMM)."""
+    prog = dx.Program(P.matmul_fwd(64), ctx=None, float64=True, flags=dx.F_NO_GEMM)
     ks = _kernels(prog.plan)
     assert len(ks) == 1 and "n=4096" in ks[0], prog.plan
 
@@ -167,11 +167,31 @@ def test_transposed_gemm_operands_use_a_tiled_prologue():
     assert "reinterpret_cast<float4*>(hi)[t]" in prog.source
 
 
-def test_wide_gemm_tiles_are_opt_in(monkeypatch):
-    prog = dx.Program(P.contraction(12800, 256, 96, True, False), ctx=None)
-    assert "dx_gemm_tf32x3_n256" not in prog.plan
-    monkeypatch.setenv("DEXLET_GEMM_N256", "1")
-    prog = dx.Program(P.contraction(12800, 256, 96, True, False), ctx=None)
-    assert "dx_gemm_tf32x3_n256 " in prog.plan and "N=256 tiles" in prog.plan
-    prog = dx.Program(P.contraction(1000, 520, 1024), ctx=None)  # ragged N: N = 128 tiles
-    assert "dx_gemm_tf32x3_n256" not in prog.plan
+EMPTY_PROGRAMS = [
+    "main = \\x:((Fin 0)=>Float). sum x\n",
+    "main = \\p:((Fin 0)=>(Fin 4)). yieldAccum \\h. for i. h!(p.i) += 1.0\n",
+    "main = \\x:((Fin 0)=>Float). for i. (x.i) * 2.0\n",
+    "main = \\x:((Fin 3)=>((Fin 0)=>Float)). for i. sum (x.i)\n",
+    "main = \\x:((Fin 0)=>Float).\n  f = \\v:((Fin 0)=>Float). sum (for i. (v.i) * (v.i))\n  grad f x\n",
+]
+
+
+@pytest.mark.parametrize("src", EMPTY_PROGRAMS)
+def test_empty_index_sets_lower_without_kernels(src):
+    """Fin 0 loops enumerate nothing (eval.cpp:295-308): no kernel is launched
+    for them and cells keep their zero (eval.cpp:452-464); lowering must not
+    divide by the empty size (it used to abort the host with SIGFPE)."""
+    prog = dx.Program(src, ctx=None)
+    assert "kernel dxk" not in prog.plan or "(Fin 3)" in src
+
+
+def test_no_experiment_switches_in_library():
+    """Only the cache/dump/diagnostic environment variables remain in the
+    product library (no DEXLET_* switch changes a result)."""
+    import re
+    here = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2104_05372_b200", "csrc")
+    found = set()
+    for f in os.listdir(here):
+        if f.endswith((".cpp", ".inc", ".cuh", ".hpp")):
+            found |= set(re.findall(r'getenv\("([A-Z_]+)"\)', open(os.path.join(here, f)).read()))
+    assert found <= {"DEXLET_CACHE_DIR", "HOME", "DEXLET_NO_DISK_CACHE", "DEXLET_DUMP_DIR", "DEXLET_DEBUG_CONTRACT"}, found
