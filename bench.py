@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -43,6 +44,16 @@ sys.path.insert(0, ROOT)
 N_PER_GPU, D, K = 1_000_000, 16, 64
 METRIC = "kmeans fwd+grad evals/s (1M points/GPU, d=16, K=64)"
 UNIT = "evals/s"
+
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def input_bytes(spec):
+    """Bytes of one step's inputs (all leaves / arrays)."""
+    if spec.get("gmm"):
+        return sum(np.asarray(a).nbytes for a in spec["inputs"])
+    return sum(np.asarray(a).nbytes for leaves in spec["inputs"] for a in leaves)
 
 
 def config_spec(name, world):
@@ -351,10 +362,10 @@ def traffic_per_launch(config="kmeans", kernel=None):
     return None
 
 
-def reference_rate(sample_n, chunks, reps, warm=1):
-    """Evals/s of the 1M-point workload from the reference evaluator timed on a
-    bounded sample (linear scaling in points; the reference's transposed sum
-    is O(n^2), so this is optimistic for the reference)."""
+def reference_time(sample_n, chunks, reps, warm=1):
+    """Seconds per fwd+grad eval of the k-means program by the unmodified
+    reference evaluator (oracle/_ref) at n = sample_n points (d, K as the
+    workload), chunks = its EvalOptions.chunks (std::thread fork-join)."""
     import oracle
     from paper_2104_05372_b200 import programs as P
     pts, asg, cs = kmeans_inputs_fast(sample_n, D, K, seed=7)
@@ -366,8 +377,22 @@ def reference_rate(sample_n, chunks, reps, warm=1):
         dt = time.perf_counter() - t0
         if i >= warm:
             times.append(dt)
-    sec = statistics.mean(times)
-    return (sample_n / N_PER_GPU) / sec, sec, times
+    return statistics.mean(times), times
+
+
+def reference_kmeans_model(cores, n_small=10_000, n_big=50_000):
+    """Measured scaling of the reference on this host: times at n_small and
+    n_big (chunks = cores; n_small also at chunks = 1), the exponent
+    p = log(t_big / t_small) / log(n_big / n_small), and the full-size
+    (1M-point) time t_big * (1M / n_big)^p.  The reference's transposed sum
+    is O(n^2) (addAtPath copies), so p is near 2."""
+    t_small, _ = reference_time(n_small, cores, 2)
+    t_big, _ = reference_time(n_big, cores, 1, warm=0)
+    t_small_c1, _ = reference_time(n_small, 1, 1)
+    p = math.log(t_big / t_small) / math.log(n_big / n_small)
+    t_full = t_big * (N_PER_GPU / n_big) ** p
+    return {"n_small": n_small, "n_big": n_big, "s_small": t_small, "s_big": t_big, "s_small_chunks1": t_small_c1,
+            "exponent": p, "s_full_extrapolated": t_full, "cores": cores}
 
 
 def reference_sample_rate(config, chunks, reps=1):
@@ -432,44 +457,75 @@ def ref_config(name, world):
     return metric, dict({"workload": workload}, **extra)
 
 
+def _mapped_repo_libs():
+    """Shared objects of this repository mapped into the process."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if len(line.split()) >= 6 else ""
+                if path.endswith(".so") and path.startswith(ROOT):
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference(args, world, rank):
-    """The reference's own CPU implementation of the path on the host cores
-    (oracle/_ref = the unmodified reference evaluator; for GMM, which the
-    language cannot express, the fp64 port of ADBench's algorithm), on our
-    arm's metric and config, each step a bounded sample of the workload."""
+    """The reference's own CPU implementation of the path on the host cores:
+    oracle/_ref = the unmodified reference evaluator compiled from
+    /root/reference sources (for GMM, which the language cannot express, the
+    fp64 port of ADBench's algorithm), on our arm's metric and config.  Each
+    timed step is a bounded sample of the workload that really runs; the
+    full-size rate is extrapolated with the exponent measured on this host.
+    This path never loads libdexlet_cuda.so (checked below)."""
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     metric, config = ref_config(args.config, world)
+    extra = {}
+    t_wall0 = time.time()
     if args.config == "gmm":
         rates = [gmm_cpu_rate(reps=1) for _ in range(max(1, args.steps))]
         rate = statistics.mean(r for r, _ in rates)
-        sec = statistics.mean(t for _, t in rates)
+        step_s = statistics.mean(t for _, t in rates)
         kind, dtype = "port", "f64"
-        sample = (f"oracle/gmm.py fp64 port on n=2000 points, {sec:.3f} s/eval, scaled linearly to 1M points")
+        sample = (f"oracle/gmm.py fp64 port on n=2000 points, {step_s:.3f} s/eval, scaled linearly to 1M points "
+                  f"(the port is linear in n)")
         config["reference_sample_points"] = 2000
     elif args.config == "kmeans":
-        rate, sec, times = reference_rate(args.ref_sample, cores, args.steps, warm=args.warmup)
-        kind, dtype = "reference", "f32"
-        sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2) on "
-                  f"n={args.ref_sample} points (d={D}, K={K}), chunks={cores}; {sec:.3f} s/eval; "
-                  f"scaled linearly to 1M points")
-        config["reference_sample_points"] = args.ref_sample
+        n_small = args.ref_sample
+        step_s, times = reference_time(n_small, cores, args.steps, warm=args.warmup)
+        model = reference_kmeans_model(cores, n_small=n_small)
+        rate = world / model["s_full_extrapolated"]
+        kind, dtype = "reference", "f64"
+        sample = (f"reference evalExpr (oracle/_ref, unmodified /root/reference sources, g++ -O2), chunks={cores}: "
+                  f"{args.steps} timed steps of n={n_small} points ({step_s:.3f} s each); n={model['n_big']} once "
+                  f"({model['s_big']:.2f} s); measured exponent {model['exponent']:.2f} -> {model['s_full_extrapolated']:.0f} s "
+                  f"per 1M-point eval (extrapolated); chunks=1 at n={n_small}: {model['s_small_chunks1']:.3f} s")
+        extra["reference_scaling"] = model
+        config["reference_sample_points"] = n_small
     else:
         runs = [reference_sample_rate(args.config, cores) for _ in range(max(1, args.steps))]
         rate = statistics.mean(r for r, _, _ in runs)
-        sec = statistics.mean(t for _, t, _ in runs)
-        kind, dtype = "reference", "f32"
-        sample = f"reference evalExpr (oracle/_ref) chunks={cores}: {runs[0][2]}; {sec:.3f} s per sample"
+        step_s = statistics.mean(t for _, t, _ in runs)
+        kind, dtype = "reference", "f64"
+        sample = f"reference evalExpr (oracle/_ref) chunks={cores}: {runs[0][2]}; {step_s:.3f} s per sample"
+    libs = _mapped_repo_libs()
+    assert not any("libdexlet_cuda" in l for l in libs), libs  # the reference arm runs none of our code
     line = {
         "impl": "reference", "metric": metric, "value": rate, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate if rate > 0 else None,
+        "steps": args.steps, "warmup": args.warmup,
+        # what was really run per step (a bounded sample), not the extrapolated full-size eval
+        "ms_per_step": step_s * 1e3, "ms_per_step_is": "measured per bounded-sample step (see cpu_baseline.sample)",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (seeded; same generators as our arm, bounded sample)",
         "config": config,
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs_loaded": libs, "wall_s": time.time() - t_wall0,
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -499,7 +555,17 @@ def main():
         ctx.init_comm(obj[0], world, rank)
 
     spec = config_spec(args.config, world)
-    prog = (GmmRunner if spec.get("gmm") else ProgramRunner)(dx, ctx, spec, rank, world)
+    Runner = GmmRunner if spec.get("gmm") else ProgramRunner
+    # Inputs larger than L2 (timing rules): the workload's inputs rotate over
+    # R device-resident copies, each its own lowered plan, so that the other
+    # R - 1 copies (>= 1.5x the 126 MB L2) are read between two reads of a
+    # copy.  Every step is one full eval over its copy; the K timed steps run
+    # back to back between one event pair (launch latency overlaps the
+    # previous step, as in a serving loop).
+    in_bytes = input_bytes(spec)
+    R = min(8, 1 + max(0, -(-int(1.5 * L2_BYTES) // max(1, in_bytes))))
+    runners = [Runner(dx, ctx, spec, rank, world) for _ in range(R)]
+    prog = runners[0]
     launches_per_run = prog.launches
 
     def barrier():
@@ -514,47 +580,50 @@ def main():
     # workload keeps running untimed until it has under-load samples, then
     # the K timed steps follow, then a short untimed tail.
     clocks = Clocks(local) if not args.profile else None
+    step = 0
     for _ in range(args.warmup):
-        ctx.l2_flush()
-        prog.run()
+        runners[step % R].run()
+        step += 1
+    ctx.sync()
     t_end = time.time() + (5.0 if clocks else 0.0)
     t_min = time.time() + 0.6
     while clocks and time.time() < t_end and (clocks.lines() < 3 or time.time() < t_min):
         for _ in range(20):
-            ctx.l2_flush()
-            prog.run()
+            runners[step % R].run()
+            step += 1
         ctx.sync()
     barrier()
-    step_ms, kern = [], {}
-    for _ in range(args.steps):
-        ctx.l2_flush()
-        e0 = ctx.event()
-        prog.run()
-        e1 = ctx.event()
-        step_ms.append(ctx.elapsed_ms(e0, e1))
-        ctx.destroy_event(e0)
-        ctx.destroy_event(e1)
+    e0 = ctx.event()
+    for i in range(args.steps):
+        runners[i % R].run()
+    e1 = ctx.event()
+    ctx.sync()
+    ms_total = ctx.elapsed_ms(e0, e1)
+    ctx.destroy_event(e0)
+    ctx.destroy_event(e1)
     # per-kernel durations (roofline): the same K steps again with an event
     # pair around every launch, kept out of the step time above
-    prog.set_timing(True)
-    ctx.l2_flush()
-    prog.run()
-    prog.kernel_times()
-    for _ in range(args.steps):
-        ctx.l2_flush()
-        prog.run()
-        for name, ms in prog.kernel_times():
+    kern = {}
+    for r in runners:
+        r.set_timing(True)
+        r.run()
+        r.kernel_times()
+    for i in range(args.steps):
+        r = runners[i % R]
+        r.run()
+        for name, ms in r.kernel_times():
             kern.setdefault(name, []).append(ms)
-    prog.set_timing(False)
+    for r in runners:
+        r.set_timing(False)
     barrier()
     t_tail = time.time() + (0.3 if clocks else 0.0)
     while time.time() < t_tail:
         for _ in range(20):
-            ctx.l2_flush()
-            prog.run()
+            runners[step % R].run()
+            step += 1
         ctx.sync()
     clk = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (--profile)"]}
-    ms_local = statistics.mean(step_ms)
+    ms_local = ms_total / args.steps
     # dominant kernel
     dom = max(kern.items(), key=lambda kv: statistics.mean(kv[1]))
     dom_ms = statistics.mean(dom[1])
@@ -599,7 +668,10 @@ def main():
                             "parallelism": (f"points sharded x{world} + NCCL allreduce of the fp64 moments"
                                             if spec.get("gmm") else
                                             f"outer loop sharded x{world} + NCCL allreduce of Accum cells"),
-                            "l2": "flushed before every timed step (256 MB scratch write, outside the events)",
+                            "l2": (f"inputs larger than L2: {R} device-resident input copies "
+                                   f"({R * in_bytes / 1e6:.0f} MB, each read once per {R} steps) rotate "
+                                   f"under K back-to-back steps timed by one event pair"),
+                            "steps_timing": "K consecutive steps between one CUDA event pair, / K",
                        "kernel_times": "second pass of the same K steps with per-launch events"},
                            **spec["extra"]),
             "roofline": {"bound": spec["bound"], "kernel": dom[0], "achieved": achieved, "peak": peak,
@@ -614,13 +686,14 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline and not args.profile and args.config == "kmeans":
             try:
-                cores = os.cpu_count() or 1
-                rate, sec, _ = reference_rate(10_000, cores, 3)
+                cores = len(os.sched_getaffinity(0))
+                model = reference_kmeans_model(cores)
                 line["cpu_baseline"] = {
-                    "value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-                    "sample": (f"reference evalExpr (oracle/_ref) on n=10000 points, chunks={cores}, "
-                               f"3 evals, {sec:.3f} s/eval, scaled linearly to 1M points (the reference's "
-                               f"transposed sum is O(n^2): optimistic for the reference)")}
+                    "value": 1.0 / model["s_full_extrapolated"], "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": (f"reference evalExpr (oracle/_ref), chunks={cores}: n={model['n_small']} "
+                               f"{model['s_small']:.3f} s, n={model['n_big']} {model['s_big']:.2f} s; measured "
+                               f"exponent {model['exponent']:.2f} -> {model['s_full_extrapolated']:.0f} s per "
+                               f"1M-point eval (extrapolated)")}
             except Exception as e:  # the oracle library must travel with the repo
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                         "sample": f"unavailable: {e}"}

@@ -492,59 +492,119 @@ __device__ __forceinline__ void dx_fin2(const P* part, int nblk, long long width
   if (ty == 0 && c < width) cell[c] += counts ? red[0][tx] * scale : red[0][tx];
 }
 
-// ---- in-kernel finalize (cooperative launch: every block is resident) ----
-// Grid barrier on a persistent counter: each launch adds gridDim.x, so the
-// target of this launch is the next multiple of gridDim.x.
-__device__ __forceinline__ void dx_grid_barrier(unsigned* counter) {
+// ---- in-kernel finalize: last-block-done fold (no grid barrier) -----------
+// Every block writes its partial row, then arrives on its group's ticket
+// (groups of DX_LBD_GB consecutive blocks); the last block of a group folds
+// the group's rows in block order into a group partial (f64 / u64), and the
+// last group to finish folds the group partials in group order into the cell.
+// The result is deterministic for a fixed grid, no block waits for another,
+// and the tickets are reset by the block that consumed them, so they never
+// wrap (any number of launches).  tick layout: [ngroups] group tickets, then
+// DX_LBD_TOP (final ticket) and DX_LBD_ERR (E-bounds flags of this launch).
+#define DX_LBD_GB 16
+#define DX_LBD_TOP 1024
+#define DX_LBD_ERR 1025
+#define DX_LBD_WORDS 1026
+__device__ __forceinline__ float dx_ldcg(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double dx_ldcg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned dx_ldcg(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ long long dx_ldcg(const long long* p) {
+  long long v;
+  asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+// Block-wide: true in exactly one block, the last of `expected` to arrive
+// on tick[slot]; that block then sees every arriving block's writes.
+__device__ __forceinline__ bool dx_lbd_arrive(unsigned* tick, int slot, unsigned expected) {
+  __shared__ int dx_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(counter, 1u);
-    const unsigned target = (prev / gridDim.x + 1u) * gridDim.x;
-    while (true) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-      if ((int)(v - target) >= 0) break;
-      __nanosleep(32);
+    dx_last = atomicAdd(&tick[slot], 1u) == expected - 1u;
+  }
+  __syncthreads();
+  const bool last = dx_last != 0;
+  if (last) __threadfence();
+  return last;
+}
+// Group fold: gpart[grp][c] = sum over blocks first .. first+cnt-1 (block
+// order) of part[b][c]; all loads of a column are issued before the sum.
+template <class P, class G>
+__device__ __forceinline__ void dx_lbd_group(const P* part, long long width, G* gpart, int grp, int first, int cnt) {
+  for (long long c = threadIdx.x; c < width; c += blockDim.x) {
+    P v[DX_LBD_GB];
+#pragma unroll
+    for (int b = 0; b < DX_LBD_GB; ++b) v[b] = b < cnt ? dx_ldcg(&part[(long long)(first + b) * width + c]) : P(0);
+    G s = G(0);
+#pragma unroll
+    for (int b = 0; b < DX_LBD_GB; ++b)
+      if (b < cnt) s += (G)v[b];
+    gpart[(long long)grp * width + c] = s;
+  }
+}
+// Final fold of the group partials (group order) into the cell: store (the
+// cell's zero-fill was folded into this kernel) or add.
+template <class G, class T>
+__device__ __forceinline__ void dx_lbd_final(const G* gpart, long long width, int ngrp, T scale, T* cell, bool counts,
+                                             bool store) {
+  for (long long c = threadIdx.x; c < width; c += blockDim.x) {
+    G s = G(0);
+    for (int g0 = 0; g0 < ngrp; g0 += 32) {
+      G v[32];
+#pragma unroll
+      for (int b = 0; b < 32; ++b) v[b] = g0 + b < ngrp ? dx_ldcg(&gpart[(long long)(g0 + b) * width + c]) : G(0);
+#pragma unroll
+      for (int b = 0; b < 32; ++b)
+        if (g0 + b < ngrp) s += v[b];
+    }
+    const T val = counts ? (T)s * scale : (T)s;
+    if (store) cell[c] = val;
+    else cell[c] += val;
+  }
+}
+
+// ---- in-kernel finalize, cooperative form (every block resident) ---------
+// Wrap-safe grid barrier: bar[0] counts arrivals, bar[1] is a generation that
+// the last arriver bumps after resetting the count; waiters compare
+// generations for equality, so the words never overflow into a hang.
+__device__ __forceinline__ void dx_grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1u) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (true) {
+        unsigned g;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        if (g != gen) break;
+        __nanosleep(20);
+      }
     }
     __threadfence();
   }
   __syncthreads();
 }
-// Paired fp32 arithmetic (sm_100 FADD2 / FFMA2: two IEEE fp32 operations per
-// instruction, each lane rounded exactly as the scalar op)
-__device__ __forceinline__ float2 dx_f2sub(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dx_f2add(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dx_f2mul(float2 a, float2 b) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 dx_f2fma(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-
 // Cooperative fold of per-block partials [nblk][width] into `cell`: block b
 // owns columns [8b, 8b+8); thread (c, g) sums rows g, g+R, ... in order, then a
-// fixed tree over the R row groups.  Deterministic for a fixed grid.
+// fixed tree over the R row groups.
+// Deterministic for a fixed grid.
 template <class T, class P>
 __device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T scale, T* cell, bool counts,
                                              bool store) {
@@ -578,6 +638,36 @@ __device__ __forceinline__ void dx_coop_fold(const P* part, long long width, T s
     }
     __syncthreads();
   }
+}
+// Paired fp32 arithmetic (sm_100 FADD2 / FFMA2: two IEEE fp32 operations per
+// instruction, each lane rounded exactly as the scalar op)
+__device__ __forceinline__ float2 dx_f2sub(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dx_f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dx_f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 dx_f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
 
 extern "C" __global__ void __launch_bounds__(1024) dx_fin_f32(const float* p, int n, long long w, float* c) { dx_fin2<float, float>(p, n, w, 1.0f, c, false); }

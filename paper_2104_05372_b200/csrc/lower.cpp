@@ -3252,15 +3252,39 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
   }
 
-  // In-kernel finalize: a cooperative launch (all blocks resident) lets the
-  // blocks meet at a grid barrier and fold the partials themselves.
-  bool coop = false;
-  for (auto& cu : g.cells) coop |= cu.partialBuf >= 0;
-  if (serial || total == 0) coop = false;
-  int syncBuf = -1;
+  // In-kernel finalize: the blocks fold the partials themselves, last block
+  // done per group of DX_LBD_GB, then the last group (dx_lbd_* in
+  // dx_device.cuh): no grid barrier, no cooperative launch, no extra kernel.
+  bool fold = false;
+  for (auto& cu : g.cells) fold |= cu.partialBuf >= 0;
+  if (serial || total == 0) fold = false;
+  // Two forms (measured on B200, bench.py back to back): narrow partial rows
+  // (k-means: 1025 words) fold fastest after a grid barrier, every block
+  // folding 8 columns (31.0 vs 38.8 us per 1M-point step); wide rows
+  // (histogram: 4096 counters x ~1200 blocks = 19 MB of partials) fold
+  // fastest last-block-done, groups folding as their blocks finish (193 vs
+  // 218 us per 2^28-key step).
+  long long widest = 0;
+  for (auto& cu : g.cells)
+    if (cu.partialBuf >= 0) widest = std::max(widest, cu.width);
+  const bool lbd = fold && widest >= 2048;
+  const bool coop = fold && !lbd;
+  int tickBuf = -1, syncBuf = -1;
+  std::vector<int> gpartBuf(g.cells.size(), -1);
   if (coop) {
-    syncBuf = newBuf(BufDecl::Sync, SK::U32, 1);
+    syncBuf = newBuf(BufDecl::Sync, SK::U32, 2);
     param(g, syncBuf, true);
+  }
+  if (lbd) {
+    tickBuf = newBuf(BufDecl::Sync, SK::U32, 1026);  // DX_LBD_WORDS
+    param(g, tickBuf, true);
+    for (size_t i = 0; i < g.cells.size(); ++i) {
+      CellUse& cu = g.cells[i];
+      if (cu.partialBuf < 0) continue;
+      gpartBuf[i] = newBuf(BufDecl::Partial, cu.strat == CellUse::Count ? SK::I : SK::D, 0);
+      plan.bufs[gpartBuf[i]].partialWidth = cu.width;  // grid x width (>= groups x width)
+      param(g, gpartBuf[i], true);
+    }
   }
 
   // Assemble source.
@@ -3587,10 +3611,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     if (tileCell < 0 && g.tile && !g.staged.empty())
       src << "    __syncthreads();  // every thread is done with this TMA stage\n";
     src << "  }\n";
-    // cooperative kernels that are the first writer of the error flag reset
-    // it themselves (block 0, before the grid barrier; flags are raised after it)
+    // last-block-done kernels collect the E-bounds flags of the launch in a
+    // ticket word; the final block forwards them (and initializes the error
+    // flag when this kernel is its first writer)
+    const bool lbdErr = lbd && takeZero(plan.errFlagBuf);
     const bool coopErr = coop && takeZero(plan.errFlagBuf);
-    if (!coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
+    if (!lbd && !coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
     // epilogue: block partials
     for (size_t i = 0; i < g.cells.size(); ++i) {
       CellUse& cu = g.cells[i];
@@ -3633,7 +3659,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
-      src << "  dx_grid_barrier(p" << syncBuf << ");\n";
+      src << "  dx_grid_barrier(" << g.params[syncBuf] << ");\n";
       if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
       for (size_t i = 0; i < g.cells.size(); ++i) {
         CellUse& cu = g.cells[i];
@@ -3646,6 +3672,37 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
             << cu.width << "LL, (" << ct << ")" << litF(counts ? cu.constVal : 1.0, true) << ", " << cu.pname
             << ", " << (counts ? "true" : "false") << ", " << (store ? "true" : "false") << ");\n";
       }
+    }
+    if (lbd) {
+      const std::string T = g.params[tickBuf];
+      src << "  {\n    const int dx_ng = (gridDim.x + DX_LBD_GB - 1) / DX_LBD_GB, dx_grp = blockIdx.x / DX_LBD_GB;\n"
+          << "    const int dx_gsz = min(DX_LBD_GB, (int)gridDim.x - dx_grp * DX_LBD_GB);\n"
+          << "    if (dx_bad) atomicOr(&" << T << "[DX_LBD_ERR], 1u);\n"
+          << "    if (dx_lbd_arrive(" << T << ", dx_grp, (unsigned)dx_gsz)) {\n";
+      for (size_t i = 0; i < g.cells.size(); ++i) {
+        CellUse& cu = g.cells[i];
+        if (cu.partialBuf < 0) continue;
+        bool counts = cu.strat == CellUse::Count;
+        src << "      dx_lbd_group<" << (counts ? "unsigned, long long" : "dx_f, double") << ">(part" << i << ", "
+            << cu.width << "LL, " << g.params[gpartBuf[i]] << ", dx_grp, dx_grp * DX_LBD_GB, dx_gsz);\n";
+      }
+      src << "      if (threadIdx.x == 0) " << T << "[dx_grp] = 0u;\n"
+          << "      if (dx_lbd_arrive(" << T << ", DX_LBD_TOP, (unsigned)dx_ng)) {\n";
+      for (size_t i = 0; i < g.cells.size(); ++i) {
+        CellUse& cu = g.cells[i];
+        if (cu.partialBuf < 0) continue;
+        std::string ct = ctype(plan.bufs[cu.targetBuf].kind);
+        bool counts = cu.strat == CellUse::Count;
+        // a cell whose only pending step is its zero-fill is overwritten
+        const bool store = takeZero(cu.targetBuf);
+        src << "        dx_lbd_final<" << (counts ? "long long" : "double") << ", " << ct << ">(" << g.params[gpartBuf[i]]
+            << ", " << cu.width << "LL, dx_ng, (" << ct << ")" << litF(counts ? cu.constVal : 1.0, true) << ", "
+            << cu.pname << ", " << (counts ? "true" : "false") << ", " << (store ? "true" : "false") << ");\n";
+      }
+      src << "        if (threadIdx.x == 0) {\n          " << T << "[DX_LBD_TOP] = 0u;\n"
+          << "          const unsigned e = atomicExch(&" << T << "[DX_LBD_ERR], 0u);\n"
+          << (lbdErr ? "          *dx_err = (int)e;\n" : "          if (e) atomicOr(dx_err, 1);\n")
+          << "        }\n      }\n    }\n  }\n";
     }
     src << "}\n\n";
   }
@@ -3681,11 +3738,13 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   int kstep = (int)plan.steps.size() - 1;
   for (auto& cu : g.cells)
     if (cu.partialBuf >= 0) plan.bufs[cu.partialBuf].partialKernel = kstep;
+  for (int gb : gpartBuf)
+    if (gb >= 0) plan.bufs[gb].partialKernel = kstep;
 
   // Finalize privatized partials into the cell (fixed block order).
   for (size_t i = 0; i < g.cells.size(); ++i) {
     CellUse& cu = g.cells[i];
-    if (cu.partialBuf < 0 || coop) continue;
+    if (cu.partialBuf < 0 || fold) continue;
     Step f;
     f.k = Step::Finalize;
     f.buf = cu.targetBuf;

@@ -1,25 +1,30 @@
-"""Dev tool: elementwise / normwise gradient error of the GMM kernels on the
-test cases (run once per env setting, e.g. DEXLET_GMM_BWD_PAIR=1)."""
-import os, sys
+"""Dev tool: GMM gradient error at the BASELINE size (n = 1M, K = 200) against
+the committed fp64 golden (tests/golden/gmm_1m_k200.npz): elementwise
+(rtMaxRelDiff) and normwise per block, and where the worst entries are."""
+import os
+import sys
+
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import paper_2104_05372_b200 as dx
-from oracle import gmm as G
+from paper_2104_05372_b200 import programs as P
 
-def rel(a, b):
-    a = np.asarray(a, dtype=np.float64); b = np.asarray(b, dtype=np.float64)
-    return float(np.max(np.abs(a - b) / (1.0 + np.maximum(np.abs(a), np.abs(b)))))
-
-def normrel(a, b):
-    a = np.asarray(a, dtype=np.float64); b = np.asarray(b, dtype=np.float64)
-    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
-
-ctx = dx.Context(0)
-for n, k in [(1000, 3), (4999, 10), (8192, 17), (20000, 24), (100000, 64)]:
-    a, mu, icf, x = G.gmm_inputs(n, 64, k, seed=100 + k)
-    g = dx.GMM(ctx, 64, k, n)
-    r = g(a, mu, icf, x)
-    w = G.gmm_objective_grad(a, mu, icf, x)
-    print(("pair" if os.environ.get("DEXLET_GMM_BWD_PAIR") else "quad"), n, k, "obj %.1e" % rel(r[0], w[0]),
-          " ".join("%s %.2e/%.2e" % (nm, rel(u, v), normrel(u, v)) for nm, u, v in zip(("da", "dm", "di"), r[1:], w[1:])),
-          "max|di| %.1f" % np.max(np.abs(w[3])), flush=True)
+z = np.load(os.path.join(ROOT, "tests", "golden", "gmm_1m_k200.npz"))
+n, d, k = int(z["n"]), int(z["d"]), int(z["k"])
+a, mu, icf, x = P.gmm_inputs(n, d, k, seed=int(z["seed"]))
+assert float(x.astype(np.float64).sum()) == float(z["x_checksum"])
+g = dx.GMM(dx.Context(0), d, k, n)
+err, da, dm, di = g(a, mu, icf, x)
+print("objective rel %.2e (got %.10g want %.10g)" % (abs(err - z["err"]) / (1 + abs(z["err"])), err, z["err"]))
+for nm, got, want in (("d_alphas", da, z["d_alphas"]), ("d_means", dm, z["d_means"]), ("d_icf", di, z["d_icf"])):
+    got = np.asarray(got, np.float64).ravel()
+    want = np.asarray(want, np.float64).ravel()
+    r = np.abs(got - want) / (1 + np.maximum(np.abs(got), np.abs(want)))
+    j = int(np.argmax(r))
+    cols = want.size // k
+    print(f"{nm}: rel {r.max():.2e} norm {np.abs(got - want).max() / max(1, np.abs(want).max()):.2e}; worst at "
+          f"component {j // cols} entry {j % cols}: got {got[j]:.6g} want {want[j]:.6g}; "
+          f"abs err max {np.abs(got - want).max():.3g}, median |want| {np.median(np.abs(want)):.3g}, "
+          f"entries > 1e-4: {(r > 1e-4).sum()} of {r.size}", flush=True)

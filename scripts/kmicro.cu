@@ -47,6 +47,13 @@ __device__ __forceinline__ unsigned swz(unsigned a) { return a ^ (((a >> 7) & 3)
 // group folds the group's partials (fixed order) into a group partial; the
 // last group folds the group partials (fixed order) into the result.
 // part: [nblk][W] floats; gpart: [ngrp][W] floats; tick: [ngrp + 1] u32.
+__device__ unsigned long long g_ts[4096][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_fold[8];
 template <int W>
 __device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB, double* out) {
   // every load of a fold is issued before the fixed-order sum (one L2 latency)
@@ -61,6 +68,7 @@ __device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const unsigned long long tg0 = gtime();
   for (int c = threadIdx.x; c < W; c += blockDim.x) {
     float v[32];
 #pragma unroll
@@ -71,6 +79,7 @@ __device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB
     gpart[(long long)grp * W + c] = s;
   }
   __syncthreads();
+  const unsigned long long tg1 = gtime();
   if (threadIdx.x == 0) {
     tick[grp] = 0;
     __threadfence();
@@ -79,6 +88,7 @@ __device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const unsigned long long tf0 = gtime();
   for (int c = threadIdx.x; c < W; c += blockDim.x) {
     float v[32];
 #pragma unroll
@@ -88,7 +98,11 @@ __device__ void lbd_fold(const float* part, float* gpart, unsigned* tick, int GB
     for (int g = 0; g < 32; ++g) s += (double)v[g];
     out[c] = s;
   }
-  if (threadIdx.x == 0) tick[ngrp] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tick[ngrp] = 0;
+    g_fold[0] = tg0; g_fold[1] = tg1; g_fold[2] = tf0; g_fold[3] = gtime();
+  }
 }
 
 __global__ void __launch_bounds__(512) k_stream(const float4* __restrict__ p, long long n4, const int4* __restrict__ a, long long na4, float* out) {
@@ -183,12 +197,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_ldg(const float* __restrict__ pt
 }
 
 // ---- variant 1b: sub-warp LDG with the next chunk's loads in flight -------
-__device__ unsigned long long g_ts[4096][6];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 template <int NW, int U>
 __global__ void __launch_bounds__(NW * 32, 1) k_ldgp(const float* __restrict__ pts, const int* __restrict__ asg,
                                                     const float* __restrict__ cs, long long n, float* part, float* gpart,
@@ -537,6 +545,9 @@ int main(int argc, char** argv) {
       std::sort(v.begin(), v.end());
       printf("  phase %d (0 entry,1 prologue,2 loop,3 flush,4 fold): min %.2f med %.2f max %.2f us\n", ph, v[0], v[v.size() / 2], v.back());
     }
+    unsigned long long gf[8];
+    CK(cudaMemcpyFromSymbol(gf, g_fold, 64));
+    printf("  final block: group fold %.2f..%.2f us, final fold %.2f..%.2f us\n", (gf[0] - t0) * 1e-3, (gf[1] - t0) * 1e-3, (gf[2] - t0) * 1e-3, (gf[3] - t0) * 1e-3);
   }
 #define TMA(NW, T, NS, GB)                                                                                      \
   {                                                                                                             \

@@ -41,6 +41,15 @@ def cases():
     out.append(("either_case_33", P.either_case(33), [r.standard_normal(33), r.standard_normal(33)]))
     out.append(("mandelbrot_8x6", P.mandelbrot(8, 6, 20),
                 [np.linspace(-2.0, 0.5, 8), np.linspace(-1.0, 1.0, 6)]))
+    # empty index sets (Fin 0): no iteration, zero cells (eval.cpp:295-308, 452-464)
+    e0 = np.zeros(0, np.float32)
+    out.append(("empty_sum", "main = \\x:((Fin 0)=>Float). sum x\n", [e0]))
+    out.append(("empty_hist", "main = \\p:((Fin 0)=>(Fin 4)). yieldAccum \\h. for i. h!(p.i) += 1.0\n",
+                [np.zeros(0, np.int32)]))
+    out.append(("empty_map", "main = \\x:((Fin 0)=>Float). for i. (x.i) * 2.0\n", [e0]))
+    out.append(("empty_rows", "main = \\x:((Fin 3)=>((Fin 0)=>Float)). for i. sum (x.i)\n", [e0]))
+    out.append(("empty_grad", "main = \\x:((Fin 0)=>Float).\n  f = \\v:((Fin 0)=>Float). sum (for i. (v.i) * (v.i))\n"
+                "  grad f x\n", [e0]))
     return out
 
 

@@ -29,6 +29,9 @@ def test_parity(ctx, name, src, inputs, f64):
     want = _ref(src, inputs)
     prog = dx.Program(src, ctx=ctx, float64=f64)
     got = prog(*inputs)
+    if not want:  # the oracle harness flattens an empty table to no leaves
+        assert all(g.size == 0 for g in got), [g.shape for g in got]
+        return
     assert len(got) == len(want), (len(got), len(want))
     kinds = prog.output_leaves()
     for (k, _), g, w in zip(kinds, got, want):
@@ -67,3 +70,18 @@ def test_repeat_runs_identical(ctx):
     b = prog(*inputs)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_many_launches_keep_the_fold_tickets_consistent(ctx):
+    """The in-kernel fold's tickets are reset by the blocks that consume them:
+    200 back-to-back runs give the first run's bit-identical result."""
+    from paper_2104_05372_b200 import programs as P
+    n, d, k = 300_000, 16, 64
+    pts, asg, cs = P.kmeans_inputs(n, d, k)
+    prog = dx.Program(P.kmeans_cost_grad(n, d, k), ctx=ctx)
+    first = prog(pts, asg, cs)
+    for _ in range(200):
+        prog.run()
+    again = [prog.get_output(0), prog.get_output(1)]
+    for a, b in zip(first, again):
+        np.testing.assert_array_equal(a, b)

@@ -42,8 +42,9 @@ def _sass(source):
 def test_kmeans_value_and_grad_is_one_fused_kernel():
     """Forward tape inlined into both consumers (no HBM tape), the cotangent
     broadcast folded (accum-to-map), cost and gradient loops fused
-    horizontally: one cooperative kernel that also folds the partials and
-    owns the zero-fills (the plan is that single launch)."""
+    horizontally: one cooperative kernel that also folds the partials after a
+    wrap-safe grid barrier and owns the zero-fills (the plan is that single
+    launch)."""
     prog = dx.Program(P.kmeans_cost_grad(100_000, 16, 64), ctx=None)
     ks = _kernels(prog.plan)
     assert len(ks) == 1, prog.plan
@@ -52,6 +53,7 @@ def test_kmeans_value_and_grad_is_one_fused_kernel():
     assert "dx_warp_tab<16, 64" in src            # warp-private row tables for dC
     assert "dx_warp_tab_flush<16, 64" in src
     assert ", true);" in src                      # fold overwrites the (never zeroed) cell
+    assert "dx_grid_barrier(" in src and "dx_coop_fold<double, dx_f>" in src
     assert "dx_block_sum(rp" in src               # register partial for the cost
     assert "dx_tma_2d(" in src                    # TMA tensor tiles of the points
     sass = _sass(src)
@@ -62,9 +64,10 @@ def test_histogram_uses_exact_shared_counters():
     prog = dx.Program(P.histogram(1 << 20, 4096), ctx=None)
     assert len(_kernels(prog.plan)) == 1
     assert "dx_count_smem" in prog.source
-    # u32 counters folded in fixed block order and scaled by the constant,
-    # after the in-kernel grid barrier (cooperative launch) or by a finalize step
-    assert "dx_coop_fold<double, unsigned>" in prog.source or "count" in prog.plan
+    # u32 counters (4096-word partial rows) folded in fixed block order (u64
+    # group sums) and scaled by the constant by the last blocks of the launch
+    assert "dx_lbd_group<unsigned, long long>" in prog.source
+    assert "dx_lbd_final<long long, double>" in prog.source
     sass = _sass(prog.source)
     assert "ATOMS" in sass and "LDG.E.128" in sass
 
