@@ -135,6 +135,9 @@ enum {
  * Reference path: parseProgram (parser.cpp:1651), checkExpr (typecheck.cpp:578),
  * simplify + optimize (simplify.cpp:1081,1107), then — instead of
  * evalExpr (eval.cpp:621) — device lowering of every for/runAccum nest.
+ * entry NULL or "": the whole file (declarations around its final
+ * expression, no inputs), as the reference harness's runSimpl evaluates it
+ * (tests/acceptance.cpp:68-71).
  * ctx may be NULL: lower and compile only (no device needed). */
 int dxl_program_create(dxc_ctx* ctx, const char* source, const char* entry,
                        const dxl_options* opts, dxl_program** out);

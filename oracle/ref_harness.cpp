@@ -193,6 +193,18 @@ int dxo_program_create(const char* source, const char* entry, dxo_program** out)
   GUARD_BEGIN
   NameSupply::reset(1000000);
   ElabProgram p = parseProgram(source, "program.dexlet");
+  if (!entry || !*entry) {
+    // whole file (the reference harness's runSimpl, tests/acceptance.cpp:68-71)
+    auto* prog = new dxo_program();
+    ExprPtr e = p.whole();
+    TypeEnv env;
+    checkExpr(Capability::pure(), env, e);
+    SimplResult r = simplify(env, e);
+    prog->optimized = optimize(contextFill(r.ctx, eRet(r.residual)));
+    prog->ir = printExpr(prog->optimized);
+    *out = prog;
+    return 0;
+  }
   const ElabDecl* m = p.find(entry);
   if (!m) fail(ErrCode::UnboundVariable, std::string("entry '") + entry + "' is not defined");
   auto* prog = new dxo_program();

@@ -287,6 +287,7 @@ class Program:
                  flags: int = 0):
         opts = DxlOptions(1 if float64 else 0, rank, world, threads, flags)
         h = _vp()
+        entry = entry or ""  # "" / None: the whole file (its final expression, no inputs)
         _check(_lib.dxl_program_create(ctx.handle if ctx else None, source.encode(), entry.encode(),
                                        ctypes.byref(opts), ctypes.byref(h)))
         self.handle = h

@@ -959,6 +959,22 @@ class Lowering {
       for (auto& e : t->elems) elems.push_back(hvalue(env, e));
       return constTable(d, elems, v->span);
     }
+    if (const auto* vc = as<VValueCase>(v)) {
+      // lazy case over function branches (reference eval.cpp:180-185): a
+      // host-known scrutinee picks its branch here, anything else runs on
+      // one device thread
+      HV sc = hvalue(env, vc->scrutinee);
+      const auto* lf = as<VLam>(vc->leftFn);
+      const auto* rf = as<VLam>(vc->rightFn);
+      if (lf && rf && sc->k == HVal::Const && sc->ty->k == DType::Idx &&
+          sc->ty->desc->kind == IndexSetDesc::Kind::Either) {
+        DescPtr d = sc->ty->desc;
+        long long ls = size(d->left);
+        if (sc->i < ls) return hexpr(hbind(env, lf->binder, hFromOrdinal(sc->i, d->left)), lf->body);
+        return hexpr(hbind(env, rf->binder, hFromOrdinal(sc->i - ls, d->right)), rf->body);
+      }
+      return serialKernel(env, eRet(v), nullptr);
+    }
     notLowerable("value " + printValue(v), v->span);
   }
 
@@ -1021,6 +1037,21 @@ class Lowering {
           return;
         case HVal::Unit: return;
         case HVal::Pair: go(x->a); go(x->b); return;
+        case HVal::Buf: {
+          // a nested table literal: its Const buffers hold the values
+          std::vector<LeafInfo> lv = leaves(x->ty);
+          for (size_t l = 0; l < lv.size(); ++l) {
+            const BufDecl& b = plan.bufs[x->bufs[l]];
+            if (b.role != BufDecl::Const) notLowerable("non-constant element in a table literal", sp);
+            std::vector<double> vals;
+            for (long long q = 0; q < lv[l].count; ++q) {
+              const long long at = x->offs[l] + q;
+              vals.push_back(b.kind == SK::F ? b.initF.at(at) : (double)b.initI.at(at));
+            }
+            perLeaf.push_back(std::move(vals));
+          }
+          return;
+        }
         default: notLowerable("non-constant element in a table literal", sp);
       }
     };

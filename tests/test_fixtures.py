@@ -1,0 +1,70 @@
+"""The reference's own fixture corpus (proj/tests/fixtures, driving criterion 1
+of its acceptance gate, tests/acceptance.cpp:112-152) through the device path,
+as whole files (runSimpl, acceptance.cpp:68-71).  Expected outcomes come from
+the unmodified reference (tests/golden/fixtures_golden.json, made by
+tests/golden/make_fixture_golden.py from oracle/_ref):
+
+* every `-- expect: error E-code` file fails with that code (the reference
+  front end, compiled unmodified into libdexlet_cuda.so, raises it before any
+  device work -- CPU test);
+* every first-order `-- expect: ok` file lowers (CPU test) and evaluates on the
+  device to the reference's values: floats within rtMaxRelDiff 1e-4 (f32) /
+  1e-9 (f64 parity mode), integers and indices bit-exact (GPU test).
+  ok_table_of_functions returns a table of closures, which has no device
+  representation (outputs are flat leaves); it is excluded and checked to fail
+  loudly instead."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_05372_b200 as dx
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+with open(os.path.join(HERE, "golden", "fixtures_golden.json")) as f:
+    FIXTURES = json.load(f)
+HIGHER_ORDER = {"ok_table_of_functions"}
+OK = sorted(k for k, v in FIXTURES.items() if v["expect"].startswith("ok") and k not in HIGHER_ORDER)
+BAD = sorted(k for k, v in FIXTURES.items() if v["expect"].startswith("error"))
+
+
+def test_corpus_is_complete():
+    assert len(FIXTURES) == 50 and len(OK) == 33 and len(BAD) == 16
+
+
+@pytest.mark.parametrize("name", BAD)
+def test_error_fixtures_raise_the_reference_code(name):
+    case = FIXTURES[name]
+    code = case["expect"].split()[1]
+    assert code in case["error"]  # the reference itself agrees with the header
+    with pytest.raises(dx.DexError) as e:
+        dx.Program(case["source"], entry="", ctx=None)
+    assert code in str(e.value), (name, str(e.value))
+
+
+@pytest.mark.parametrize("name", OK)
+def test_ok_fixtures_lower(name):
+    prog = dx.Program(FIXTURES[name]["source"], entry="", ctx=None)
+    assert prog.plan.startswith("plan:")
+
+
+def test_function_valued_result_fails_loudly():
+    with pytest.raises(dx.DexError):
+        dx.Program(FIXTURES["ok_table_of_functions"]["source"], entry="", ctx=None)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", OK)
+@pytest.mark.parametrize("f64", [False, True], ids=["f32", "f64"])
+def test_ok_fixtures_on_device(ctx, name, f64):
+    case = FIXTURES[name]
+    got = dx.Program(case["source"], entry="", ctx=ctx, float64=f64)()
+    assert len(got) == len(case["outputs"]), name
+    for g, w, kind in zip(got, case["outputs"], case["output_kinds"]):
+        w = np.asarray(w, dtype=np.float64)
+        if kind == "float":
+            assert oracle.rel_diff(g, w) <= (1e-9 if f64 else 1e-4), (name, g, w)
+        else:
+            np.testing.assert_array_equal(np.asarray(g, dtype=np.int64), w.astype(np.int64))
