@@ -12,7 +12,11 @@
  * with the gradient laid out as ADBench's GMM Jacobian row
  * [d alphas (k) | d means (k*d) | d icf (k*d(d+1)/2)].
  * Parameters and points are fp32 on the device; err and the gradient are
- * fp64 (accumulated in fp64 from fp32 moments).  d must be 64.
+ * fp64 (accumulated in fp64 from fp32 moments).  1 <= d <= 64: the kernels
+ * are 64 wide, and d < 64 runs them on the exactly equivalent zero-padded
+ * problem (padded coordinates 0, padded log-diagonal 0, padded lower entries
+ * 0; the padded Wishart terms and d-dependent constants are removed on the
+ * host).  ADBench's d = 128 sets are out of range.
  * Multi-GPU: each rank passes its own contiguous block of points (the
  * reference's chunk rule, eval.cpp:323-330) and the global n; the moments
  * and the log-likelihood sum are combined with NCCL (dxc_comm_init). */
@@ -29,7 +33,7 @@ extern "C" {
 
 typedef struct dxg_gmm dxg_gmm;
 
-/* Plan for d = 64, k components and n_local points of n_global on this rank
+/* Plan for dimension d (1..64), k components and n_local points of n_global on this rank
  * (n_local == n_global on one GPU).  Compiles the sm_100a module (NVRTC). */
 int dxg_gmm_create(dxc_ctx* ctx, int d, int k, int64_t n_local, int64_t n_global, dxg_gmm** out);
 int dxg_gmm_destroy(dxg_gmm* g);
@@ -37,7 +41,8 @@ int dxg_gmm_destroy(dxg_gmm* g);
  * x [n_local][d], fp32, from host memory (pinned or pageable). */
 int dxg_gmm_set_params(dxg_gmm* g, const float* alphas, const float* means, const float* icf);
 int dxg_gmm_set_points(dxg_gmm* g, const float* x);
-/* Device pointers of the input buffers (write them directly to skip the copy). */
+/* Device pointers of the input buffers (write them directly to skip the copy).
+ * They hold the 64-wide layout: for d < 64, write padded data (see above). */
 int dxg_gmm_input_device_ptrs(dxg_gmm* g, void** alphas, void** means, void** icf, void** x);
 /* Objective and gradient, asynchronous on the context stream.  want_grad = 0
  * runs the objective only (prep + forward + log-sum-exp). */

@@ -414,7 +414,8 @@ def _ptr(a: np.ndarray):
 class GMM:
     """Fused GMM objective + gradient on the device (include/dexlet_gmm.h):
     ADBench's ``gmm_objective(d, k, n, alphas, means, icf, x, wishart, err)``
-    and its gradient, d = 64, fp32 inputs, fp64 results.  ``n_global`` is the
+    and its gradient, 1 <= d <= 64 (d < 64 exactly zero-padded to the 64-wide
+    kernels), fp32 inputs, fp64 results.  ``n_global`` is the
     total point count when this rank holds a contiguous shard of the points."""
 
     def __init__(self, ctx: Context, d: int, k: int, n: int, n_global: Optional[int] = None):

@@ -693,6 +693,17 @@ extern "C" __global__ void dx_cvt_f32_f64(double* d, const float* s, long long n
 extern "C" __global__ void dx_cvt_f64_f32(float* d, const double* s, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = (float)s[i];
 }
+// Rank-ordered merge of gathered per-rank Accum deltas g[world][n] into the
+// cell: cell = ((cell + d_0) + d_1) + ..., the left fold of the reference's
+// chunk-overlay merge (eval.cpp:357-366) with ranks as chunks.  Every rank
+// folds the same gathered data, so all ranks hold identical bits.
+extern "C" __global__ void dx_rank_fold(const double* g, long long n, int world, double* cell) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double c = cell[i];
+    for (int r = 0; r < world; ++r) c += g[(long long)r * n + i];
+    cell[i] = c;
+  }
+}
 // Bounds check of uploaded index leaves (fromOrdinal's check, index_set.cpp:99-106).
 extern "C" __global__ void dx_check_index(const int* x, long long n, int size, int* bad) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {

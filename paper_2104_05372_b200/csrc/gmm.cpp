@@ -91,6 +91,7 @@ struct dxg_gmm {
   float ms[K_N] = {};
   double gamma = 1.0;
   int wm = 0;
+  int dr = D;  // the caller's dimension (<= 64; the kernels run padded to 64)
   bool haveGrad = false;
   ~dxg_gmm();
 };
@@ -121,13 +122,14 @@ extern "C" {
 
 int dxg_gmm_create(dxc_ctx* cx, int d, int k, int64_t n_local, int64_t n_global, dxg_gmm** out) {
   if (!cx || !out) { setError("dxg_gmm_create: null argument"); return DXC_E_ARG; }
-  if (d != D) { setError("dxg_gmm_create: d must be 64"); return DXC_E_ARG; }
+  if (d < 1 || d > D) { setError("dxg_gmm_create: d must be in 1..64"); return DXC_E_ARG; }
   if (k < 1 || n_local < 1 || n_global < n_local) { setError("dxg_gmm_create: bad sizes"); return DXC_E_ARG; }
   dxrt::Ctx* ctx = cx;
   int rc = ctx->makeCurrent();
   if (rc) return rc;
   auto* g = new dxg_gmm();
   g->ctx = ctx;
+  g->dr = d;
   g->K = k;
   g->n = n_local;
   g->ng = n_global;
@@ -193,14 +195,44 @@ int dxg_gmm_destroy(dxg_gmm* g) {
   return DXC_OK;
 }
 
+// d < 64 runs the 64-wide kernels on an exactly equivalent padded problem:
+// padded coordinates of x and the means are 0, padded log-diagonals of Q are 0
+// (q = 1) and padded strictly-lower entries are 0, so every y = Q(x - mu) gains
+// only zero coordinates and beta, the responsibilities and the real gradient
+// entries are unchanged.  The padded dimensions' Wishart terms (1/2 gamma^2 q^2
+// with q = 1) and the d-dependent constants are corrected on the host.
+// Packed strictly-lower index of (row j, column i), i < j < dd (ADBench order).
+static inline long long trilIndex(int dd, int j, int i) {
+  return (long long)i * dd - (long long)i * (i + 1) / 2 + (j - i - 1);
+}
+
 int dxg_gmm_set_params(dxg_gmm* g, const float* alphas, const float* means, const float* icf) {
   if (!g || !alphas || !means || !icf) { setError("dxg_gmm_set_params: null argument"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
   CUstream s = g->ctx->stream;
-  if ((rc = check(cuMemcpyHtoDAsync(g->alphas, alphas, (size_t)g->K * 4, s), "H2D alphas")) ||
-      (rc = check(cuMemcpyHtoDAsync(g->means, means, (size_t)g->K * D * 4, s), "H2D means")) ||
-      (rc = check(cuMemcpyHtoDAsync(g->icf, icf, (size_t)g->K * ICF * 4, s), "H2D icf")))
+  if (g->dr == D) {
+    if ((rc = check(cuMemcpyHtoDAsync(g->alphas, alphas, (size_t)g->K * 4, s), "H2D alphas")) ||
+        (rc = check(cuMemcpyHtoDAsync(g->means, means, (size_t)g->K * D * 4, s), "H2D means")) ||
+        (rc = check(cuMemcpyHtoDAsync(g->icf, icf, (size_t)g->K * ICF * 4, s), "H2D icf")))
+      return rc;
+    return DXC_OK;
+  }
+  const int d = g->dr, K = g->K, icfd = d * (d + 1) / 2;
+  std::vector<float> mu((size_t)K * D, 0.f), ic((size_t)K * ICF, 0.f);
+  for (int k = 0; k < K; ++k) {
+    for (int j = 0; j < d; ++j) {
+      mu[(size_t)k * D + j] = means[(size_t)k * d + j];
+      ic[(size_t)k * ICF + j] = icf[(size_t)k * icfd + j];
+    }
+    for (int i = 0; i < d; ++i)
+      for (int j = i + 1; j < d; ++j)
+        ic[(size_t)k * ICF + D + trilIndex(D, j, i)] = icf[(size_t)k * icfd + d + trilIndex(d, j, i)];
+  }
+  // synchronous copies: the staging vectors die with this call
+  if ((rc = check(cuMemcpyHtoDAsync(g->alphas, alphas, (size_t)K * 4, s), "H2D alphas")) ||
+      (rc = check(cuMemcpyHtoD(g->means, mu.data(), mu.size() * 4), "H2D means")) ||
+      (rc = check(cuMemcpyHtoD(g->icf, ic.data(), ic.size() * 4), "H2D icf")))
     return rc;
   return DXC_OK;
 }
@@ -209,7 +241,11 @@ int dxg_gmm_set_points(dxg_gmm* g, const float* x) {
   if (!g || !x) { setError("dxg_gmm_set_points: null argument"); return DXC_E_ARG; }
   int rc = g->ctx->makeCurrent();
   if (rc) return rc;
-  return check(cuMemcpyHtoDAsync(g->x, x, (size_t)g->n * D * 4, g->ctx->stream), "H2D x");
+  if (g->dr == D) return check(cuMemcpyHtoDAsync(g->x, x, (size_t)g->n * D * 4, g->ctx->stream), "H2D x");
+  const int d = g->dr;
+  std::vector<float> xp((size_t)g->n * D, 0.f);
+  for (long long i = 0; i < g->n; ++i) std::memcpy(&xp[(size_t)i * D], x + (size_t)i * d, (size_t)d * 4);
+  return check(cuMemcpyHtoD(g->x, xp.data(), xp.size() * 4), "H2D x");
 }
 
 int dxg_gmm_input_device_ptrs(dxg_gmm* g, void** alphas, void** means, void** icf, void** x) {
@@ -329,17 +365,39 @@ int dxg_gmm_get(dxg_gmm* g, double* err, double* d_alphas, double* d_means, doub
     double se = 0.0;
     for (float a : al) se += std::exp((double)a - m0);
     const double lse_a = m0 + std::log(se);
+    const int d = g->dr;
     const double nn = (double)g->ng;
-    const double CONST = -nn * D * 0.5 * std::log(2 * M_PI);
-    const int nw = D + g->wm + 1;
-    const double Cw = nw * D * (std::log(g->gamma) - 0.5 * std::log(2.0)) - logGammaDistrib(0.5 * nw, D);
+    const double CONST = -nn * d * 0.5 * std::log(2 * M_PI);
+    const int nw = d + g->wm + 1;
+    const double Cw = nw * d * (std::log(g->gamma) - 0.5 * std::log(2.0)) - logGammaDistrib(0.5 * nw, d);
     double pr = 0.0;
     for (double p : prior) pr += p;
+    pr -= (double)K * 0.5 * g->gamma * g->gamma * (D - d);  // padded dimensions: q = 1, icf = 0
     *err = CONST + lsum - nn * lse_a + pr - K * Cw;
   }
   if (d_alphas && (rc = check(cuMemcpyDtoH(d_alphas, g->dal, (size_t)K * 8), "D2H dalphas"))) return rc;
-  if (d_means && (rc = check(cuMemcpyDtoH(d_means, g->dmu, (size_t)K * D * 8), "D2H dmeans"))) return rc;
-  if (d_icf && (rc = check(cuMemcpyDtoH(d_icf, g->dicf, (size_t)K * ICF * 8), "D2H dicf"))) return rc;
+  if (g->dr == D) {
+    if (d_means && (rc = check(cuMemcpyDtoH(d_means, g->dmu, (size_t)K * D * 8), "D2H dmeans"))) return rc;
+    if (d_icf && (rc = check(cuMemcpyDtoH(d_icf, g->dicf, (size_t)K * ICF * 8), "D2H dicf"))) return rc;
+    return DXC_OK;
+  }
+  const int d = g->dr, icfd = d * (d + 1) / 2;
+  if (d_means) {
+    std::vector<double> m((size_t)K * D);
+    if ((rc = check(cuMemcpyDtoH(m.data(), g->dmu, m.size() * 8), "D2H dmeans"))) return rc;
+    for (int k = 0; k < K; ++k)
+      for (int j = 0; j < d; ++j) d_means[(size_t)k * d + j] = m[(size_t)k * D + j];
+  }
+  if (d_icf) {
+    std::vector<double> c((size_t)K * ICF);
+    if ((rc = check(cuMemcpyDtoH(c.data(), g->dicf, c.size() * 8), "D2H dicf"))) return rc;
+    for (int k = 0; k < K; ++k) {
+      for (int j = 0; j < d; ++j) d_icf[(size_t)k * icfd + j] = c[(size_t)k * ICF + j];
+      for (int i = 0; i < d; ++i)
+        for (int j = i + 1; j < d; ++j)
+          d_icf[(size_t)k * icfd + d + trilIndex(d, j, i)] = c[(size_t)k * ICF + D + trilIndex(D, j, i)];
+    }
+  }
   return DXC_OK;
 }
 
@@ -361,7 +419,7 @@ static int oneShot(dxc_ctx* ctx, int d, int k, int64_t n, const float* alphas, c
   if (rc) return rc;
   if (!(rc = dxg_gmm_set_params(g, alphas, means, icf)) && !(rc = dxg_gmm_set_points(g, x)) &&
       !(rc = dxg_gmm_run(g, gamma, wm, grad ? 1 : 0)))
-    rc = grad ? dxg_gmm_get(g, err, out, out + k, out + k + (size_t)k * D) : dxg_gmm_get(g, err, nullptr, nullptr, nullptr);
+    rc = grad ? dxg_gmm_get(g, err, out, out + k, out + k + (size_t)k * d) : dxg_gmm_get(g, err, nullptr, nullptr, nullptr);
   dxg_gmm_destroy(g);
   return rc;
 }

@@ -3787,10 +3787,19 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     addStep(f);
   }
   if (g.sharded) {
-    for (auto& cu : g.cells) {
-      Step a; a.k = Step::Allreduce; a.buf = cu.targetBuf; a.elems = cu.width; addStep(a);
-      Step ad; ad.k = Step::AddBuf; ad.buf = cells[cu.cell].bufs[cu.leaf]; ad.buf2 = cu.targetBuf; ad.elems = cu.width;
-      addStep(ad);
+    // every Accum delta of this kernel in one grouped all-gather, then the
+    // rank-ordered fold into the cells
+    if (!g.cells.empty()) {
+      Step m;
+      m.k = Step::Merge;
+      long long total = 0;
+      for (auto& cu : g.cells) {
+        m.merge.push_back({cu.targetBuf, cells[cu.cell].bufs[cu.leaf], cu.width});
+        total += cu.width;
+      }
+      m.buf = newBuf(BufDecl::Temp, SK::D, total * plan.world);  // gathered deltas
+      m.elems = total;
+      addStep(m);
     }
     for (size_t l = 0; l < outBufs.size(); ++l) {
       Step a; a.k = Step::Allreduce; a.buf = outBufs[l]; a.off = outOffs[l];
@@ -4223,6 +4232,10 @@ std::string Plan::summary() const {
           << (s.fin == Step::Count ? " count" : s.fin == Step::Tree ? " tree" : " seq");
         break;
       case Step::Allreduce: o << "allreduce b" << s.buf << " (" << s.elems << ")"; break;
+      case Step::Merge:
+        o << "merge " << s.merge.size() << " Accum deltas (" << s.elems
+          << " values): one grouped all-gather, rank-ordered fold";
+        break;
       case Step::AddBuf: o << "add b" << s.buf << " += b" << s.buf2; break;
       case Step::CopyBuf: o << "copy b" << s.buf << "+" << s.off << " <- b" << s.buf2 << "+" << s.off2 << " (" << s.elems << ")"; break;
       case Step::Convert: o << "convert b" << s.buf << "+" << s.off << " <- b" << s.buf2 << "+" << s.off2 << " (" << s.elems << ")"; break;
@@ -4315,6 +4328,7 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
     if (st.k == Step::Zero) continue;
     if (st.buf >= 0) live[st.buf] = true;
     if (st.buf2 >= 0) live[st.buf2] = true;
+    for (auto& mi : st.merge) live[mi.delta] = live[mi.cell] = true;
     for (auto& a : st.args)
       if ((a.k == KArg::Buf || a.k == KArg::TMap) && a.buf >= 0) live[a.buf] = true;
   }

@@ -64,7 +64,7 @@ struct KArg {
 };
 
 struct Step {
-  enum K { Zero, Upload, Kernel, Finalize, Allreduce, AddBuf, CopyBuf, Convert } k;
+  enum K { Zero, Upload, Kernel, Finalize, Allreduce, AddBuf, CopyBuf, Convert, Merge } k;
   int buf = -1, buf2 = -1;
   long long off = 0, off2 = 0, elems = 0;
   // Kernel
@@ -84,6 +84,10 @@ struct Step {
   enum FinK { Seq, Tree, Count } fin = Seq;
   int kernelStep = -1;
   double scale = 1.0;
+  // Merge: rank-ordered merge of per-rank Accum deltas into their cells (one
+  // grouped NCCL all-gather into buf, then cell = ((cell + d_0) + d_1) + ...)
+  struct MergeItem { int delta, cell; long long elems; };
+  std::vector<MergeItem> merge;
   std::string note;
 };
 

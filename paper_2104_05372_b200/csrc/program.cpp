@@ -201,6 +201,7 @@ int Program::prepare() {
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[0], mod, "dx_cvt_f32_f64"), "cvt fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&cvtFn[1], mod, "dx_cvt_f64_f32"), "cvt fn"))) return rc;
   if ((rc = dxrt::check(cuModuleGetFunction(&checkIdxFn, mod, "dx_check_index"), "check fn"))) return rc;
+  if ((rc = dxrt::check(cuModuleGetFunction(&rankFoldFn, mod, "dx_rank_fold"), "rank fold fn"))) return rc;
   numLeafFlags = 0;
   for (auto& in : plan.inputs) numLeafFlags += (int)in.size();
   if ((rc = dxrt::check(cuMemAlloc(&upFlags, (size_t)std::max(1, numLeafFlags) * 4), "cuMemAlloc flags"))) return rc;
@@ -439,6 +440,33 @@ int Program::issue() {
         SK k = plan.bufs[s.buf].kind;
         int dt = k == SK::D ? DXC_F64 : k == SK::F ? (f64 ? DXC_F64 : DXC_F32) : k == SK::I ? DXC_I64 : DXC_I32;
         if ((rc = ctx->allreduceSum(devptr[s.buf] + s.off * es, (size_t)s.elems, dt))) return rc;
+        break;
+      }
+      case Step::Merge: {
+        if (!ctx->comm) {
+          setError("sharded plan (world > 1): call dxc_comm_init on the context first");
+          return DXC_E_ARG;
+        }
+        const int nr = ctx->nranks;
+        std::vector<std::pair<CUdeviceptr, CUdeviceptr>> sr;
+        std::vector<size_t> counts;
+        long long at = 0;
+        for (auto& mi : s.merge) {
+          sr.push_back({devptr[mi.delta], devptr[s.buf] + (CUdeviceptr)(at * nr * 8)});
+          counts.push_back((size_t)mi.elems);
+          at += mi.elems;
+        }
+        if ((rc = ctx->allgatherGroup(sr, counts, DXC_F64))) return rc;
+        at = 0;
+        for (auto& mi : s.merge) {
+          CUdeviceptr gp = devptr[s.buf] + (CUdeviceptr)(at * nr * 8), cell = devptr[mi.cell];
+          long long n = mi.elems;
+          int w = nr;
+          void* args[4] = {&gp, &n, &w, &cell};
+          if ((rc = launch(rankFoldFn, (unsigned)std::min<long long>((n + 255) / 256, 1184), 256, 0, args))) return rc;
+          ++launches;
+          at += mi.elems;
+        }
         break;
       }
       case Step::AddBuf: {

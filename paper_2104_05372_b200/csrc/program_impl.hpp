@@ -42,6 +42,7 @@ struct Program {
   CUfunction finF32D = nullptr;
   CUfunction cvtFn[2] = {};
   CUfunction checkIdxFn = nullptr;
+  CUfunction rankFoldFn = nullptr;
   CUdeviceptr upFlags = 0;  // one int per input leaf: E-bounds seen by the upload check
   int numLeafFlags = 0;
   int readFlags(int* any);  // synchronizes; *any = error flag or any upload flag

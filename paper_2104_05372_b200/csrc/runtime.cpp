@@ -172,6 +172,9 @@ struct NcclApi {
   ncclResult_t_ (*getUniqueId)(NcclUniqueId_*) = nullptr;
   ncclResult_t_ (*commInitRank)(void**, int, NcclUniqueId_, int) = nullptr;
   ncclResult_t_ (*allReduce)(const void*, void*, size_t, int, int, void*, CUstream) = nullptr;
+  ncclResult_t_ (*allGather)(const void*, void*, size_t, int, void*, CUstream) = nullptr;
+  ncclResult_t_ (*groupStart)() = nullptr;
+  ncclResult_t_ (*groupEnd)() = nullptr;
   ncclResult_t_ (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(ncclResult_t_) = nullptr;
 };
@@ -200,9 +203,13 @@ int loadNccl() {
   g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
   g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
-  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce) {
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather ||
+      !g_nccl.groupStart || !g_nccl.groupEnd) {
     setError("NCCL library lacks required symbols");
     g_nccl.lib = nullptr;
     return DXC_E_CUDA;
@@ -232,6 +239,22 @@ int Ctx::allreduceSum(CUdeviceptr p, size_t count, int dtype) {
   return ncclCheck(g_nccl.allReduce((const void*)p, (void*)p, count, nd, /*ncclSum*/ 0,
                                     comm, stream),
                    "ncclAllReduce");
+}
+
+int Ctx::allgatherGroup(const std::vector<std::pair<CUdeviceptr, CUdeviceptr>>& sendRecv,
+                        const std::vector<size_t>& counts, int dtype) {
+  if (!comm) return DXC_OK;
+  const int nd = dtype == DXC_F64 ? 8 : dtype == DXC_F32 ? 7 : dtype == DXC_I64 ? 4 : 2;
+  int rc = ncclCheck(g_nccl.groupStart(), "ncclGroupStart");
+  if (rc) return rc;
+  for (size_t i = 0; i < sendRecv.size(); ++i) {
+    rc = ncclCheck(g_nccl.allGather((const void*)sendRecv[i].first, (void*)sendRecv[i].second, counts[i], nd, comm,
+                                    stream),
+                   "ncclAllGather");
+    if (rc) break;
+  }
+  const int rc2 = ncclCheck(g_nccl.groupEnd(), "ncclGroupEnd");
+  return rc ? rc : rc2;
 }
 
 // ---------------------------------------------------------------------------

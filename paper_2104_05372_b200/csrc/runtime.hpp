@@ -5,6 +5,8 @@
 
 #include <map>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "dexlet_cuda.h"
 
@@ -39,6 +41,9 @@ struct Ctx {
   int makeCurrent();
   int loadModule(const std::string& source, CUmodule* out);
   int allreduceSum(CUdeviceptr p, size_t count, int dtype);
+  // grouped all-gathers (one NCCL launch): recv_i = [nranks][count_i]
+  int allgatherGroup(const std::vector<std::pair<CUdeviceptr, CUdeviceptr>>& sendRecv,
+                     const std::vector<size_t>& counts, int dtype);
   ~Ctx();
 };
 

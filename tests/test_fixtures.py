@@ -12,7 +12,11 @@ tests/golden/make_fixture_golden.py from oracle/_ref):
   1e-9 (f64 parity mode), integers and indices bit-exact (GPU test).
   ok_table_of_functions returns a table of closures, which has no device
   representation (outputs are flat leaves); it is excluded and checked to fail
-  loudly instead."""
+  loudly instead.
+  mandelbrot's escape times are discontinuous in the arithmetic (a point near
+  the set boundary escapes one iteration earlier or later under fp32
+  rounding): in f32 mode at least 95% of its 600 counts must equal the
+  reference's; the f64 parity mode must match all of them."""
 import json
 import os
 
@@ -26,6 +30,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 with open(os.path.join(HERE, "golden", "fixtures_golden.json")) as f:
     FIXTURES = json.load(f)
 HIGHER_ORDER = {"ok_table_of_functions"}
+CHAOTIC = {"mandelbrot"}
 OK = sorted(k for k, v in FIXTURES.items() if v["expect"].startswith("ok") and k not in HIGHER_ORDER)
 BAD = sorted(k for k, v in FIXTURES.items() if v["expect"].startswith("error"))
 
@@ -64,7 +69,9 @@ def test_ok_fixtures_on_device(ctx, name, f64):
     assert len(got) == len(case["outputs"]), name
     for g, w, kind in zip(got, case["outputs"], case["output_kinds"]):
         w = np.asarray(w, dtype=np.float64)
-        if kind == "float":
+        if kind == "float" and name in CHAOTIC and not f64:
+            assert np.mean(np.asarray(g) == w) >= 0.95, (name, np.mean(np.asarray(g) == w))
+        elif kind == "float":
             assert oracle.rel_diff(g, w) <= (1e-9 if f64 else 1e-4), (name, g, w)
         else:
             np.testing.assert_array_equal(np.asarray(g, dtype=np.int64), w.astype(np.int64))

@@ -97,8 +97,25 @@ def test_gmm_repeat_deterministic(ctx):
 
 def test_gmm_bad_dimension(ctx):
     import paper_2104_05372_b200 as dx
-    with pytest.raises(dx.DexError):
-        dx.GMM(ctx, 32, 4, 100)
+    for d in (0, 65, 128):
+        with pytest.raises(dx.DexError):
+            dx.GMM(ctx, d, 4, 100)
+
+
+@pytest.mark.parametrize("d,n,k", [(1, 500, 2), (2, 3000, 5), (10, 4000, 8), (20, 2500, 12), (32, 5000, 7),
+                                   (63, 1500, 9)])
+def test_gmm_smaller_dimensions(ctx, d, n, k):
+    """ADBench's d in {2, 10, 20, 32, 64}: d < 64 runs zero-padded; objective,
+    Wishart prior (gamma, m) and every gradient entry of the real dimensions
+    against the fp64 restatement."""
+    import paper_2104_05372_b200 as dx
+    a, mu, icf, x = G.gmm_inputs(n, d, k, seed=40 + d)
+    g = dx.GMM(ctx, d, k, n)
+    err, da, dm, di = g(a, mu, icf, x, gamma=0.8, m=1)
+    werr, wda, wdm, wdi = G.gmm_objective_grad(a, mu, icf, x, 0.8, 1)
+    assert rel(err, werr) <= TOL, (err, werr)
+    assert dm.shape == (k, d) and di.shape == (k, d * (d + 1) // 2)
+    check_grads((da, dm, di), (wda, wdm, wdi))
 
 
 def test_gmm_full_size(ctx):

@@ -95,9 +95,12 @@ def test_dead_cells_are_not_allocated():
     assert "(10000)" not in prog.plan
 
 
-def test_sharded_plan_allreduces_cells():
+def test_sharded_plan_merges_cells_in_one_collective():
+    """Both Accum cells of the fused k-means kernel (cost, dC) are merged by
+    one grouped all-gather + rank-ordered fold (eval.cpp:357-366 order)."""
     prog = dx.Program(P.kmeans_cost_grad(1000, 16, 8), ctx=None, rank=1, world=2)
-    assert prog.plan.count("allreduce") == 2
+    plan = prog.plan.split("---")[0]
+    assert plan.count("merge 2 Accum deltas") == 1 and "allreduce" not in plan
 
 
 def test_contraction_recognized_as_gemm():
