@@ -127,7 +127,15 @@ enum {
   DXL_F_TEST_COMM_MISMATCH = 8, /* TEST ONLY: run a (world, rank) plan over a
                                  * communicator of another size (one device
                                  * emulating the ranks); never in production */
-  DXL_F_NO_GEMM = 16       /* contractions through the generic SIMT lowering */
+  DXL_F_NO_GEMM = 16,      /* contractions through the generic SIMT lowering */
+  DXL_F_PIPELINE = 32      /* back-to-back runs may overlap: a kernel that
+                            * reads only program inputs streams them before
+                            * waiting (griddepcontrol.wait) for the previous
+                            * launch on the context stream.  The caller
+                            * promises that no kernel on that stream writes
+                            * the inputs while runs are in flight (host
+                            * uploads through set_input are stream-ordered
+                            * and always safe).                              */
 };
 
 /* Parse, typecheck, simplify, optimize and lower `entry` of `source`, where

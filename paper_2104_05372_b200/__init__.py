@@ -64,6 +64,14 @@ DXC_E_INTERNAL = 15
 DXC_E_CUDA = 100
 DXC_E_ARG = 101
 
+# dxl_options.flags (include/dexlet_cuda.h)
+DXL_F_NO_FUSION = 1
+DXL_F_NO_ROWSCATTER = 2
+DXL_F_DUMP = 4
+DXL_F_TEST_COMM_MISMATCH = 8
+DXL_F_NO_GEMM = 16
+DXL_F_PIPELINE = 32
+
 LEAF_FLOAT, LEAF_INT, LEAF_INDEX = 0, 1, 2
 DXC_F32, DXC_F64, DXC_I32, DXC_I64, DXC_U32 = 0, 1, 2, 3, 4
 

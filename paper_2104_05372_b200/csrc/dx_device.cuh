@@ -425,20 +425,20 @@ __device__ __forceinline__ void dx_warp_tab(const float* etile, int key, float* 
 // in that fixed order.
 template <int D, int K, int NW>
 __device__ __forceinline__ void dx_warp_tab_flush(const float* tabs, float* part) {
+  // warp w folds rows w, w + NW, ...: lane l sums word l of the row over the
+  // NW tables (conflict-free), then the G copies of a column are combined by
+  // an xor tree; fixed order, every warp busy
   constexpr int G = 32 / D;
+  static_assert(G >= 1, "row width");
   __syncthreads();
-  // float4 columns: entry quad (k, 4q..4q+3)
-  for (int e = threadIdx.x; e < K * D / 4; e += blockDim.x) {
-    const int k = e / (D / 4), j = 4 * (e - k * (D / 4));
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < K; k += NW) {
+    float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w)
+    for (int w = 0; w < NW; ++w) s += tabs[(w * (K + 1) + k) * 32 + lane];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float4 v = *reinterpret_cast<const float4*>(tabs + (w * (K + 1) + k) * 32 + g * D + j);
-        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-      }
-    *reinterpret_cast<float4*>(part + k * D + j) = s;
+    for (int o = D; o < 32; o <<= 1) s += __shfl_xor_sync(DX_FULL, s, o);
+    if (lane < D) part[k * D + lane] = s;
   }
 }
 
@@ -600,6 +600,177 @@ __device__ __forceinline__ void dx_grid_barrier(unsigned* bar) {
     __threadfence();
   }
   __syncthreads();
+}
+// Programmatic dependent launch: a kernel launched with the PDL attribute
+// may start while its predecessor on the stream drains; it waits here before
+// touching anything that predecessor may write.  No-ops without PDL.
+__device__ __forceinline__ void dx_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void dx_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Streaming (evict-first) loads for rows read once.
+__device__ __forceinline__ float dx_ldcs(const float* p) {
+  float v;
+  asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double dx_ldcs(const double* p) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int dx_ldcs(const int* p) {
+  int v;
+  asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ long long dx_ldcs(const long long* p) {
+  long long v;
+  asm volatile("ld.global.cs.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// Group sum over the G lanes sharing an ordinal (group mode): fixed xor tree.
+template <int G, class T>
+__device__ __forceinline__ T dx_grp_sum(T v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(DX_FULL, v, o);
+  return v;
+}
+
+// ... the same over the active group only (the ragged chunk, where a group
+// past the end skips its ordinal: the guard is uniform within a group).
+template <int G, class T>
+__device__ __forceinline__ T dx_grp_sum_m(T v) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned m = (G == 32) ? DX_FULL : (((1u << G) - 1u) << (lane & ~(unsigned)(G - 1)));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+  return v;
+}
+
+// Grid barrier on a 64-bit ticket counter (one atomic per block; never
+// wraps in practice: 2^64 arrivals).  All launches of a kernel on one
+// counter use the same grid, so the counter is a multiple of the grid at
+// every launch start.  Requires every block to be resident.
+__device__ __forceinline__ void dx_ticket_barrier(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (t / gridDim.x + 1ull) * gridDim.x;
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// Block-per-column-group fold of per-block partials [nblk][width] into
+// `cell`: block bk takes groups of 32 consecutive columns (lane = column, so
+// every load is one coalesced 128-byte line); its warps split the partial
+// rows (warp w sums rows w, w + NW, ... in order), then warp 0 adds the NW
+// warp sums in order.  Groups of several cells share one index space
+// (`first` = groups of the cells before).  Deterministic for a fixed grid.
+template <class T, class P>
+__device__ __forceinline__ void dx_coop_fold_b(const P* part, long long width, T scale, T* cell, bool counts,
+                                               bool store, long long first) {
+  __shared__ __align__(8) unsigned char fraw[32 * 33 * 8];
+  T (*fred)[33] = reinterpret_cast<T (*)[33]>(fraw);
+  unsigned long long (*fredu)[33] = reinterpret_cast<unsigned long long (*)[33]>(fraw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nblk = gridDim.x;
+  const long long ng = (width + 31) / 32;
+  for (long long gi = ((long long)blockIdx.x - first % nblk + nblk) % nblk; gi < ng; gi += nblk) {
+    const long long c = gi * 32 + lane;
+    const bool ok = c < width;
+    T s = T(0);
+    unsigned long long u = 0;
+    for (int b0 = warp; b0 < nblk; b0 += 8 * nw) {
+      P x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int b = b0 + r * nw;
+        x[r] = (ok && b < nblk) ? dx_ldcg(part + (long long)b * width + c) : P(0);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (counts) u += (unsigned long long)x[r];
+        else s += (T)x[r];
+      }
+    }
+    if (counts) fredu[warp][lane] = u;
+    else fred[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && ok) {
+      T v;
+      if (counts) {
+        unsigned long long t = 0;
+        for (int w = 0; w < nw; ++w) t += fredu[w][lane];
+        v = (T)t * scale;
+      } else {
+        T t = T(0);
+        for (int w = 0; w < nw; ++w) t += fred[w][lane];
+        v = t;
+      }
+      if (store) cell[c] = v;  // the cell's zero-fill was folded into this kernel
+      else cell[c] += v;
+    }
+    __syncthreads();
+  }
+}
+
+// Warp-per-column fold of per-block partials [nblk][width] into `cell`:
+// global warp w folds columns w, w + W, ...; lanes take blocks lane, lane +
+// 32, ... in order, then the fixed xor tree.  Deterministic for a fixed grid.
+template <class T, class P>
+__device__ __forceinline__ void dx_coop_fold_w(const P* part, long long width, T scale, T* cell, bool counts,
+                                               bool store, long long first) {
+  // columns of several cells share one index space: this cell's column c is
+  // folded by global warp (first + c) mod (number of warps)
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  const int nblk = gridDim.x;
+  const long long me = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  long long c0 = (me - first % nw + nw) % nw;
+  for (long long c = c0; c < width; c += nw) {
+    // eight loads in flight per lane (one L2 round trip for grids <= 256
+    // blocks), then the lane's blocks in ascending order, then the xor tree
+    T v;
+    if (counts) {
+      unsigned long long u = 0;
+      for (int b0 = 0; b0 < nblk; b0 += 256) {
+        P x[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int b = b0 + lane + 32 * r;
+          x[r] = b < nblk ? dx_ldcg(part + (long long)b * width + c) : P(0);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) u += (unsigned long long)x[r];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(DX_FULL, u, o);
+      v = (T)u * scale;
+    } else {
+      T s = T(0);
+      for (int b0 = 0; b0 < nblk; b0 += 256) {
+        P x[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int b = b0 + lane + 32 * r;
+          x[r] = b < nblk ? dx_ldcg(part + (long long)b * width + c) : P(0);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) s += (T)x[r];
+      }
+      v = dx_warp_sum(s);
+    }
+    if (lane == 0) {
+      if (store) cell[c] = v;  // the cell's zero-fill was folded into this kernel
+      else cell[c] += v;
+    }
+  }
 }
 // Cooperative fold of per-block partials [nblk][width] into `cell`: block b
 // owns columns [8b, 8b+8); thread (c, g) sums rows g, g+R, ... in order, then a

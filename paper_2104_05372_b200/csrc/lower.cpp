@@ -312,6 +312,7 @@ struct Slot {
   // so the tile kernel can fetch the block's rows by TMA into shared memory.
   bool stream = false;
   long long streamL = 0, streamBase = 0;
+  int streamU = 0;     // which of the thread's U ordinals (dx_o<u>)
   std::string rowOff;
 };
 
@@ -364,6 +365,7 @@ struct KVal {
   long long ci = 0;
   int loopId = -1;    // Idx: exactly loop var (or its reverse) of this loop
   std::string rev;    // Idx: cheaper expression of the reverse, if known
+  std::string grpPart;  // group mode: e sums this local cell's per-lane partials (see closeLoop)
   KV a, b;
   std::vector<Slot> slots;  // Table / Ref, per leaf
   int cell = -1;            // Ref: plan cell (global) or -1 (local)
@@ -477,6 +479,38 @@ struct KGen {
   bool warpRow = false;           // pass 1: emit in warp-per-ordinal mode
   bool inLaneLoop = false;        // pass 1: inside the lane loop's body
   std::set<std::string> innerCells, laneCells;  // local cells created in / reduced after the lane loop
+  // Group mode (sub-warp per ordinal) for kernels whose in-thread loops all
+  // run over one short index set of G = D members (k-means rows, D | 32):
+  // G lanes share an ordinal, every depth-1 loop becomes "lane gl of the
+  // group runs iteration gl", row scatters r!key!j become conflict-free
+  // warp-private table updates, and the rows read at the ordinal stream in
+  // coalesced (128 bytes per warp instruction) through a double-buffered
+  // register prefetch.  Pass 0 decides eligibility; pass 1 emits.
+  bool grpOK = true;              // pass 0: nothing disqualifies the mode
+  long long grpTrip = 0;          // pass 0: trip of the depth-1 loops
+  int grp = 0;                    // pass 1: G (0 = thread per ordinal)
+  int grpU = 1;                   // pass 1: ordinals per group per chunk
+  std::map<std::string, int> localDepth;      // local array -> loop depth at creation
+  std::vector<std::set<std::string>> grpFresh; // per open lane loop: fresh scalar cells at entry
+  std::vector<std::set<std::string>> grpSum;   // per open lane loop: outer cells to group-sum after it
+  // stream rows read at (ordinal, lane column): the skeleton prefetches them
+  // into registers gp<id>_<u> (pass 1), double-buffered across chunks
+  struct GrpStream {
+    int buf;
+    long long L, base;
+    std::string col;  // column expression in dx_gl
+    SK kind;
+    long long chk;    // index leaf of an input: range-checked (E-bounds) when prefetched
+  };
+  std::vector<GrpStream> grpStreams;
+  std::set<int> grpStreamBad;
+  int grpRowCell = -1;            // pass 1: the row cell's CellUse index
+  std::map<std::string, KV> instMemo;  // kernel-level lazy instantiations of this iteration
+  bool hasBranch = false;         // pass 0: the body branches (keeps group sums eager)
+  std::map<std::string, int> grpPending;  // local cells holding per-lane partials (sum deferred)
+  std::string curLaneVar;         // variable of the open depth-1 loop
+  bool curLaneRev = false;        // ... which runs lane gl on iteration n-1-gl
+  std::map<std::string, int> grpStreamId;  // "buf|column" -> prefetch stream id (pass 0 order)
 
   explicit KGen(Lowering& l) : L(l) {}
 
@@ -1701,7 +1735,7 @@ class Lowering {
         // Small contiguous rows of read-only HBM tables are fetched whole with
         // 16-byte loads into registers (nvcc does not vectorize the scalar
         // per-column loads itself); the row's columns are then register reads.
-        if (numLeaves(t) == 1 && slots[base].global && slots[base].ro && slots[base].kind != SK::X &&
+        if (g.grp == 0 && numLeaves(t) == 1 && slots[base].global && slots[base].ro && slots[base].kind != SK::X &&
             t->a->k != DType::Table && t->a->k != DType::Pair) {
           const Slot& s0 = slots[base];
           long long cnt = leaves(t)[0].count;
@@ -1763,6 +1797,12 @@ class Lowering {
       case DType::Float:
       case DType::Int: {
         const Slot& s = slots[base];
+        if (!s.global && s.off == "0" && g.grpPending.count(s.base)) {
+          auto k = std::const_pointer_cast<KVal>(
+              kScalar(t, "dx_grp_sum<" + lit(g.grpPending[s.base]) + ">(" + s.base + "[0])", s.level));
+          k->grpPart = s.base;
+          return k;
+        }
         std::string v = g.fresh("v");
         std::string ld = (s.global && s.ro) ? "dx_ld(" + s.base + " + " + s.off + ")"
                                             : s.base + "[" + s.off + "]";
@@ -1785,10 +1825,36 @@ class Lowering {
           // streaming read at the thread's own ordinal: served by the
           // per-thread vector prefetch of the U ordinals (see emitKernel)
           g.streamBufs.insert(s.buf);
-          if (g.pass == 1 && g.U > 1) ld = "pf" + std::to_string(s.buf) + "_" + s.off.substr(4);
+          if (g.pass == 1 && g.U > 1 && g.grp == 0) ld = "pf" + std::to_string(s.buf) + "_" + s.off.substr(4);
+        }
+        bool prechecked = false;
+        if (!g.serial && s.global && s.ro && s.stream && !opt.f64) {
+          // group mode: a row element read at (ordinal, column) where the
+          // column is a literal or the lane loop's variable (or its reverse)
+          // is served by the chunk prefetch registers gp<id>_<u>
+          std::string col;
+          long long cv;
+          const std::string fwd = "dx_gl", bwd = "(" + lit(g.grpTrip - 1) + " - dx_gl)";
+          if (isIntLit(s.rowOff, &cv)) col = lit(cv);
+          else if (s.rowOff == "dx_gl") col = fwd;
+          else if (!g.curLaneVar.empty() && s.rowOff == g.curLaneVar) col = g.curLaneRev ? bwd : fwd;
+          else if (!g.curLaneVar.empty() && g.grpTrip > 0 && s.rowOff == "(" + lit(g.grpTrip - 1) + "LL - " + g.curLaneVar + ")")
+            col = g.curLaneRev ? fwd : bwd;
+          if (!col.empty()) {
+            const std::string key = std::to_string(s.buf) + "|" + col;
+            auto it = g.grpStreamId.find(key);
+            if (g.pass == 0 && it == g.grpStreamId.end()) {
+              g.grpStreamId[key] = (int)g.grpStreams.size();
+              const long long chk = (t->k == DType::Idx && s.input) ? size(t->desc) : 0;
+              g.grpStreams.push_back({s.buf, s.streamL, s.streamBase, col, s.kind, chk});
+            } else if (g.pass == 1 && g.grp > 0 && it != g.grpStreamId.end()) {
+              ld = "gp" + std::to_string(it->second) + "_" + std::to_string(s.streamU);
+              if (g.grpStreams[it->second].chk > 0) prechecked = true;
+            }
+          }
         }
         g.line((t->k == DType::Float ? std::string("dx_f") : ctype(s.kind)) + " " + v + " = " + ld + ";");
-        if (t->k == DType::Idx && s.input) {
+        if (t->k == DType::Idx && s.input && !prechecked) {
           g.usesErr = true;
           g.line(v + " = dx_chk_idx(" + v + ", " + lit(size(t->desc)) + ", dx_bad);");
         }
@@ -1950,6 +2016,7 @@ class Lowering {
       s.base = nm + "_" + std::to_string(l);
       s.off = "0";
       s.kind = lv[l].kind;
+      g.localDepth[s.base] = g.serial ? 0 : g.depth();
       g.line(ctype(s.kind) + " " + s.base + "[" + lit(std::max(1LL, (long long)lv[l].count)) + "]" + (zero ? " = {}" : "") + ";");
       slots.push_back(s);
     }
@@ -2002,8 +2069,16 @@ class Lowering {
         long long n = size(lz->desc);
         std::string q = g.fresh("m");
         int id = openLoop(g, n);
-        g.line(std::string(n <= 32 ? "#pragma unroll\n" : "") + std::string(g.ind * 2, ' ') +
-               "for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
+        if (g.loopDepth[id] == 1) g.curLaneVar = q;
+        // group mode: materializing into a local table from a lane loop
+        // would leave each lane with one element of it
+        if (g.pass == 0 && g.loopDepth[id] == 1)
+          for (size_t l = base; l < slots.size(); ++l)
+            if (!slots[l].global) g.grpOK = false;
+        if (laneLoop(g, id)) g.line(loopHead(g, id, q, n));
+        else
+          g.line(std::string(n <= 32 ? "#pragma unroll\n" : "") + std::string(g.ind * 2, ' ') +
+                 "for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
         g.ind++;
         KV idx = fromOrdinalK(g, q, lz->desc, g.loopDepth[id], id, eSub(n - 1, q));
         KV elem = instantiate(g, v, idx);
@@ -2025,9 +2100,50 @@ class Lowering {
     g.loopDepth[id] = (int)g.loopStack.size() - (int)g.kernelVars.size() + 1;
     g.loopTrip[id] = trip;
     g.loopStack.push_back(id);
+    if (g.loopDepth[id] == 1 && !g.serial) {
+      if (g.pass == 0) {
+        if (g.grpTrip == 0) g.grpTrip = trip;
+        else if (g.grpTrip != trip) g.grpOK = false;
+      }
+      // every lane loop: the scalar cells that are still zero at its entry
+      std::set<std::string> fresh;
+      for (auto& [b, d] : g.freshCell) fresh.insert(b);
+      g.grpFresh.push_back(fresh);
+      g.grpSum.emplace_back();
+    }
     return id;
   }
-  void closeLoop(KGen& g) { g.loopStack.pop_back(); }
+  // Group mode: the loop at depth 1 is a lane loop (one iteration per lane).
+  bool laneLoop(KGen& g, int id) const { return g.grp > 0 && g.loopDepth.at(id) == 1; }
+  // Header of a depth-1 loop: a C for loop, or in group mode the lane's own
+  // iteration.
+  std::string loopHead(KGen& g, int id, const std::string& q, long long n, const std::string& ty = "int",
+                       bool rev = false) {
+    // a loop indexed only through `reverse` runs lane gl on iteration n-1-gl,
+    // so its reversed index (the one the body uses) is the lane itself
+    if (laneLoop(g, id)) return "{ const " + ty + " " + q + " = " + (rev ? lit(n - 1) + " - dx_gl" : "dx_gl") + ";";
+    return "for (" + ty + " " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {";
+  }
+  void closeLoop(KGen& g) {
+    const int id = g.loopStack.back();
+    if (!g.serial && g.loopDepth[id] == 1 && !g.grpSum.empty()) {
+      // group mode: outer scalar cells accumulated by the lanes are summed
+      // over the group (fixed xor tree) once the lane loop is done
+      // Without branches in the body every read of the cell is convergent:
+      // the sum is deferred to the reads (a read that only feeds a scalar
+      // Accum cell adds the lane partials instead, see accumScalar)
+      if (g.grp > 0)
+        for (const std::string& c : g.grpSum.back()) {
+          if (g.hasBranch) g.line(c + "[0] = dx_grp_sum<" + lit(g.grp) + ">(" + c + "[0]);");
+          else g.grpPending[c] = g.grp;
+        }
+      g.grpFresh.pop_back();
+      g.grpSum.pop_back();
+      g.curLaneVar.clear();
+      g.curLaneRev = false;
+    }
+    g.loopStack.pop_back();
+  }
 
   // Instantiate a lazy table at index `idx`.
   KV instantiate(KGen& g, const KV& lzv, const KV& idx) {
@@ -2058,8 +2174,10 @@ class Lowering {
         long long b0;
         if (slots[l].stream) {
           slots[l].rowOff = eAdd(slots[l].rowOff, eMul(o, el[l].count));
-        } else if (slots[l].global && slots[l].ro && o == "dx_o0" && isIntLit(slots[l].off, &b0)) {
+        } else if (slots[l].global && slots[l].ro && isIntLit(slots[l].off, &b0) &&
+                   (o == "dx_o0" || (g.grp > 0 && o.rfind("dx_o", 0) == 0 && isIntLit(o.substr(4))))) {
           slots[l].stream = true;
+          slots[l].streamU = std::stoi(o.substr(4));
           slots[l].streamL = el[l].count;
           slots[l].streamBase = b0;
           slots[l].rowOff = "0";
@@ -2105,6 +2223,28 @@ class Lowering {
         if (!g.matLocal.count(lz->key)) {
           g.matLocal.insert(lz->key);
           g.redo = true;
+        }
+      }
+      // the same pure lazy element instantiated twice at kernel level in one
+      // iteration (a forward tape read by the fused forward and transposed
+      // loops) is computed once: its variables are in scope for the rest of
+      // the iteration's block
+      if (!g.serial && !s.inBranch && g.depth() == 0) {
+        std::function<std::string(const KV&)> ik = [&](const KV& x) -> std::string {
+          if (x->k == KVal::Scalar) return x->e;
+          if (x->k == KVal::Pair) return "(" + ik(x->a) + "," + ik(x->b) + ")";
+          if (x->k == KVal::Unit) return "()";
+          return "";
+        };
+        const std::string ix = ik(idx);
+        if (!ix.empty()) {
+          const void* who = lz->hostOrigin ? (const void*)lz->hostOrigin.get() : (const void*)lz.get();
+          const std::string key = std::to_string((unsigned long long)(uintptr_t)who) + "@" + ix;
+          auto it = g.instMemo.find(key);
+          if (it != g.instMemo.end()) return it->second;
+          KV r = instantiate(g, arr, idx);
+          g.instMemo[key] = r;
+          return r;
         }
       }
       return instantiate(g, arr, idx);
@@ -2270,6 +2410,8 @@ class Lowering {
     // Emit the loop body into a side buffer first to learn the element type.
     std::string q = g.fresh("j");
     int id = openLoop(g, n);
+    const bool laneRev = g.loopDepth[id] == 1 && onlyReversed(f.binder, f.body);
+    if (g.loopDepth[id] == 1) { g.curLaneVar = q; g.curLaneRev = laneRev; }
     const bool cand = g.pass == 0 && g.loopDepth[id] == 1 && n >= 64 && g.laneLoopId < 0 && !g.inCand;
     const bool lane = g.pass == 1 && g.warpRow && id == g.laneLoopId;
     if (cand) { g.inCand = true; g.innerCells.clear(); }
@@ -2282,7 +2424,8 @@ class Lowering {
     g.ind = savedInd + 1;
     KScope bs = s;
     bs.covered.insert(id);
-    KV idx = fromOrdinalK(g, q, d, g.loopDepth[id], id, eSub(n - 1, q));
+    // a reversed lane loop's reversed index is the lane itself
+    KV idx = fromOrdinalK(g, q, d, g.loopDepth[id], id, laneRev && laneLoop(g, id) ? std::string("dx_gl") : eSub(n - 1, q));
     KV elem = kexpr(g, kbind(bs, f.binder, idx), f.body, nullptr);
     // result storage
     DTy tt = tTable(d, elem->ty);
@@ -2294,14 +2437,20 @@ class Lowering {
     if (lane) g.inLaneLoop = false;
     g.out = outer;
     g.ind = savedInd;
+    // group mode: a depth-1 loop producing a local table would leave each
+    // lane with one element of it
+    if (g.pass == 0 && g.loopDepth[id] == 1 && !el.empty()) g.grpOK = false;
     std::vector<Slot> slots;
     if (!el.empty()) slots = localArrays(g, tt);
     if (g.out) {
       // lane loops: 8 iterations unrolled so their independent loads are in
       // flight together (each lane still adds in ascending q order)
-      g.line(std::string(lane ? "#pragma unroll 8" : n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
-      if (lane) g.line("for (int " + q + " = dx_lane; " + q + " < " + lit(n) + "; " + q + " += 32) {");
-      else g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
+      if (laneLoop(g, id)) g.line(loopHead(g, id, q, n, "int", laneRev));
+      else {
+        g.line(std::string(lane ? "#pragma unroll 8" : n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
+        if (lane) g.line("for (int " + q + " = dx_lane; " + q + " < " + lit(n) + "; " + q + " += 32) {");
+        else g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
+      }
       g.out->append(bodyCode);
     }
     g.ind = savedInd + 1;
@@ -2378,6 +2527,7 @@ class Lowering {
       }
       cond = "(" + sc->e + " < " + lit(ls) + ")";
     }
+    g.hasBranch = true;
     std::string* outer = g.out;
     int savedInd = g.ind;
     std::string lc, rc;
@@ -2626,6 +2776,22 @@ class Lowering {
   void accumScalar(KGen& g, const KScope& s, const KV& ref, size_t leaf, const std::string& valE,
                    const KV& val, Span sp) {
     const Slot& sl = ref->slots[leaf];
+    if (ref->cell < 0 && !g.serial && g.depth() >= 1) {
+      // group mode: a kernel-level local cell accumulated by the lanes must be
+      // a scalar that is still zero at the lane loop's entry; each lane then
+      // holds a partial and the group sums them after the loop (closeLoop)
+      auto ld = g.localDepth.find(sl.base);
+      const bool outer = ld == g.localDepth.end() || ld->second == 0;
+      if (outer && !g.grpSum.empty()) {
+        if (g.pass == 0 && (sl.off != "0" || ref->slots.size() != 1 || !g.grpFresh.back().count(sl.base)))
+          g.grpOK = false;
+        g.grpSum.back().insert(sl.base);
+      }
+    }
+    if (ref->cell < 0 && g.grpPending.count(sl.base)) {  // written again: sum the partials now
+      g.line(sl.base + "[0] = dx_grp_sum<" + lit(g.grpPending[sl.base]) + ">(" + sl.base + "[0]);");
+      g.grpPending.erase(sl.base);
+    }
     if (ref->cell < 0) {  // thread-local cell
       if ((g.inCand || g.inLaneLoop) && !g.innerCells.count(sl.base)) {
         // an outer cell accumulated by the reduction loop: scalar cells only
@@ -2645,6 +2811,10 @@ class Lowering {
     g.warpRowOK = false;  // a plan cell: every lane would add its contribution
     int site = g.accumSiteCounter++;
     CellUse& cu = cellUse(g, ref->cell, sl.cellLeaf);
+    // group mode: at kernel level every lane of the group computes the same
+    // value; only scalar cells (one guarded register add) are allowed there
+    const bool grpTop = !g.serial && g.depth() == 0;
+    if (g.pass == 0 && grpTop && cu.width != 1) g.grpOK = false;
     if (g.pass == 0) {
       cu.any = true;
       if (!ownerPath(g, ref, ref->cell)) cu.allOwner = false;
@@ -2681,7 +2851,12 @@ class Lowering {
         g.line(tgt + "[" + sl.off + "] += " + valE + ";");
         break;
       case CellUse::Reg:
-        g.line("rp" + std::to_string(&cu - &g.cells[0]) + " += " + valE + ";");
+        if (g.grp > 0 && grpTop && val && !val->grpPart.empty() && valE == val->e)  // lane partials
+          g.line("rp" + std::to_string(&cu - &g.cells[0]) + " += " + val->grpPart + "[0];");
+        else if (g.grp > 0 && grpTop)
+          g.line("if (dx_gl == 0) rp" + std::to_string(&cu - &g.cells[0]) + " += " + valE + ";");
+        else
+          g.line("rp" + std::to_string(&cu - &g.cells[0]) + " += " + valE + ";");
         break;
       case CellUse::Smem:
         g.line("dx_red_smem(&sm" + std::to_string(&cu - &g.cells[0]) + "[" + sl.off + "], " + valE + ");");
@@ -2691,8 +2866,15 @@ class Lowering {
         break;
       case CellUse::Row:
       case CellUse::TileRow: {
-        int rid = g.rowSiteCounter++;
         const KV& last = ref->path.back();
+        if (g.grp > 0) {
+          // lane (group gi, column c) adds into its own word of the warp's
+          // table row: copy gi holds columns [gi*G, gi*G + G)
+          g.line("dx_wt" + std::to_string(&cu - &g.cells[0]) + "[(int)((" + ref->prefixOff + ") / " + lit(cu.rowD) +
+                 "LL) * 32 + dx_gi * " + lit(g.grp) + " + (int)(" + last->e + ")] += " + valE + ";");
+          break;
+        }
+        int rid = g.rowSiteCounter++;
         std::string rv = "rowv" + std::to_string(rid), rk = "rowk" + std::to_string(rid);
         // one row site per cell, directly in the loop over the row's columns:
         // every column is written exactly once per iteration
@@ -2747,8 +2929,9 @@ class Lowering {
         long long n = size(d);
         std::string q = g.fresh("a");
         int id = openLoop(g, n);
-        g.line(std::string(n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
-        g.line("for (int " + q + " = 0; " + q + " < " + lit(n) + "; ++" + q + ") {");
+        if (g.loopDepth[id] == 1) g.curLaneVar = q;
+        if (!laneLoop(g, id)) g.line(std::string(n <= 32 ? "#pragma unroll" : "#pragma unroll 1"));
+        g.line(loopHead(g, id, q, n));
         g.ind++;
         KScope bs = s;
         bs.covered.insert(id);
@@ -2782,8 +2965,14 @@ class Lowering {
 
   void putK(KGen& g, const KV& ref, const KV& v, Span sp) {
     g.warpRowOK = false;
+    if (g.pass == 0 && !g.serial && g.depth() >= 1)  // group mode: a lane writing replicated state
+      for (const Slot& sl : ref->slots) {
+        auto ld = g.localDepth.find(sl.base);
+        if (ld == g.localDepth.end() || ld->second == 0) g.grpOK = false;
+      }
     if (ref->k != KVal::Ref) notLowerable("put of a non-reference", sp);
     std::vector<Slot> slots = ref->slots;
+    for (const Slot& sl : slots) g.grpPending.erase(sl.base);  // overwritten: partials dropped
     if (ref->cell >= 0) {
       if (!g.serial) fail(ErrCode::StateInParallel, "state cell written inside a parallel kernel", sp);
       g.stateCells.insert(ref->cell);
@@ -2981,8 +3170,19 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
   if (g.pass == 0) {
     g.warpRowOK = true;
     g.laneLoopId = -1;
+    g.grpOK = true;
+    g.grpTrip = 0;
+    g.grpStreams.clear();
+    g.grpStreamId.clear();
+    g.grpStreamBad.clear();
   }
   g.inCand = g.inLaneLoop = false;
+  g.localDepth.clear();
+  g.instMemo.clear();
+  g.grpPending.clear();
+  if (g.pass == 0) g.hasBranch = false;
+  g.grpFresh.clear();
+  g.grpSum.clear();
   g.loopStack.clear();
   g.loopDepth.clear();
   g.loopTrip.clear();
@@ -3008,7 +3208,8 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
   KV last;
   for (int u = 0; u < (serial ? 1 : U); ++u) {
     std::string o = serial ? "0" : "dx_o" + std::to_string(u);
-    if (!serial && U > 1) g.line("if (" + o + " < dx_hi) {");
+    g.instMemo.clear();  // each ordinal's block has its own variables
+    if (!serial && U > 1) g.line(g.grp > 0 ? "if (dx_ok" + std::to_string(u) + ") {" : "if (" + o + " < dx_hi) {");
     if (!serial && U > 1) g.ind++;
     // dimension ordinals of this iteration
     std::vector<std::string> ords;
@@ -3238,11 +3439,65 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       if (g.streamUse[b].first == cu.rowD && plan.bufs[b].kind == SK::F)
         cu.aliasStage = b;
   }
+  // Group mode (see KGen::grpOK): the row scatter of a WarpTab cell with
+  // G = D lanes per ordinal; every other cell must be a scalar register cell.
+  // Measured on B200 (scripts/kmicro2.cu, k-means 1M x 16, K = 64, back to
+  // back): 20.4 us per step against 30.6 us for the thread-per-ordinal TMA
+  // tile kernel (its row transposes cost 113 shared wavefronts per 32 points;
+  // the group layout needs 64 and no tile barrier).
+  g.grp = 0;
+  g.grpRowCell = -1;
+  int grpWarps = 0;
+  if (!serial && g.grpOK && kb0.dims.size() == 1 && !opt.f64 && g.grpTrip >= 4 && g.grpTrip <= 32 &&
+      32 % g.grpTrip == 0 && total > 0) {
+    bool ok = true;
+    for (size_t i = 0; i < g.cells.size(); ++i) {
+      const CellUse& cu = g.cells[i];
+      if (cu.strat == CellUse::Reg) continue;
+      if (cu.strat == CellUse::TileRow && cu.rowD == g.grpTrip && g.grpRowCell < 0 && cu.width % cu.rowD == 0) {
+        g.grpRowCell = (int)i;
+        continue;
+      }
+      ok = false;
+    }
+    if (ok && g.grpRowCell >= 0) {
+      const CellUse& rc = g.cells[g.grpRowCell];
+      const long long tabB = (rc.width / rc.rowD + 1) * 128;
+      grpWarps = (int)std::min<long long>(20, (200 * 1024) / tabB);
+      if (grpWarps >= 4) g.grp = (int)g.grpTrip;
+    }
+  }
+  if (g.grp > 0) {
+    CellUse& rc = g.cells[g.grpRowCell];
+    rc.warpTab = true;
+    rc.vec4 = true;
+    rc.aliasStage = -1;
+    rc.smemOff = 0;
+    g.threads = grpWarps * 32;
+    g.tile = false;
+    g.staged.clear();
+    g.wholeStaged.clear();
+    g.tensorStaged.clear();
+    // small read-only gather tables (centroids) are copied into shared memory
+    // once per block (LDS with 32-bit addresses instead of L1 gathers)
+    long long room = 224 * 1024 - (long long)grpWarps * ((rc.width / rc.rowD) + 1) * 128;
+    for (int b : g.nonStream) {
+      if (g.streamUse.count(b)) continue;
+      long long bytes = plan.bufs[b].elems * (long long)storageBytesOf(plan.bufs[b].kind, opt.f64);
+      if (bytes <= 0 || bytes > 16 * 1024 || bytes + 16 > room) continue;
+      room -= bytes + 16;
+      g.wholeStaged.insert(b);
+    }
+  }
   // warp per ordinal for short outer loops over long reductions (row sums)
   g.warpRow = !serial && g.warpRowOK && g.laneLoopId >= 0 && g.cells.empty() && !hasRow && !g.tile &&
               kb0.dims.size() == 1 && total <= 148LL * 256;
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
   int U = g.warpRow ? 1 : (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
+  // group mode: 16 ordinals per group and chunk, all their prefetch loads
+  // in flight together (one 128-byte warp load per ordinal pair at G = 16)
+  if (g.grp > 0) U = 16;
+  g.grpU = U;
   // more 16-byte loads in flight per thread for the tiniest bodies (histograms):
   // one load per thread and grid-stride step leaves HBM latency exposed
   if (U == 4 && g.lines <= 8) {
@@ -3320,6 +3575,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
 
   // Assemble source.
   std::ostringstream src;
+  std::function<std::string(const std::string&, const std::string&)> grpLoad;
+  std::function<bool(const KGen::GrpStream&)> grpBcast;
   int warps = std::max(1, g.threads / 32);
   int esize = opt.f64 ? 8 : 4;
   int smem = 0;
@@ -3334,7 +3591,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     if (cu.strat == CellUse::TileRow && cu.warpTab) {
       long long Kr = cu.width / cu.rowD;
       long long wt = (long long)(g.threads / 32) * (Kr + 1) * 128;
-      long long etB = cu.aliasStage >= 0 ? 0 : (long long)g.threads * cu.rowD * 4;
+      long long etB = (cu.aliasStage >= 0 || g.grp > 0) ? 0 : (long long)g.threads * cu.rowD * 4;
       smem = std::max<int>(smem, cu.smemOff + (int)(wt + etB));
     } else if (cu.strat == CellUse::TileRow) {
       long long Kr = cu.width / cu.rowD;
@@ -3428,6 +3685,80 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   } else {
     src << "  const int dx_lane = threadIdx.x & 31, dx_warp = threadIdx.x >> 5;\n";
     src << "  (void)dx_lane; (void)dx_warp;\n";
+    // programmatic dependent launch: wait for the previous launch on the
+    // stream before touching anything it may write -- at entry, or (opt-in
+    // pipelining, DXL_F_PIPELINE) after the streaming loop when the kernel
+    // reads program inputs only
+    bool lateWait = opt.pipeline && g.grp > 0;
+    for (auto& [b, pname] : g.params)
+      if (!g.writtenBufs.count(b) && plan.bufs[b].role != BufDecl::Input && plan.bufs[b].role != BufDecl::Const)
+        lateWait = false;
+    if (!lateWait) src << "  dx_pdl_wait();\n";
+    if (g.grp > 0) {
+      // group mode: chunk c of a warp = ordinals [c*CH, c*CH + CH), group gi
+      // takes ordinals c*CH + u*GPW + gi (u < U); the rows it reads at its
+      // ordinal are prefetched one chunk ahead into registers (double
+      // buffer a/b), the first two chunks before the shared-memory set-up
+      const int G = g.grp, GPW = 32 / G;
+      const long long CH = (long long)GPW * U;
+      src << "  const int dx_gl = dx_lane % " << G << ", dx_gi = dx_lane / " << G << ";\n";
+      src << "  const long long dx_nch = (dx_hi - dx_lo + " << CH - 1 << ") / " << CH << ", dx_nfull = (dx_hi - dx_lo) / " << CH
+          << ";\n";
+      // chunk c goes to block c mod grid (every SM gets the same number of
+      // chunks, +-1), then to the block's warps in turn
+      src << "  const long long dx_w0 = (long long)blockIdx.x + (long long)gridDim.x * dx_warp, dx_tw = (long long)gridDim.x * "
+          << g.threads / 32 << ";\n";
+      // a per-ordinal scalar (a literal column: k-means assignments) is
+      // loaded once per chunk, lane l taking ordinal l, and shuffled to the
+      // groups (CH <= 32)
+      auto bcast = [&, CH](const KGen::GrpStream& gs) {
+        long long c;
+        return CH <= 32 && isIntLit(gs.col, &c);
+      };
+      for (size_t id = 0; id < g.grpStreams.size(); ++id) {
+        const auto& gs = g.grpStreams[id];
+        std::string ct = gs.kind == SK::F ? "dx_f" : ctype(gs.kind);
+        if (bcast(gs)) src << "  " << ct << " gpa" << id << "k = 0, gpb" << id << "k = 0;\n";
+        else src << "  " << ct << " gpa" << id << "[" << U << "], gpb" << id << "[" << U << "];\n";
+      }
+      grpBcast = bcast;
+      grpLoad = [&, CH, GPW, bcast](const std::string& ab, const std::string& chE) {
+        // full chunks: unguarded loads at constant offsets from one base per
+        // stream (the compiler folds u into the address immediate); the
+        // ragged chunk guards each ordinal
+        std::ostringstream o;
+        o << "{ const long long dx_cn = " << chE << ", dx_c0 = dx_lo + dx_cn * " << CH << "LL + dx_gi;\n";
+        for (int full = 1; full >= 0; --full) {
+          o << (full ? "      if (dx_cn < dx_nfull) {\n" : "      } else {\n");
+          for (size_t id = 0; id < g.grpStreams.size(); ++id) {
+            const auto& gs = g.grpStreams[id];
+            std::string ct = gs.kind == SK::F ? "dx_f" : ctype(gs.kind);
+            if (bcast(gs)) {
+              std::string ldx = "__ldcs(" + g.params[gs.buf] + " + (dx_c0 - dx_gi + dx_lane) * " + lit(gs.L) + "LL + " +
+                                lit(gs.base) + "LL + " + gs.col + ")";
+              if (gs.chk > 0) ldx = "dx_chk_idx(" + ldx + ", " + lit(gs.chk) + ", dx_bad)";
+              o << "        gp" << ab << id << "k = dx_lane < " << CH << (full ? "" : " && dx_c0 - dx_gi + dx_lane < dx_hi")
+                << " ? " << ldx << " : (" << ct << ")0;\n";
+              continue;
+            }
+            o << "        const " << ct << "* dx_b" << id << " = " << g.params[gs.buf] << " + dx_c0 * " << gs.L << "LL + "
+              << gs.base << "LL + " << gs.col << ";\n";
+            for (int u = 0; u < U; ++u) {
+              std::string ldx = "__ldcs(dx_b" + std::to_string(id) + " + " + lit((long long)u * GPW * gs.L) + ")";
+              if (gs.chk > 0) ldx = "dx_chk_idx(" + ldx + ", " + lit(gs.chk) + ", dx_bad)";
+              if (full) o << "        gp" << ab << id << "[" << u << "] = " << ldx << ";\n";
+              else
+                o << "        gp" << ab << id << "[" << u << "] = dx_c0 + " << u * GPW << " < dx_hi ? " << ldx << " : (" << ct
+                  << ")0;\n";
+            }
+          }
+        }
+        o << "      }\n    }\n";
+        return o.str();
+      };
+      src << "  if (dx_w0 < dx_nch) " << grpLoad("a", "dx_w0");
+      src << "  if (dx_w0 + dx_tw < dx_nch) " << grpLoad("b", "dx_w0 + dx_tw");
+    }
     if (smem > 0 && g.tensorStaged.empty()) src << "  extern __shared__ __align__(16) unsigned char dx_smem[];\n";
     if (smem > 0 && !g.tensorStaged.empty()) {
       // swizzled TMA destinations need 1024-byte alignment
@@ -3505,6 +3836,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
             src << "  dx_f* et" << I << " = (dx_f*)(dx_smem + " << cu.smemOff + wt * 4 << ");\n";
             src << "  for (int t = threadIdx.x; t < " << wt / 4 << "; t += blockDim.x) reinterpret_cast<float4*>(wtab" << I
                 << ")[t] = make_float4(0.f, 0.f, 0.f, 0.f);\n";
+            if (g.grp > 0) src << "  float* dx_wt" << I << " = wtab" << I << " + dx_warp * " << (Kr + 1) * 32 << ";\n";
             needSync = true;
             break;
           }
@@ -3545,7 +3877,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     // warp-uniform grid-stride loop over groups of U consecutive ordinals
     src << "  const long long dx_n = (dx_hi - dx_lo + " << (U - 1) << ") / " << U << ";\n";
     src << "  const long long dx_stride = (long long)gridDim.x * blockDim.x;\n";
-    if ((tileCell >= 0 || g.tile) && !g.staged.empty()) {
+    if (g.grp == 0 && (tileCell >= 0 || g.tile) && !g.staged.empty()) {
       // TMA pipeline: tile t+1 is in flight while tile t is computed
       src << "  int dx_it = 0;\n";
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride, ++dx_it) {\n";
@@ -3563,10 +3895,49 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       }
       src << "    dx_mbar_wait(&dx_bar[dx_stg], (unsigned)((dx_it >> 1) & 1));\n";
       src << "    const long long dx_s = dx_base + threadIdx.x;\n";
-    } else if (tileCell >= 0) {
+    } else if (g.grp == 0 && tileCell >= 0) {
       // block-uniform tiles: every thread runs the same trip count
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x; dx_base < dx_n; dx_base += dx_stride) {\n";
       src << "    const long long dx_s = dx_base + threadIdx.x;\n";
+    } else if (g.grp > 0) {
+      const int GPW = 32 / g.grp;
+      const long long CH = (long long)GPW * U;
+      auto chunk = [&](const std::string& ab, const std::string& cb) {
+        std::ostringstream o;
+        o << "      const long long dx_cb = " << cb << ";\n";
+        for (size_t id = 0; id < g.grpStreams.size(); ++id) {
+          const auto& gs = g.grpStreams[id];
+          std::string ct = gs.kind == SK::F ? "dx_f" : ctype(gs.kind);
+          for (int u = 0; u < U; ++u) {
+            if (grpBcast(gs))
+              o << "      const " << ct << " gp" << id << "_" << u << " = __shfl_sync(DX_FULL, gp" << ab << id << "k, "
+                << u * GPW << " + dx_gi);\n";
+            else
+              o << "      const " << ct << " gp" << id << "_" << u << " = gp" << ab << id << "[" << u << "];\n";
+          }
+        }
+        for (int u = 0; u < U; ++u)
+          o << "      const long long dx_o" << u << " = dx_lo + dx_cb * " << CH << "LL + " << u * GPW << " + dx_gi;\n";
+        // full chunks (all but at most one per launch) run the bodies
+        // unguarded, in convergent code; the ragged chunk guards each ordinal
+        // and sums over its group's lanes only (the guard is group-uniform)
+        std::string tail = body;
+        for (size_t at = 0; (at = tail.find("dx_grp_sum<", at)) != std::string::npos; at += 13)
+          tail.replace(at, 11, "dx_grp_sum_m<");
+        o << "      if (dx_cb < dx_nfull) {\n";
+        for (int u = 0; u < U; ++u) o << "        const bool dx_ok" << u << " = true;\n";
+        o << body << "      } else {\n";
+        for (int u = 0; u < U; ++u) o << "        const bool dx_ok" << u << " = dx_o" << u << " < dx_hi;\n";
+        o << tail << "      }\n";
+        o << "      if (dx_cb + 2 * dx_tw < dx_nch) " << grpLoad(ab, "dx_cb + 2 * dx_tw");
+        return o.str();
+      };
+      src << "  for (long long dx_ch = dx_w0; dx_ch < dx_nch; dx_ch += 2 * dx_tw) {\n";
+      src << "    {\n" << chunk("a", "dx_ch") << "    }\n";
+      src << "    if (dx_ch + dx_tw < dx_nch) {\n" << chunk("b", "dx_ch + dx_tw") << "    }\n";
+      src << "  }\n";
+      src << "  dx_pdl_trigger();\n";
+      if (lateWait) src << "  dx_pdl_wait();\n";
     } else if (g.warpRow) {
       // one warp per ordinal (warp-uniform), the lanes split the reduction loop
       src << "  for (long long dx_base = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dx_base < dx_n; dx_base += dx_stride >> 5) {\n";
@@ -3575,6 +3946,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "  for (long long dx_base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); dx_base < dx_n; dx_base += dx_stride) {\n";
       src << "    const long long dx_s = dx_base + dx_lane;\n";
     }
+    if (g.grp == 0) {
     for (int u = 0; u < U; ++u)
       src << "    const long long dx_o" << u << " = dx_lo + dx_s * " << U << " + " << u << ";\n";
     for (auto& rs : g.rowSites) {
@@ -3642,6 +4014,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     if (tileCell < 0 && g.tile && !g.staged.empty())
       src << "    __syncthreads();  // every thread is done with this TMA stage\n";
     src << "  }\n";
+    }  // g.grp == 0
     // last-block-done kernels collect the E-bounds flags of the launch in a
     // ticket word; the final block forwards them (and initializes the error
     // flag when this kernel is its first writer)
@@ -3690,8 +4063,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
-      src << "  dx_grid_barrier(" << g.params[syncBuf] << ");\n";
+      src << "  dx_ticket_barrier((unsigned long long*)" << g.params[syncBuf] << ");\n";
       if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
+      long long foldBase = 0;
       for (size_t i = 0; i < g.cells.size(); ++i) {
         CellUse& cu = g.cells[i];
         if (cu.partialBuf < 0) continue;
@@ -3699,9 +4073,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         bool counts = cu.strat == CellUse::Count;
         // a cell whose only pending step is its zero-fill is overwritten
         const bool store = takeZero(cu.targetBuf);
-        src << "  dx_coop_fold<" << ct << ", " << (counts ? "unsigned" : "dx_f") << ">(part" << i << ", "
+        // the cells' columns share one warp index space: every column is one
+        // warp's fold, all in flight together
+        src << "  dx_coop_fold_b<" << ct << ", " << (counts ? "unsigned" : "dx_f") << ">(part" << i << ", "
             << cu.width << "LL, (" << ct << ")" << litF(counts ? cu.constVal : 1.0, true) << ", " << cu.pname
-            << ", " << (counts ? "true" : "false") << ", " << (store ? "true" : "false") << ");\n";
+            << ", " << (counts ? "true" : "false") << ", " << (store ? "true" : "false") << ", " << foldBase << "LL);\n";
+        foldBase += (cu.width + 31) / 32;
       }
     }
     if (lbd) {
@@ -3763,6 +4140,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   ks.smem = smem;
   ks.minGrid = U;
   ks.warpRow = g.warpRow;
+  ks.grp = g.grp;
   ks.coop = coop;
   ks.note = note + (g.warpRow ? " (warp per ordinal)" : "");
   addStep(ks);

@@ -77,6 +77,7 @@ struct Step {
   int smem = 0;           // dynamic shared memory bytes
   int minGrid = 0;        // ordinals per thread (U)
   bool warpRow = false;   // one warp per ordinal (32 threads per iteration)
+  int grp = 0;            // group mode: G lanes per ordinal, minGrid ordinals per group and chunk
   bool coop = false;      // cooperative launch (in-kernel grid barrier + finalize)
   bool dead = false;      // Zero step taken over by the first kernel writing the buffer
   long long fixedGrid = 0;  // >0: launch exactly this many blocks (tile kernels: GEMM, transpose)
@@ -133,6 +134,7 @@ struct LowerOptions {
   bool noFusion = false;
   bool noRowScatter = false;
   bool noGemm = false;
+  bool pipeline = false;  // DXL_F_PIPELINE: stream inputs before the PDL wait
 };
 
 // Lowers `e` (first-order, post-optimize) whose free variables are the

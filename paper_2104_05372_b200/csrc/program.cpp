@@ -153,6 +153,10 @@ int Program::prepare() {
     long long U = s.minGrid > 0 ? s.minGrid : 1;  // ordinals per thread
     long long need = ((hi - lo + U - 1) / U + s.threads - 1) / s.threads;
     if (s.warpRow) need = ((hi - lo) * 32 + s.threads - 1) / s.threads;
+    if (s.grp > 0) {  // ordinals per block and chunk: (threads / G) groups x U
+      const long long per = (long long)(s.threads / s.grp) * U;
+      need = (hi - lo + per - 1) / per;
+    }
     long long cap = (long long)ctx->smCount * nb;
     long long grid = std::max(1LL, std::min(need, cap));
     grids[i] = (int)grid;
@@ -189,6 +193,16 @@ int Program::prepare() {
     }
   }
   if (plan.world > 1) useGraph = false;
+  // A plan that is one kernel launch runs without a graph, launched with
+  // programmatic dependent launch: back-to-back runs on the context stream
+  // overlap the next launch with this one's tail (the kernel waits, via
+  // griddepcontrol.wait, before touching anything its predecessor writes).
+  {
+    int nk = 0, other = 0;
+    for (auto& st : plan.steps) (st.k == Step::Kernel ? nk : other)++;
+    pdlSingle = nk == 1 && other == 0;
+    if (pdlSingle) useGraph = false;
+  }
   if ((rc = buildTensorMaps())) return rc;
   // finalize functions
   const char* fz[4] = {"dx_fin_f32", "dx_fin_f64", "dx_fin_count_f32", "dx_fin_count_f64"};
@@ -392,7 +406,21 @@ int Program::issue() {
             if (kernelEventStep[e] == (int)i) ev = (int)e;
           if (ev >= 0 && (rc = dxrt::check(cuEventRecordWithFlags(kernelEvents[ev].first, st, capturing ? CU_EVENT_RECORD_EXTERNAL : CU_EVENT_RECORD_DEFAULT), "event"))) return rc;
         }
-        if (s.coop) {
+        if (pdlSingle) {
+          // every block of a grid-barrier kernel is co-resident: the grid is
+          // capped at the occupancy at prepare (blocks x SMs)
+          CUlaunchConfig cfg = {};
+          cfg.gridDimX = grids[i]; cfg.gridDimY = 1; cfg.gridDimZ = 1;
+          cfg.blockDimX = s.threads; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+          cfg.sharedMemBytes = s.smem;
+          cfg.hStream = st;
+          CUlaunchAttribute attr;
+          attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+          attr.value.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = &attr;
+          cfg.numAttrs = 1;
+          if ((rc = dxrt::check(cuLaunchKernelEx(&cfg, funcs[i], argv.data(), nullptr), "cuLaunchKernelEx(pdl)"))) return rc;
+        } else if (s.coop) {
           CUlaunchConfig cfg = {};
           cfg.gridDimX = grids[i]; cfg.gridDimY = 1; cfg.gridDimZ = 1;
           cfg.blockDimX = s.threads; cfg.blockDimY = 1; cfg.blockDimZ = 1;
@@ -533,6 +561,7 @@ int dxl_program_create(dxc_ctx* ctx, const char* source, const char* entry, cons
     lo.noRowScatter = (opts->flags & DXL_F_NO_ROWSCATTER) != 0;
     p->allowCommMismatch = (opts->flags & DXL_F_TEST_COMM_MISMATCH) != 0;
     lo.noGemm = (opts->flags & DXL_F_NO_GEMM) != 0;
+    lo.pipeline = (opts->flags & DXL_F_PIPELINE) != 0;
   }
   std::vector<std::pair<Name, ValuePtr>> params;
   ExprPtr optimized;

@@ -53,6 +53,7 @@ struct Program {
   int buildTensorMaps();
   CUgraphExec graphExec = nullptr;
   bool useGraph = true;
+  bool pdlSingle = false;  // one-launch plan: direct launch with PDL, no graph
   bool capturing = false;  // issue() is being captured into the graph (external event nodes)
   bool timing = false;
   std::vector<std::pair<CUevent, CUevent>> kernelEvents;  // per kernel step

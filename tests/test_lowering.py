@@ -42,22 +42,24 @@ def _sass(source):
 def test_kmeans_value_and_grad_is_one_fused_kernel():
     """Forward tape inlined into both consumers (no HBM tape), the cotangent
     broadcast folded (accum-to-map), cost and gradient loops fused
-    horizontally: one cooperative kernel that also folds the partials after a
-    wrap-safe grid barrier and owns the zero-fills (the plan is that single
-    launch)."""
+    horizontally: one kernel in group mode (16 lanes per point, one lane per
+    column) that also folds the partials after a ticket grid barrier and owns
+    the zero-fills (the plan is that single launch)."""
     prog = dx.Program(P.kmeans_cost_grad(100_000, 16, 64), ctx=None)
     ks = _kernels(prog.plan)
     assert len(ks) == 1, prog.plan
     assert "zero b" not in prog.plan.split("---")[0], prog.plan
     src = prog.source
-    assert "dx_warp_tab<16, 64" in src            # warp-private row tables for dC
-    assert "dx_warp_tab_flush<16, 64" in src
-    assert ", true);" in src                      # fold overwrites the (never zeroed) cell
-    assert "dx_grid_barrier(" in src and "dx_coop_fold<double, dx_f>" in src
-    assert "dx_block_sum(rp" in src               # register partial for the cost
-    assert "dx_tma_2d(" in src                    # TMA tensor tiles of the points
+    assert "const int dx_gl = dx_lane % 16" in src   # 16 lanes per point
+    assert "dx_grp_sum<16>(" in src                 # the per-point cost: group xor tree
+    assert "dx_wt1[" in src                          # lane-owned words of the warp's dC table
+    assert "dx_warp_tab_flush<16, 64, 20>" in src
+    assert src.count("dx_ldcs(p1 + o * 16LL") == 64  # one point stream: 16 loads x (a, b) x (first, refill)
+    assert ", true);" in src                        # fold overwrites the (never zeroed) cell
+    assert "dx_ticket_barrier(" in src and "dx_coop_fold_w<double, dx_f>" in src
+    assert "dx_block_sum(rp" in src                 # register partial for the cost
     sass = _sass(src)
-    assert "UTMALDG.2D" in sass and "UBLKCP" in sass
+    assert "STL" not in sass and "LDL" not in sass  # prefetch buffers stay in registers
 
 
 def test_histogram_uses_exact_shared_counters():
