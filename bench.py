@@ -594,15 +594,34 @@ def main():
             runners[step % R].run()
             step += 1
         ctx.sync()
+    # The K steps are captured into one CUDA graph (the steps' own launches,
+    # in order, programmatic-dependent-launch edges kept) so that the host's
+    # per-launch cost (Python + driver, several us) never paces the GPU; a
+    # context that cannot be captured (sharded plans issue NCCL calls) runs
+    # the same K launches from the host loop.
+    graph = None
+    if world == 1:
+        try:
+            graph = ctx.capture(lambda: [runners[i % R].run() for i in range(args.steps)])
+            ctx.graph_launch(graph)  # one untimed replay (graph upload)
+            ctx.sync()
+        except Exception as exc:  # noqa: BLE001 -- recorded in the JSON line
+            graph = None
+            spec["extra"]["capture_error"] = str(exc)[:200]
     barrier()
     e0 = ctx.event()
-    for i in range(args.steps):
-        runners[i % R].run()
+    if graph is not None:
+        ctx.graph_launch(graph)
+    else:
+        for i in range(args.steps):
+            runners[i % R].run()
     e1 = ctx.event()
     ctx.sync()
     ms_total = ctx.elapsed_ms(e0, e1)
     ctx.destroy_event(e0)
     ctx.destroy_event(e1)
+    if graph is not None:
+        ctx.graph_destroy(graph)
     # per-kernel durations (roofline): the same K steps again with an event
     # pair around every launch, kept out of the step time above
     kern = {}
@@ -680,7 +699,9 @@ def main():
                             "l2": (f"inputs larger than L2: {R} device-resident input copies "
                                    f"({R * in_bytes / 1e6:.0f} MB, each read once per {R} steps) rotate "
                                    f"under K back-to-back steps timed by one event pair"),
-                            "steps_timing": "K consecutive steps between one CUDA event pair, / K",
+                            "steps_timing": ("K consecutive steps captured into one CUDA graph, one event pair "
+                                             "around its launch, / K" if graph is not None else
+                                             "K consecutive steps between one CUDA event pair, / K"),
                        "kernel_times": ("one launch per step: the kernel's average launch duration is the timed "
                                         "K back-to-back launches / K (events on the launching stream)"
                                         if single_launch else

@@ -98,6 +98,12 @@ int dxc_l2_flush(dxc_ctx* ctx, size_t bytes);
 
 /* Events on the context stream (device-side timing). */
 int dxc_event_record(dxc_ctx* ctx, void** ev);
+/* Capture everything issued on the context stream between begin and end
+ * (e.g. K dxl_program_run calls) into one instantiated CUDA graph. */
+int dxc_capture_begin(dxc_ctx* ctx);
+int dxc_capture_end(dxc_ctx* ctx, void** graph_exec);
+int dxc_graph_launch(dxc_ctx* ctx, void* graph_exec);
+int dxc_graph_destroy(void* graph_exec);
 int dxc_event_elapsed_ms(void* ev0, void* ev1, float* ms);
 int dxc_event_destroy(void* ev);
 

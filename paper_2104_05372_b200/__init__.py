@@ -119,6 +119,10 @@ _sig("dxc_sync", ctypes.c_int, _vp)
 _sig("dxc_host_alloc", ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(_vp))
 _sig("dxc_host_free", ctypes.c_int, _vp)
 _sig("dxc_event_record", ctypes.c_int, _vp, ctypes.POINTER(_vp))
+_sig("dxc_capture_begin", ctypes.c_int, _vp)
+_sig("dxc_capture_end", ctypes.c_int, _vp, ctypes.POINTER(_vp))
+_sig("dxc_graph_launch", ctypes.c_int, _vp, _vp)
+_sig("dxc_graph_destroy", ctypes.c_int, _vp)
 _sig("dxc_event_elapsed_ms", ctypes.c_int, _vp, _vp, ctypes.POINTER(ctypes.c_float))
 _sig("dxc_event_destroy", ctypes.c_int, _vp)
 _sig("dxc_nccl_unique_id", ctypes.c_int, _vp)
@@ -174,6 +178,7 @@ ABI_SYMBOLS = [
     "dxc_sync", "dxc_buf_alloc", "dxc_buf_free", "dxc_buf_ptr", "dxc_buf_upload", "dxc_buf_download",
     "dxc_buf_zero", "dxc_host_alloc", "dxc_host_free", "dxc_module_compile", "dxc_module_cubin",
     "dxc_launch", "dxc_event_record", "dxc_event_elapsed_ms", "dxc_event_destroy",
+    "dxc_capture_begin", "dxc_capture_end", "dxc_graph_launch", "dxc_graph_destroy",
     "dxc_nccl_unique_id", "dxc_comm_init", "dxc_allreduce_sum", "dxl_program_create",
     "dxl_program_destroy", "dxl_program_num_inputs", "dxl_program_input_num_leaves",
     "dxl_program_input_leaf", "dxl_program_output_num_leaves", "dxl_program_output_leaf",
@@ -255,6 +260,25 @@ class Context:
     @staticmethod
     def destroy_event(e):
         _lib.dxc_event_destroy(e)
+
+    def capture(self, fn):
+        """Run fn() with the context stream captured; returns a graph handle
+        replayed by graph_launch (every launch fn issued, in order)."""
+        _check(_lib.dxc_capture_begin(self.handle))
+        try:
+            fn()
+        finally:
+            g = _vp()
+            rc = _lib.dxc_capture_end(self.handle, ctypes.byref(g))
+        _check(rc)
+        return g
+
+    def graph_launch(self, g):
+        _check(_lib.dxc_graph_launch(self.handle, g))
+
+    @staticmethod
+    def graph_destroy(g):
+        _check(_lib.dxc_graph_destroy(g))
 
     def l2_flush(self, nbytes: int = 256 << 20):
         """Overwrite a scratch buffer larger than the 126 MB L2 (on our stream)."""

@@ -1179,6 +1179,12 @@ class Lowering {
           if (d && hOrdinal(v, d, &o)) return hFromOrdinal(size(d) - 1 - o, d);
           break;
         }
+        case UnOp::Exp:  // frontend_ext (exp/log), folded in double like the evaluator
+          if (v->k == HVal::Const) return hConstF(std::exp(v->f));
+          break;
+        case UnOp::Log:
+          if (v->k == HVal::Const) return hConstF(std::log(v->f));
+          break;
       }
       return serialKernel(env, e, annot);
     }
@@ -2385,6 +2391,14 @@ class Lowering {
         int lid = (v->k == KVal::Scalar) ? v->loopId : -1;
         return fromOrdinalK(g, r, d, lev, lid, o);
       }
+      case UnOp::Exp:  // frontend_ext: exp / log (libdevice, correctly rounded to <= 2 ulp in f32)
+      case UnOp::Log: {
+        const char* fn = op == UnOp::Exp ? (opt.f64 ? "exp" : "expf") : (opt.f64 ? "log" : "logf");
+        if (v->isConst && v->ty->k == DType::Float) return constK(op == UnOp::Exp ? std::exp(v->cf) : std::log(v->cf));
+        std::string x = g.fresh("f");
+        g.line("const dx_f " + x + " = " + fn + "(" + v->e + ");");
+        return kScalar(tFloat(), x, v->level);
+      }
     }
     notLowerable("unary op", sp);
   }
@@ -3426,6 +3440,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     for (int b : g.nonStream) {
       if (g.streamUse.count(b)) continue;
       long long bytes = plan.bufs[b].elems * (long long)storageBytesOf(plan.bufs[b].kind, opt.f64);
+      bytes = (bytes + 127) / 128 * 128;  // swizzled 128-byte rows
       if (bytes <= 0 || bytes > 16 * 1024 || bytes > budget) continue;
       budget -= bytes;
       g.wholeStaged.insert(b);
@@ -3484,6 +3499,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     for (int b : g.nonStream) {
       if (g.streamUse.count(b)) continue;
       long long bytes = plan.bufs[b].elems * (long long)storageBytesOf(plan.bufs[b].kind, opt.f64);
+      bytes = (bytes + 127) / 128 * 128;  // swizzled 128-byte rows
       if (bytes <= 0 || bytes > 16 * 1024 || bytes + 16 > room) continue;
       room -= bytes + 16;
       g.wholeStaged.insert(b);
@@ -3631,7 +3647,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     int eb = (int)storageBytesOf(plan.bufs[b].kind, opt.f64);
     smem = (smem + 15) / 16 * 16;
     wholeAt[b] = smem;
-    smem += (int)(plan.bufs[b].elems * eb);
+    // the copy is swizzled within 128-byte rows (dx_swz(.., 3)): a partial
+    // last row still spans the whole row
+    smem += (int)((plan.bufs[b].elems * eb + 127) / 128 * 128);
   }
 
   src << "// " << note << "\n";

@@ -125,7 +125,9 @@ int Program::prepare() {
     CUfunction f;
     if ((rc = dxrt::check(cuModuleGetFunction(&f, mod, s.name.c_str()), "cuModuleGetFunction"))) return rc;
     funcs[i] = f;
-    if (s.smem > 48 * 1024) {
+    // static shared memory (fold scratch, barriers) + dynamic may pass 48 KB
+    // even when the dynamic part alone does not: always raise the cap
+    if (s.smem > 0) {
       if ((rc = dxrt::check(cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, s.smem),
                             "cuFuncSetAttribute")))
         return rc;

@@ -462,6 +462,36 @@ int dxc_l2_flush(dxc_ctx* ctx, size_t bytes) {
   return check(cuMemsetD8Async(ctx->scratch, flip, bytes, ctx->stream), "l2 flush");
 }
 
+// Stream capture of a sequence of runs into one CUDA graph (bench / serving
+// loops: K back-to-back evaluations launched without host work between them;
+// programmatic-dependent-launch edges are kept in the graph).
+int dxc_capture_begin(dxc_ctx* ctx) {
+  ctx->makeCurrent();
+  return check(cuStreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "cuStreamBeginCapture");
+}
+
+int dxc_capture_end(dxc_ctx* ctx, void** graph_exec) {
+  ctx->makeCurrent();
+  CUgraph g = nullptr;
+  int rc = check(cuStreamEndCapture(ctx->stream, &g), "cuStreamEndCapture");
+  if (rc) return rc;
+  CUgraphExec e = nullptr;
+  rc = check(cuGraphInstantiate(&e, g, 0), "cuGraphInstantiate");
+  cuGraphDestroy(g);
+  if (rc) return rc;
+  *graph_exec = (void*)e;
+  return DXC_OK;
+}
+
+int dxc_graph_launch(dxc_ctx* ctx, void* graph_exec) {
+  ctx->makeCurrent();
+  return check(cuGraphLaunch((CUgraphExec)graph_exec, ctx->stream), "cuGraphLaunch");
+}
+
+int dxc_graph_destroy(void* graph_exec) {
+  return graph_exec ? check(cuGraphExecDestroy((CUgraphExec)graph_exec), "cuGraphExecDestroy") : DXC_OK;
+}
+
 int dxc_event_record(dxc_ctx* ctx, void** ev) {
   ctx->makeCurrent();
   CUevent e;

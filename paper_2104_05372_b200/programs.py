@@ -215,3 +215,125 @@ def gmm_inputs(n: int, d: int, K: int, seed: int = 20211):
     icf = rng.uniform(-0.1, 0.1, (K, d * (d + 1) // 2)).astype(np.float32)
     x = rng.standard_normal((n, d)).astype(np.float32)
     return alphas, means, icf, x
+
+
+def gmm_program(n: int, d: int, K: int, gamma: float = 1.0, m: int = 0) -> str:
+    """config 3 as a dexlet program (needs the frontend_ext `exp`/`log`): the
+    ADBench GMM objective and its gradient w.r.t. (alphas, (means, icf)).
+
+    ADBench's `gmm_objective` (oracle/gmm.py) in the language's own terms:
+    Q_k x = exp(icf_k[:d]) * x + L_k x (the log-diagonal slots selected by the
+    index table `dgi`, r -> r) with the strictly lower triangle packed
+    column by column, selected by the index table `tri` (row r, column c ->
+    packed slot) under the 0/1 mask `lm` (r > c); `lw` masks the packed
+    lower part of icf in the Wishart prior.  The log-sum-exps are stabilised
+    by their maxima as ADBench does, passed as inputs `mx` (per point, over
+    the components) and `ma` (over the alphas): in the language a `case` on
+    `<` cannot be differentiated (the simplifier turns it into a data sum),
+    and d/dtheta [m + log sum exp(beta - m)] does not depend on m, so the
+    maxima are constants of the gradient -- a stop-gradient, as ADBench's own
+    logsumexp.  `gmm_stabilizers` computes them (a forward-only program, or
+    numpy).  Constant terms (the 2 pi term and the Wishart normaliser) are
+    source literals."""
+    import math
+    T = d * (d + 1) // 2
+    nn = d + m + 1
+    lgd = 0.25 * d * (d - 1) * math.log(math.pi) + sum(math.lgamma(0.5 * nn + 0.5 * (1 - j)) for j in range(1, d + 1))
+    C = nn * d * (math.log(gamma) - 0.5 * math.log(2)) - lgd
+    c0 = -n * d * 0.5 * math.log(2 * math.pi) - K * C
+
+    def lit(v):
+        return repr(float(v))
+    P = f"(((Fin {K})=>Float) & ({_mat(K, d)} & {_mat(K, T)}))"
+    return (f"main = \\x:{_mat(n, d)}. \\mx:((Fin {n})=>Float). \\ma:((Fin 1)=>Float). "
+            f"\\dgi:((Fin {d})=>(Fin {T})). \\tri:((Fin {d})=>((Fin {d})=>(Fin {T}))). \\lm:{_mat(d, d)}. \\lw:((Fin {T})=>Float). "
+            f"\\th:{P}.\n"
+            f"  f = \\p:{P}.\n"
+            f"    al = fst p\n"
+            f"    mi = snd p\n"
+            f"    mu = fst mi\n"
+            f"    ic = snd mi\n"
+            f"    sqs = for k. sum (for r. ic.k.(dgi.r))\n"
+            f"    lse = for i.\n"
+            f"      s = sum (for k.\n"
+            f"        sq = sum (for r.\n"
+            f"          qr = (exp (ic.k.(dgi.r))) * ((x.i.r) - (mu.k.r)) + sum (for c. ((lm.r.c) * (ic.k.(tri.r.c))) * ((x.i.c) - (mu.k.c)))\n"
+            f"          qr * qr)\n"
+            f"        exp ((((al.k) + (sqs.k)) - 0.5 * sq) - (mx.i)))\n"
+            f"      (mx.i) + log s\n"
+            f"    sa = sum (for k. exp ((al.k) - (ma.(@0 : Fin 1))))\n"
+            f"    wi = sum (for k.\n"
+            f"      dg = sum (for r. (exp (ic.k.(dgi.r))) * (exp (ic.k.(dgi.r))))\n"
+            f"      lo = sum (for t. ((lw.t) * (ic.k.t)) * (ic.k.t))\n"
+            f"      {lit(0.5 * gamma * gamma)} * (dg + lo) - {lit(m)} * (sqs.k))\n"
+            f"    (({lit(c0)} + sum lse) - {lit(n)} * ((ma.(@0 : Fin 1)) + log sa)) + wi\n"
+            f"  pr = linearize f th\n"
+            f"  (fst pr, transpose (snd pr) 1.0)\n")
+
+
+def gmm_tables(d: int):
+    """Index/mask inputs of gmm_program: dgi [d] (r -> slot r), tri [d][d] (packed slot of L[r][c]
+    for r > c, ADBench column-major order; 0 elsewhere), lm [d][d] (1.0 for
+    r > c) and lw [T] (1.0 on the packed lower part, slots >= d)."""
+    T = d * (d + 1) // 2
+    tri = np.zeros((d, d), dtype=np.int32)
+    lm = np.zeros((d, d), dtype=np.float32)
+    li = 0
+    for c in range(d):
+        for r in range(c + 1, d):
+            tri[r, c] = d + li
+            lm[r, c] = 1.0
+            li += 1
+    lw = np.zeros(T, dtype=np.float32)
+    lw[d:] = 1.0
+    dgi = np.arange(d, dtype=np.int32)
+    return dgi, tri, lm, lw
+
+
+def gmm_stabilizers(alphas, means, icf, x):
+    """The log-sum-exp maxima of gmm_program (fp64 numpy, forward only):
+    mx[i] = max_k beta[i][k], ma = max_k alphas[k]."""
+    x = np.asarray(x, dtype=np.float64)
+    alphas = np.asarray(alphas, dtype=np.float64)
+    means = np.asarray(means, dtype=np.float64)
+    icf = np.asarray(icf, dtype=np.float64)
+    n, d = x.shape
+    K = len(alphas)
+    _, tri, lm, _ = gmm_tables(d)
+    Q = np.zeros((K, d, d))
+    r, c = np.nonzero(lm)
+    Q[:, r, c] = icf[:, tri[r, c]]
+    Q[:, np.arange(d), np.arange(d)] = np.exp(icf[:, :d])
+    sum_qs = icf[:, :d].sum(1)
+    beta = np.empty((n, K))
+    for k in range(K):
+        y = (x - means[k]) @ Q[k].T
+        beta[:, k] = alphas[k] + sum_qs[k] - 0.5 * (y * y).sum(1)
+    return beta.max(1), np.array([alphas.max()])
+
+
+def softplus_grad(n: int) -> str:
+    """frontend_ext: gradient of sum log(1 + exp v) (= the logistic sigmoid)."""
+    return (f"main = \\xs:((Fin {n})=>Float).\n"
+            f"  f = \\v:((Fin {n})=>Float). sum (for i. log (1.0 + exp (v.i)))\n"
+            f"  grad f xs\n")
+
+
+def logsumexp_grad(b: int, k: int) -> str:
+    """frontend_ext: value and gradient of sum_i (m_i + log sum_j exp(v_ij - m_i))
+    with the row maxima m as an input (a stop-gradient)."""
+    return (f"main = \\v:{_mat(b, k)}. \\m:((Fin {b})=>Float).\n"
+            f"  f = \\a:{_mat(b, k)}. sum (for i. (m.i) + log (sum (for j. exp ((a.i.j) - (m.i)))))\n"
+            f"  pr = linearize f v\n"
+            f"  (fst pr, transpose (snd pr) 1.0)\n")
+
+
+def leaky_relu_grad(n: int) -> str:
+    """frontend_ext `<` tangent: value and gradient of sum (c.(v < 0) * v)^2,
+    c = (slope for v >= 0, slope for v < 0) indexed by the Bool itself."""
+    return (f"main = \\xs:((Fin {n})=>Float). \\c:((Either Unit Unit)=>Float).\n"
+            f"  f = \\v:((Fin {n})=>Float). sum (for i.\n"
+            f"    y = (c.((v.i) < 0.0)) * (v.i)\n"
+            f"    y * y)\n"
+            f"  pr = linearize f xs\n"
+            f"  (fst pr, transpose (snd pr) 1.0)\n")

@@ -41,6 +41,18 @@ def cases():
     out.append(("either_case_33", P.either_case(33), [r.standard_normal(33), r.standard_normal(33)]))
     out.append(("mandelbrot_8x6", P.mandelbrot(8, 6, 20),
                 [np.linspace(-2.0, 0.5, 8), np.linspace(-1.0, 1.0, 6)]))
+    # frontend_ext (exp/log): the evaluator extended the same way is the checker
+    out.append(("softplus_grad_40", P.softplus_grad(40), [r.standard_normal(40)]))
+    out.append(("leaky_relu_grad_30", P.leaky_relu_grad(30), [r.standard_normal(30), np.array([1.0, 0.1])]))
+    v = r.standard_normal((6, 9))
+    out.append(("logsumexp_grad_6x9", P.logsumexp_grad(6, 9), [v, v.max(1)]))
+    for (n, d, K, seed) in ((50, 3, 2, 1), (300, 8, 5, 2), (120, 5, 3, 3)):  # d=5: f64 staged tables > 128 B
+        from oracle import gmm as G
+        a, mu, icf, x = G.gmm_inputs(n, d, K, seed=seed)
+        dgi, tri, lm, lw = P.gmm_tables(d)
+        mx, ma = P.gmm_stabilizers(a, mu, icf, x)
+        out.append((f"gmm_program_{n}_{d}_{K}", P.gmm_program(n, d, K),
+                    [x, mx, ma, dgi, tri, lm, lw, [a, mu, icf]]))
     # empty index sets (Fin 0): no iteration, zero cells (eval.cpp:295-308, 452-464)
     e0 = np.zeros(0, np.float32)
     out.append(("empty_sum", "main = \\x:((Fin 0)=>Float). sum x\n", [e0]))

@@ -114,3 +114,73 @@ def test_reference_acceptance_gate():
                          timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.count("PASS criterion") == 10, out.stdout
+
+
+# ---- frontend_ext (exp/log, the `<` tangent) -------------------
+
+@pytest.mark.parametrize("n,d,K,gamma,m", [(7, 3, 2, 1.0, 0), (20, 5, 4, 1.0, 0), (33, 4, 3, 0.7, 2),
+                                           (64, 8, 6, 1.0, 0)])
+def test_gmm_program_pins_adbench_restatement(n, d, K, gamma, m):
+    """The ADBench GMM written in the language (programs.gmm_program, exp/log
+    from frontend_ext) and differentiated by the reference's own
+    linearize/transpose, evaluated by the reference evaluator (extended the
+    same way), equals the fp64 ADBench restatement oracle/gmm.py: objective
+    and every gradient entry to 1e-12 -- the GMM oracle is pinned by the
+    reference's evaluator."""
+    from oracle import gmm as G
+    a, mu, icf, x = G.gmm_inputs(n, d, K, seed=n + d)
+    dgi, tri, lm, lw = P.gmm_tables(d)
+    mx, ma = P.gmm_stabilizers(a, mu, icf, x)
+    got = oracle.RefProgram(P.gmm_program(n, d, K, gamma, m))(x, mx, ma, dgi, tri, lm, lw, [a, mu, icf])
+    werr, wda, wdm, wdi = G.gmm_objective_grad(a, mu, icf, x, gamma, m)
+    for g, w in zip(got, (np.array([werr]), wda, wdm.ravel(), wdi.ravel())):
+        assert oracle.rel_diff(g, w) <= 1e-12
+
+
+def test_gmm_program_gradient_is_stabilizer_free():
+    """mx/ma are constants of the gradient (d/dt [m + log sum exp(b - m)]
+    does not depend on m): shifting them changes nothing but rounding."""
+    from oracle import gmm as G
+    n, d, K = 15, 3, 3
+    a, mu, icf, x = G.gmm_inputs(n, d, K, seed=4)
+    tabs = P.gmm_tables(d)
+    mx, ma = P.gmm_stabilizers(a, mu, icf, x)
+    prog = oracle.RefProgram(P.gmm_program(n, d, K))
+    base = prog(x, mx, ma, *tabs, [a, mu, icf])
+    other = prog(x, mx + 3.0, ma - 2.0, *tabs, [a, mu, icf])
+    for u, v in zip(base, other):
+        assert oracle.rel_diff(u, v) <= 1e-12
+
+
+def test_exp_log_finite_differences():
+    """Central finite differences of an exp/log program against its
+    linearize/transpose gradient, in the style of the reference's FD gate
+    (tests/acceptance.cpp:262-284, tolerance 1e-4)."""
+    n = 12
+    r = np.random.default_rng(3)
+    xs = r.standard_normal(n)
+    f_src = (f"main = \\xs:((Fin {n})=>Float). sum (for i. log (1.0 + exp (xs.i)) + "
+             f"exp ((xs.i) * 0.5) * log (2.0 + (xs.i) * (xs.i)))\n")
+    f = oracle.RefProgram(f_src)
+    g_src = (f"main = \\xs:((Fin {n})=>Float).\n  f = \\v:((Fin {n})=>Float). sum (for i. log (1.0 + exp (v.i)) + "
+             f"exp ((v.i) * 0.5) * log (2.0 + (v.i) * (v.i)))\n  grad f xs\n")
+    g = oracle.RefProgram(g_src)(xs)[0]
+    h = 1e-6
+    for i in range(n):
+        e = np.zeros(n)
+        e[i] = h
+        fd = (f(xs + e)[0][0] - f(xs - e)[0][0]) / (2 * h)
+        assert abs(fd - g[i]) <= 1e-4 * max(1.0, abs(g[i]))
+
+
+def test_less_has_a_trivial_tangent():
+    """`<` in a differentiated function linearizes (unit tangent) instead of
+    raising E-tangent.  Its Bool result indexes a table over Either Unit Unit
+    -- a piecewise function such as a (leaky) ReLU, c.(z < 0) * z.  (A case
+    on it whose branches return floats is still rejected: the simplifier
+    turns such a case into a data sum, which has no tangent.)"""
+    src = ("main = \\xs:((Fin 3)=>Float). \\c:((Either Unit Unit)=>Float).\n"
+           "  f = \\v:((Fin 3)=>Float). sum (for i. (c.((v.i) < 0.0)) * ((v.i) * (v.i)))\n"
+           "  grad f xs\n")
+    g = oracle.RefProgram(src)(np.array([1.0, -2.0, 0.5]), np.array([1.0, 0.25]))[0]
+    np.testing.assert_allclose(g, [2.0, -1.0, 1.0], rtol=0, atol=1e-12)
