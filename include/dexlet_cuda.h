@@ -134,6 +134,10 @@ enum {
                                  * communicator of another size (one device
                                  * emulating the ranks); never in production */
   DXL_F_NO_GEMM = 16,      /* contractions through the generic SIMT lowering */
+  DXL_F_COUNT = 64,        /* count work like EvalCounters (eval.hpp:60-65):
+                            * executed + - * /, accum updates, cells; read
+                            * with dxl_program_counters.  Diagnostics mode:
+                            * contractions use the generic (counted) kernels */
   DXL_F_PIPELINE = 32      /* back-to-back runs may overlap: a kernel that
                             * reads only program inputs streams them before
                             * waiting (griddepcontrol.wait) for the previous
@@ -186,6 +190,13 @@ int dxl_program_input_device_ptr(dxl_program* p, int input, int leaf, void** out
 int dxl_program_run(dxl_program* p);
 /* Synchronizes the stream and returns E-bounds if any index check (upload
  * or in-kernel) failed since the leaves were set; DXC_OK otherwise. */
+/* Work counters of the last run (DXL_F_COUNT programs): out[0] arithmetic
+ * ops, out[1] accumulator updates, out[2] cells allocated, out[3]
+ * nodesEvaluated (0: there is no IR walk on the device).  Semantics of
+ * EvalCounters (eval.hpp:60-65) as the lowered program executes them: host-
+ * folded arithmetic and the broadcast updates an accum-to-map replaces are
+ * added statically; a lazy element inlined once is counted once. */
+int dxl_program_counters(dxl_program* p, long long* out4);
 int dxl_program_check(dxl_program* p);
 /* Copies an output leaf to host memory (synchronizes the stream). */
 int dxl_program_get_output(dxl_program* p, int leaf, void* host, int dtype);

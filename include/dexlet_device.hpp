@@ -24,9 +24,13 @@ struct DeviceOptions {
   int world = 1;         // number of GPUs sharing every outer loop
 };
 
-// The device counterpart of evalExpr.  `counters` is accepted for signature
-// compatibility; the device path does not count interpreter work (its unit of
-// work is a kernel, not an IR node) and leaves it untouched.
+// The device counterpart of evalExpr.  With `counters`, the program is
+// lowered in count mode (DXL_F_COUNT) and arithmeticOps / accumUpdates /
+// cellsAllocated receive the work the lowered program executes (the
+// reference's units: one per evaluated + - * /, one per `+=`, one per
+// runAccum / runState cell); nodesEvaluated stays untouched (no IR walk).
+// The reference acceptance gate's work criteria (acceptance.cpp:459-569)
+// run on these counts (tests/test_gpu_full.py::test_work_criteria_*).
 RtPtr evalExprDevice(const EnvPtr& env, const ExprPtr& e, const DeviceOptions& opts = {},
                      EvalCounters* counters = nullptr);
 

@@ -71,6 +71,7 @@ DXL_F_DUMP = 4
 DXL_F_TEST_COMM_MISMATCH = 8
 DXL_F_NO_GEMM = 16
 DXL_F_PIPELINE = 32
+DXL_F_COUNT = 64
 
 LEAF_FLOAT, LEAF_INT, LEAF_INDEX = 0, 1, 2
 DXC_F32, DXC_F64, DXC_I32, DXC_I64, DXC_U32 = 0, 1, 2, 3, 4
@@ -120,6 +121,7 @@ _sig("dxc_host_alloc", ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(_vp))
 _sig("dxc_host_free", ctypes.c_int, _vp)
 _sig("dxc_event_record", ctypes.c_int, _vp, ctypes.POINTER(_vp))
 _sig("dxc_capture_begin", ctypes.c_int, _vp)
+_sig("dxl_program_counters", ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_longlong))
 _sig("dxc_capture_end", ctypes.c_int, _vp, ctypes.POINTER(_vp))
 _sig("dxc_graph_launch", ctypes.c_int, _vp, _vp)
 _sig("dxc_graph_destroy", ctypes.c_int, _vp)
@@ -178,7 +180,7 @@ ABI_SYMBOLS = [
     "dxc_sync", "dxc_buf_alloc", "dxc_buf_free", "dxc_buf_ptr", "dxc_buf_upload", "dxc_buf_download",
     "dxc_buf_zero", "dxc_host_alloc", "dxc_host_free", "dxc_module_compile", "dxc_module_cubin",
     "dxc_launch", "dxc_event_record", "dxc_event_elapsed_ms", "dxc_event_destroy",
-    "dxc_capture_begin", "dxc_capture_end", "dxc_graph_launch", "dxc_graph_destroy",
+    "dxc_capture_begin", "dxc_capture_end", "dxc_graph_launch", "dxc_graph_destroy", "dxl_program_counters",
     "dxc_nccl_unique_id", "dxc_comm_init", "dxc_allreduce_sum", "dxl_program_create",
     "dxl_program_destroy", "dxl_program_num_inputs", "dxl_program_input_num_leaves",
     "dxl_program_input_leaf", "dxl_program_output_num_leaves", "dxl_program_output_leaf",
@@ -390,6 +392,13 @@ class Program:
         if dt is None:
             raise DexError(DXC_E_ARG, f"input {i} leaf {leaf}: unsupported dtype {arr.dtype}")
         _check(_lib.dxl_program_set_input_n(self.handle, i, leaf, arr.ctypes.data_as(_vp), dt, arr.size))
+
+    def counters(self) -> dict:
+        """EvalCounters of the last run (programs created with DXL_F_COUNT)."""
+        out = (ctypes.c_longlong * 4)()
+        _check(_lib.dxl_program_counters(self.handle, out))
+        return {"arithmeticOps": out[0], "accumUpdates": out[1], "cellsAllocated": out[2],
+                "nodesEvaluated": out[3]}
 
     def check(self):
         """Raise DexError(E-bounds) if an index check failed (synchronizes)."""

@@ -70,6 +70,7 @@ SHIM(cuEventElapsedTime, (float* ms, CUevent a, CUevent b), (ms, a, b))
 SHIM(cuEventDestroy, (CUevent e), (e))
 SHIM(cuStreamBeginCapture, (CUstream s, CUstreamCaptureMode m), (s, m))
 SHIM(cuStreamEndCapture, (CUstream s, CUgraph* g), (s, g))
+SHIM(cuStreamIsCapturing, (CUstream s, CUstreamCaptureStatus* st), (s, st))
 SHIM(cuGraphInstantiate, (CUgraphExec* e, CUgraph g, unsigned long long f), (e, g, f))
 SHIM(cuGraphLaunch, (CUgraphExec e, CUstream s), (e, s))
 SHIM(cuGraphExecDestroy, (CUgraphExec e), (e))

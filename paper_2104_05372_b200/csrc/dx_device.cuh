@@ -720,6 +720,25 @@ __device__ __forceinline__ void dx_coop_fold_b(const P* part, long long width, T
   }
 }
 
+// Work counters (count mode, EvalCounters eval.hpp:60-65): per-thread
+// counts summed per warp, one atomic per warp per counter.
+__device__ __forceinline__ void dx_count_add(unsigned long long* c, unsigned long long ops, unsigned long long acc,
+                                             unsigned long long cells) {
+  if (ops) atomicAdd(c, ops);
+  if (acc) atomicAdd(c + 1, acc);
+  if (cells) atomicAdd(c + 2, cells);
+}
+__device__ __forceinline__ void dx_count_flush(unsigned long long* c, unsigned long long ops, unsigned long long acc,
+                                               unsigned long long cells) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ops += __shfl_xor_sync(DX_FULL, ops, o);
+    acc += __shfl_xor_sync(DX_FULL, acc, o);
+    cells += __shfl_xor_sync(DX_FULL, cells, o);
+  }
+  if ((threadIdx.x & 31) == 0) dx_count_add(c, ops, acc, cells);
+}
+
 // Warp-per-column fold of per-block partials [nblk][width] into `cell`:
 // global warp w folds columns w, w + W, ...; lanes take blocks lane, lane +
 // 32, ... in order, then the fixed xor tree.  Deterministic for a fixed grid.

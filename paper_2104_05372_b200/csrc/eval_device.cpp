@@ -158,7 +158,6 @@ void checkRc(int rc) {
 }  // namespace
 
 RtPtr evalExprDevice(const EnvPtr& env, const ExprPtr& e, const DeviceOptions& opts, EvalCounters* counters) {
-  (void)counters;
   // inputs = free variables bound in the environment
   std::vector<std::pair<Name, ValuePtr>> inputs;
   std::vector<RtPtr> values;
@@ -175,6 +174,10 @@ RtPtr evalExprDevice(const EnvPtr& env, const ExprPtr& e, const DeviceOptions& o
   lo.f64 = opts.float64;
   lo.rank = opts.rank;
   lo.world = opts.world;
+  // counters requested: count mode (kernels add the + - * / and += they
+  // execute; see dxl_program_counters for what is added statically)
+  lo.count = counters != nullptr;
+  if (lo.count) lo.noGemm = true;
   dev::Program prog;
   prog.ctx = contextFor(opts.device);
   prog.plan = dev::lowerProgram(e, inputs, lo);
@@ -210,6 +213,13 @@ RtPtr evalExprDevice(const EnvPtr& env, const ExprPtr& e, const DeviceOptions& o
   int flag = 0;
   checkRc(dxrt::check(cuMemcpyDtoH(&flag, prog.devptr[prog.plan.errFlagBuf], 4), "flag"));
   if (flag) fail(ErrCode::OutOfBounds, "an index value is outside its index set");
+  if (counters) {  // EvalCounters semantics (eval.hpp:60-65), summed like the reference's
+    long long c[3] = {0, 0, 0};
+    checkRc(dxrt::check(cuMemcpyDtoH(c, prog.devptr[prog.plan.countBuf], sizeof c), "counters"));
+    counters->arithmeticOps += c[0] + prog.plan.staticOps;
+    counters->accumUpdates += c[1] + prog.plan.staticAccums;
+    counters->cellsAllocated += c[2] + prog.plan.cellsAllocated;
+  }
   // download + unpack outputs
   std::vector<std::vector<double>> outs;
   for (const auto& o : prog.plan.outputs) {

@@ -672,6 +672,7 @@ class Lowering {
   // Cells.
 
   int newCell(const DTy& payload, bool accum) {
+    plan.cellsAllocated++;
     Cell c;
     c.payload = payload;
     c.lv = leaves(payload);
@@ -1151,6 +1152,7 @@ class Lowering {
     if (const auto* b = as<EBinOp>(e)) {
       HV l = hvalue(env, b->l), r = hvalue(env, b->r);
       if (l->k == HVal::Const && r->k == HVal::Const) {
+        if (b->op != BinOp::Less) plan.staticOps++;  // evaluated once, at lowering time
         switch (b->op) {
           case BinOp::Add: return hConstF(l->f + r->f);
           case BinOp::Sub: return hConstF(l->f - r->f);
@@ -1246,6 +1248,7 @@ class Lowering {
     Cell& c = cells[ref->cell];
     if (!c.dirty && !c.lazy && v->k == HVal::Const && v->ty->k == DType::Float) {
       c.host[0][ref->offs[0]] += v->f;
+      plan.staticAccums++;
       return hUnit();
     }
     if (!c.dirty && !c.lazy && v->k == HVal::Pair) {
@@ -1259,6 +1262,7 @@ class Lowering {
       go(v);
       if (ok && fl.size() == ref->offs.size()) {
         for (size_t l = 0; l < fl.size(); ++l) c.host[l][ref->offs[l]] += fl[l];
+        plan.staticAccums++;
         return hUnit();
       }
     }
@@ -1521,6 +1525,7 @@ class Lowering {
     h->st = std::make_shared<LazyState>();
     h->ty = c.payload;
     c.lazy = h;
+    plan.staticAccums += size(d);  // the n broadcast updates the map replaces
     return true;
   }
 
@@ -2285,6 +2290,7 @@ class Lowering {
     if (const auto* a = as<EAccum>(e)) {
       KV ref = kvalue(g, s, a->ref);
       KV v = kvalue(g, s, a->value);
+      if (opt.count) g.line("++dx_cacc;");  // one EAccum (eval.cpp:482-492), any payload
       accumK(g, s, ref, v, e->span);
       return kUnit();
     }
@@ -2304,6 +2310,7 @@ class Lowering {
 
   KV binop(KGen& g, BinOp op, const KV& l, const KV& r, Span sp) {
     if (l->k != KVal::Scalar || r->k != KVal::Scalar) notLowerable("arithmetic on non-scalars", sp);
+    if (opt.count && op != BinOp::Less) g.line("++dx_cops;");  // eval.cpp:500-514 counts each
     int lev = std::max(l->level, r->level);
     if (l->isConst && r->isConst && l->ty->k == DType::Float && r->ty->k == DType::Float) {
       switch (op) {
@@ -2697,6 +2704,7 @@ class Lowering {
     }
     DescPtr d = resolveDesc(f->annot, kernelLook(g, s0));
     if (!descEq(d, payload->desc)) return nullptr;
+    if (opt.count) g.line("dx_cacc += " + lit(size(d)) + ";");  // the broadcast updates the map replaces
     // evaluate the prefix lets, then the map
     KScope s = s0;
     for (const ELet* l : pre) s = kbind(s, l->binder, kexpr(g, s, l->bound, l->annot));
@@ -2728,6 +2736,7 @@ class Lowering {
     if (!ra) fail(ErrCode::Internal, "runAccum reached the lowering unannotated", e->span);
     DTy payload = resolveType(ra->payload, kernelLook(g, s));
     if (KV m = accumToMapK(g, s, r, payload)) return m;
+    if (opt.count) g.line("++dx_ccell;");
     std::vector<Slot> slots = localArrays(g, payload, true);
     std::vector<LeafInfo> plv = leaves(payload);
     if (g.inCand || g.inLaneLoop)
@@ -2747,6 +2756,7 @@ class Lowering {
     KV init = kvalue(g, s, r.init);
     const auto* ra = as<VRefType>(r.action.refAnnot);
     DTy payload = ra ? resolveType(ra->payload, kernelLook(g, s)) : init->ty;
+    if (opt.count) g.line("++dx_ccell;");
     std::vector<Slot> slots = localArrays(g, payload);
     storeK(g, init, slots);
     auto ref = std::make_shared<KVal>();
@@ -3463,7 +3473,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   g.grp = 0;
   g.grpRowCell = -1;
   int grpWarps = 0;
-  if (!serial && g.grpOK && kb0.dims.size() == 1 && !opt.f64 && g.grpTrip >= 4 && g.grpTrip <= 32 &&
+  if (!serial && !opt.count && g.grpOK && kb0.dims.size() == 1 && !opt.f64 && g.grpTrip >= 4 && g.grpTrip <= 32 &&
       32 % g.grpTrip == 0 && total > 0) {
     bool ok = true;
     for (size_t i = 0; i < g.cells.size(); ++i) {
@@ -3506,7 +3516,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     }
   }
   // warp per ordinal for short outer loops over long reductions (row sums)
-  g.warpRow = !serial && g.warpRowOK && g.laneLoopId >= 0 && g.cells.empty() && !hasRow && !g.tile &&
+  g.warpRow = !serial && !opt.count && g.warpRowOK && g.laneLoopId >= 0 && g.cells.empty() && !hasRow && !g.tile &&
               kb0.dims.size() == 1 && total <= 148LL * 256;
   // tiny bodies: several consecutive ordinals per thread (vector loads, ILP)
   int U = g.warpRow ? 1 : (!serial && !hasRow && g.lines <= 16 && g.loopCounter <= (int)kb0.dims.size()) ? 4 : 1;
@@ -3542,6 +3552,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   g.rowSites.clear();
   for (auto& cu : g.cells) cu.pname = param(g, cu.targetBuf, true);
   runParts(g, parts, serial, U, outBufs, outOffs, intoBufs, intoOffs);
+  if (opt.count) param(g, plan.countBuf, true);
 
   // Partial buffers for privatized strategies.
   for (size_t i = 0; i < g.cells.size(); ++i) {
@@ -3696,9 +3707,12 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   { KArg a; a.k = KArg::Buf; a.buf = plan.errFlagBuf; args.push_back(a); }
   for (auto& al : aligns) src << al;
   src << "  int dx_bad = 0;\n";
+  if (opt.count) src << "  unsigned long long dx_cops = 0, dx_cacc = 0, dx_ccell = 0;\n";
 
   if (serial) {
     src << "  if (blockIdx.x != 0 || threadIdx.x != 0) return;\n  {\n" << body << "  }\n";
+    if (opt.count)
+      src << "  dx_count_add((unsigned long long*)" << g.params[plan.countBuf] << ", dx_cops, dx_cacc, dx_ccell);\n";
     src << "  if (dx_bad) atomicOr(dx_err, 1);\n}\n\n";
   } else {
     src << "  const int dx_lane = threadIdx.x & 31, dx_warp = threadIdx.x >> 5;\n";
@@ -4033,6 +4047,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "    __syncthreads();  // every thread is done with this TMA stage\n";
     src << "  }\n";
     }  // g.grp == 0
+    if (opt.count)
+      src << "  dx_count_flush((unsigned long long*)" << g.params[plan.countBuf] << ", dx_cops, dx_cacc, dx_ccell);\n";
     // last-block-done kernels collect the E-bounds flags of the launch in a
     // ticket word; the final block forwards them (and initializes the error
     // flag when this kernel is its first writer)
@@ -4647,6 +4663,10 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
   L.plan.errFlagBuf = L.newBuf(BufDecl::Flag, SK::X, 1);
   {
     Step z; z.k = Step::Zero; z.buf = L.plan.errFlagBuf; z.elems = 1; L.plan.steps.push_back(z);
+  }
+  if (opts.count) {  // [ops, accum updates, cells] of one run
+    L.plan.countBuf = L.newBuf(BufDecl::Flag, SK::I, 3);
+    Step z; z.k = Step::Zero; z.buf = L.plan.countBuf; z.elems = 3; L.plan.steps.push_back(z);
   }
   HEnvP env;
   for (size_t i = 0; i < inputs.size(); ++i) {

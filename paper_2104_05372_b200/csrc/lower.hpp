@@ -124,6 +124,13 @@ struct Plan {
   int errFlagBuf = -1;          // E-bounds flag raised by fused index checks
   int numKernels = 0;
   bool gemm = false;            // uses the tcgen05 contraction kernels (dx_gemm.cuh)
+  // Work counters (EvalCounters, eval.hpp:60-65) in count mode: kernels add
+  // the + - * / they execute and the += they perform into countBuf (2 x u64,
+  // zeroed by the plan's first step); work the lowering did at build time or
+  // replaced wholesale (host-folded arithmetic, accum-to-map broadcasts,
+  // contraction GEMMs) is added as static per-run counts.
+  int countBuf = -1;
+  long long staticOps = 0, staticAccums = 0, cellsAllocated = 0;
   std::string summary() const;
 };
 
@@ -135,6 +142,7 @@ struct LowerOptions {
   bool noRowScatter = false;
   bool noGemm = false;
   bool pipeline = false;  // DXL_F_PIPELINE: stream inputs before the PDL wait
+  bool count = false;     // DXL_F_COUNT: count executed ops / accum updates
 };
 
 // Lowers `e` (first-order, post-optimize) whose free variables are the

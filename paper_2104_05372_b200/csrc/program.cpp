@@ -327,6 +327,18 @@ int Program::run() {
   ctx->makeCurrent();
   if (tmapsDirty && (rc = buildTensorMaps())) return rc;
   if (!useGraph) return issue();
+  {
+    // inside a caller's stream capture (dxc_capture_begin): record this run's
+    // launches into the caller's graph instead of launching the plan's graph
+    CUstreamCaptureStatus cs = CU_STREAM_CAPTURE_STATUS_NONE;
+    if ((rc = dxrt::check(cuStreamIsCapturing(ctx->stream, &cs), "cuStreamIsCapturing"))) return rc;
+    if (cs == CU_STREAM_CAPTURE_STATUS_ACTIVE) {
+      capturing = true;
+      int irc = issue();
+      capturing = false;
+      return irc;
+    }
+  }
   if (!graphExec) {
     // capture the whole plan once; replay it with a single launch per run
     if ((rc = dxrt::check(cuStreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture"))) return rc;
@@ -564,6 +576,9 @@ int dxl_program_create(dxc_ctx* ctx, const char* source, const char* entry, cons
     p->allowCommMismatch = (opts->flags & DXL_F_TEST_COMM_MISMATCH) != 0;
     lo.noGemm = (opts->flags & DXL_F_NO_GEMM) != 0;
     lo.pipeline = (opts->flags & DXL_F_PIPELINE) != 0;
+    // count mode: every contraction through the generic (counted) lowering
+    lo.count = (opts->flags & DXL_F_COUNT) != 0;
+    if (lo.count) lo.noGemm = true;
   }
   std::vector<std::pair<Name, ValuePtr>> params;
   ExprPtr optimized;
@@ -746,6 +761,24 @@ int dxl_program_check(dxl_program* p) {
   int rc = p->readFlags(&flag);
   if (rc) return rc;
   if (flag) { setError("E-bounds: an input ordinal is outside its index set"); return DXC_E_BOUNDS; }
+  return DXC_OK;
+  GUARD_END
+}
+
+int dxl_program_counters(dxl_program* p, long long* out4) {
+  GUARD_BEGIN
+  if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+  if (p->plan.countBuf < 0) { setError("program not created with DXL_F_COUNT"); return DXC_E_ARG; }
+  if (!p->prepared) { setError("program has not run"); return DXC_E_ARG; }
+  p->ctx->makeCurrent();
+  long long c[3] = {0, 0, 0};
+  int rc = dxrt::check(cuMemcpyDtoHAsync(c, p->devptr[p->plan.countBuf], sizeof c, p->ctx->stream), "counters");
+  if (!rc) rc = dxrt::check(cuStreamSynchronize(p->ctx->stream), "cuStreamSynchronize");
+  if (rc) return rc;
+  out4[0] = c[0] + p->plan.staticOps;        // arithmeticOps
+  out4[1] = c[1] + p->plan.staticAccums;     // accumUpdates
+  out4[2] = c[2] + p->plan.cellsAllocated;   // cellsAllocated
+  out4[3] = 0;                               // nodesEvaluated: no IR walk on the device
   return DXC_OK;
   GUARD_END
 }
