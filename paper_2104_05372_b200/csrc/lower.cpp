@@ -313,6 +313,7 @@ struct Slot {
   bool stream = false;
   long long streamL = 0, streamBase = 0;
   int streamU = 0;     // which of the thread's U ordinals (dx_o<u>)
+  long long rowW = 0;  // indexed first by the kernel's dim-0 ordinal: within that row of rowW elements
   std::string rowOff;
 };
 
@@ -415,6 +416,7 @@ struct CellUse {
   int rowSitesN = 0;     // row-eligible accumulation sites (pass 0)
   bool vec4 = false;     // TileRow with float4 column blocks (f32, D % 4 == 0)
   bool warpTab = false;  // TileRow realised as warp-private tables (dx_warp_tab)
+  bool ownRows = true;   // Owner accesses all at row dx_o0 (the rank's own rows when sharded)
   int aliasStage = -1;   // TMA-staged stream buffer whose stage doubles as the row tile
   long long width = 0;
   int partialBuf = -1;
@@ -506,6 +508,9 @@ struct KGen {
   std::set<int> grpStreamBad;
   int grpRowCell = -1;            // pass 1: the row cell's CellUse index
   std::map<std::string, KV> instMemo;  // kernel-level lazy instantiations of this iteration
+  std::string dim0Ord;            // ordinal expression of the first kernel dim (this iteration)
+  std::map<int, std::set<long long>> rowUse;  // pass 0: buf -> row widths of its dim-0-row reads
+  std::set<int> rowBad;                       // pass 0: bufs also read elsewhere
   bool hasBranch = false;         // pass 0: the body branches (keeps group sums eager)
   std::map<std::string, int> grpPending;  // local cells holding per-lane partials (sum deferred)
   std::string curLaneVar;         // variable of the open depth-1 loop
@@ -1709,6 +1714,8 @@ class Lowering {
   // Pass-0 bookkeeping of read-only HBM reads for TMA staging decisions.
   void noteRead(KGen& g, const Slot& s, bool vector) {
     if (g.pass != 0 || !s.global || !s.ro || s.buf < 0) return;
+    if (s.rowW > 0) g.rowUse[s.buf].insert(s.rowW);
+    else g.rowBad.insert(s.buf);
     if (s.stream) {
       auto it = g.streamUse.find(s.buf);
       if (it == g.streamUse.end()) g.streamUse[s.buf] = {s.streamL, s.streamBase};
@@ -2066,7 +2073,11 @@ class Lowering {
           const Slot& src = v->slots[l];
           if (d.global) g.writtenBufs.insert(d.buf);
           std::string q = g.fresh("q");
-          if (src.global && src.ro && g.pass == 0) g.nonStream.insert(src.buf);
+          if (src.global && src.ro && g.pass == 0) {
+            g.nonStream.insert(src.buf);
+            if (src.rowW > 0) g.rowUse[src.buf].insert(src.rowW);
+            else g.rowBad.insert(src.buf);
+          }
           std::string ld = (src.global && src.ro) ? "dx_ld(" + src.base + " + " + eAdd(src.off, q) + ")"
                                                   : src.base + "[" + eAdd(src.off, q) + "]";
           g.line("for (long long " + q + " = 0; " + q + " < " + lit(lv[l].count) + "; ++" + q + ") " +
@@ -2193,6 +2204,8 @@ class Lowering {
           slots[l].streamBase = b0;
           slots[l].rowOff = "0";
         }
+        long long z;
+        if (slots[l].global && o == g.dim0Ord && isIntLit(slots[l].off, &z) && z == 0) slots[l].rowW = el[l].count;
         slots[l].off = eAdd(slots[l].off, eMul(o, el[l].count));
         long long oc;
         slots[l].align = gcdll(slots[l].align, isIntLit(o, &oc) ? alignOf(oc * el[l].count) : el[l].count);
@@ -2842,6 +2855,8 @@ class Lowering {
     if (g.pass == 0) {
       cu.any = true;
       if (!ownerPath(g, ref, ref->cell)) cu.allOwner = false;
+      else if (ref->path.empty() || ref->path[0]->e != g.dim0Ord)
+        cu.ownRows = false;  // the row must be the dim-0 ordinal itself (not n-1-o)
       if (val && val->isConst && val->ty->k == DType::Float && val->cf == std::floor(val->cf) &&
           std::fabs(val->cf) < 1e6) {
         if (!cu.haveConst) { cu.haveConst = true; cu.constVal = val->cf; }
@@ -3249,6 +3264,7 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
         }
       }
     }
+    if (!ords.empty()) g.dim0Ord = ords[0];
     for (const KernelBody& kb : parts) {
       KScope s;
       s.host = kb.env;
@@ -3412,6 +3428,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     g.stateCells.clear();
     g.streamUse.clear();
     g.nonStream.clear();
+    g.rowUse.clear();
+    g.rowBad.clear();
     g.needAlign.clear();
     g.usesErr = false;
     g.usesScratch = false;
@@ -4177,6 +4195,19 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   ks.grp = g.grp;
   ks.coop = coop;
   ks.note = note + (g.warpRow ? " (warp per ordinal)" : "");
+  ks.rwKnown = true;
+  for (auto& [b, pn] : g.params)
+    if (!g.writtenBufs.count(b)) ks.readBufs.insert(b);
+  for (auto& cu : g.cells) ks.readBufs.insert(cu.targetBuf);  // += reads the cell (or its delta)
+  if (g.sharded && !kb0.dims.empty() && total > 0) {
+    const long long n0 = size(kb0.dims[0]);
+    ks.rowBlock = n0 > 0 ? total / n0 : 1;
+    ks.rowsOf = n0;
+    // every read of the buffer is inside the row of the kernel's own dim-0
+    // ordinal (one row width): the rank reads only its own rows
+    for (auto& [b, ws] : g.rowUse)
+      if (!g.rowBad.count(b) && ws.size() == 1) ks.rowReads[b] = *ws.begin();
+  }
   addStep(ks);
   int kstep = (int)plan.steps.size() - 1;
   for (auto& cu : g.cells)
@@ -4204,18 +4235,34 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     if (!g.cells.empty()) {
       Step m;
       m.k = Step::Merge;
-      long long total = 0;
+      long long mtotal = 0;
       for (auto& cu : g.cells) {
-        m.merge.push_back({cu.targetBuf, cells[cu.cell].bufs[cu.leaf], cu.width});
-        total += cu.width;
+        Step::MergeItem mi{cu.targetBuf, cells[cu.cell].bufs[cu.leaf], cu.width};
+        // Owner updates (the path starts with the kernel's own ordinal): each
+        // rank's delta is zero outside its own rows
+        const long long n0 = kb0.dims.empty() ? 0 : size(kb0.dims[0]);
+        if (cu.strat == CellUse::Owner && cu.ownRows && n0 > 0 && cu.width % n0 == 0) {
+          mi.rowN = n0;
+          mi.rowW = cu.width / n0;
+        }
+        m.merge.push_back(mi);
+        mtotal += cu.width;
       }
-      m.buf = newBuf(BufDecl::Temp, SK::D, total * plan.world);  // gathered deltas
-      m.elems = total;
+      m.buf = newBuf(BufDecl::Temp, SK::D, mtotal * plan.world);  // gathered deltas
+      m.elems = mtotal;
       addStep(m);
     }
     for (size_t l = 0; l < outBufs.size(); ++l) {
       Step a; a.k = Step::Allreduce; a.buf = outBufs[l]; a.off = outOffs[l];
       a.elems = leaves(tTable(kb0.desc, elemTy))[l].count;
+      // a map over the kernel's own ordinal: rank r holds rows of its shard
+      bool fwd = true;  // reversed dims store row n-1-o
+      for (auto& kb : parts) fwd = fwd && !kb.dimReversed.empty() && !kb.dimReversed[0];
+      const long long n0 = kb0.dims.empty() ? 0 : size(kb0.dims[0]);
+      if (fwd && outOffs[l] == 0 && n0 > 0 && a.elems % n0 == 0) {
+        a.rowShardN = n0;
+        a.rowShardW = a.elems / n0;
+      }
       addStep(a);
     }
   }
@@ -4342,7 +4389,10 @@ HV Lowering::flattenEffectNest(const HEnvP& env, const EFor& f, const DescPtr& d
   kb.desc = descPair(d, d2);
   kb.dims = {d, d2};
   kb.dimBinders = {f.binder, inner->binder};
-  kb.dimReversed = {false, false};
+  // loops indexed only through `reverse` (transposed nests) run reversed, so
+  // element (i, j) of the body is ordinal (i, j): forward rows, and under
+  // sharding the rank's own rows
+  kb.dimReversed = {onlyReversed(f.binder, body), onlyReversed(inner->binder, body)};
   kb.body = [this, body](KGen& g, const KScope& s) { return kexpr(g, s, body, nullptr); };
   kb.env = env;
   kb.note = "parallel for " + printName(f.binder) + " x " + printName(inner->binder) + " (flattened)";
@@ -4638,6 +4688,15 @@ std::string Plan::summary() const {
       case Step::Kernel:
         o << "kernel " << s.name << (s.serial ? " serial" : "") << (s.coop ? " coop" : "") << " n=" << s.total
           << " smem=" << s.smem << "  // " << s.note;
+        if (world > 1 && s.rwKnown) {  // sharded dataflow: what the kernel reads, own rows marked
+          o << "  [reads";
+          for (int b : s.readBufs) {
+            o << " b" << b;
+            auto it = s.rowReads.find(b);
+            if (it != s.rowReads.end()) o << "(rows of " << s.rowsOf << " x" << it->second << ")";
+          }
+          o << "]";
+        }
         break;
       case Step::Finalize:
         o << "finalize b" << s.buf << " <- partials b" << s.buf2 << " w=" << s.elems
@@ -4655,6 +4714,161 @@ std::string Plan::summary() const {
     o << "\n";
   }
   return o.str();
+}
+
+// Data-parallel dataflow for sharded plans (world > 1).  A sharded kernel
+// over N ordinals leaves rank r with the rows of its chunk of N: the rows of
+// a map it produced (zero-filled elsewhere) and of an Accum cell it updated
+// only at its own ordinal (Owner).  The plan summed such buffers across ranks
+// right after the producer (an Allreduce, or the rank-ordered Merge of the
+// cell deltas).  That collective is dropped when every later reader of the
+// buffer (until it is overwritten) is a sharded kernel over the same N that
+// reads it only at its own ordinal's row of the same width, and the buffer
+// is not a program output: the rows the readers touch are exactly the local
+// ones.  A dropped Merge item becomes a local add of the rank's own delta.
+// This is what keeps batch-sharded networks (configs[4]) from exchanging
+// their activations: only the parameter cotangents are merged.
+static void dropLocalCollectives(Plan& plan) {
+  if (plan.world <= 1) return;
+  std::set<int> outputs;
+  for (auto& o : plan.outputs)
+    if (o.buf >= 0) outputs.insert(o.buf);
+  auto reads = [&](const Step& st, int b) {
+    switch (st.k) {
+      case Step::Zero: return false;
+      case Step::Kernel:
+        if (st.rwKnown) return st.readBufs.count(b) > 0;
+        for (auto& a : st.args)
+          if ((a.k == KArg::Buf || a.k == KArg::TMap) && a.buf == b) return true;
+        return false;
+      case Step::Merge:
+        for (auto& mi : st.merge)
+          if (mi.delta == b || mi.cell == b) return true;
+        return st.buf == b;
+      default: return st.buf == b || st.buf2 == b;
+    }
+  };
+  auto localOnly = [&](size_t from, int b, long long N, long long W) {
+    if (outputs.count(b) || N <= 0 || W <= 0) return false;
+    for (size_t j = from; j < plan.steps.size(); ++j) {
+      const Step& st = plan.steps[j];
+      if (st.dead) continue;
+      if (st.k == Step::Zero && st.buf == b && st.off == 0) return true;  // overwritten: no later reader
+      if (!reads(st, b)) continue;
+      if (st.k != Step::Kernel || !st.rwKnown || !(st.sharded || st.rowsShifted) || st.rowsOf != N) return false;
+      auto it = st.rowReads.find(b);
+      if (it == st.rowReads.end() || it->second != W) return false;
+    }
+    return true;
+  };
+  std::vector<Step> out;
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    Step st = plan.steps[i];
+    if (st.k == Step::Allreduce && localOnly(i + 1, st.buf, st.rowShardN, st.rowShardW)) continue;
+    if (st.k == Step::Merge) {
+      std::vector<Step::MergeItem> keep;
+      std::vector<Step> adds;
+      for (auto& mi : st.merge) {
+        if (localOnly(i + 1, mi.cell, mi.rowN, mi.rowW)) {
+          Step a;
+          a.k = Step::AddBuf;
+          a.buf = mi.cell;
+          a.buf2 = mi.delta;
+          a.elems = mi.elems;
+          adds.push_back(a);
+        } else {
+          keep.push_back(mi);
+        }
+      }
+      if (!keep.empty()) {
+        long long tot = 0;
+        for (auto& mi : keep) tot += mi.elems;
+        st.merge = keep;
+        st.elems = tot;
+        out.push_back(st);
+      }
+      for (auto& a : adds) out.push_back(a);
+      continue;
+    }
+    out.push_back(st);
+  }
+  // kernel step indices referenced by partial buffers / finalize steps moved
+  std::vector<int> remap(plan.steps.size(), -1);
+  // recompute the kernel indices: kernels keep their relative order and are
+  // never dropped, so the k-th kernel step maps to the k-th kernel step
+  std::vector<int> oldK, newK;
+  for (size_t i = 0; i < plan.steps.size(); ++i)
+    if (plan.steps[i].k == Step::Kernel) oldK.push_back((int)i);
+  for (size_t i = 0; i < out.size(); ++i)
+    if (out[i].k == Step::Kernel) newK.push_back((int)i);
+  for (size_t t = 0; t < oldK.size() && t < newK.size(); ++t) remap[oldK[t]] = newK[t];
+  for (auto& st : out)
+    if (st.kernelStep >= 0) st.kernelStep = remap[st.kernelStep];
+  for (auto& b : plan.bufs)
+    if (b.partialKernel >= 0) b.partialKernel = remap[b.partialKernel];
+  plan.steps = out;
+}
+
+// Sharded plans: each Merge (grouped all-gather + rank-ordered fold of Accum
+// deltas) moves down to just before the first later step that touches one of
+// its cells or deltas; merges that meet are fused, so a plan whose cells are
+// read only at the end (a network's parameter cotangents, the loss) does one
+// collective.
+static void fuseMerges(Plan& plan) {
+  if (plan.world <= 1) return;
+  auto touches = [&](const Step& st, const std::set<int>& bufs) {
+    auto hit = [&](int b) { return b >= 0 && bufs.count(b) > 0; };
+    if (hit(st.buf) || hit(st.buf2)) return true;
+    for (auto& a : st.args)
+      if ((a.k == KArg::Buf || a.k == KArg::TMap) && hit(a.buf)) return true;
+    for (auto& mi : st.merge)
+      if (hit(mi.delta) || hit(mi.cell)) return true;
+    return false;
+  };
+  std::vector<Step> out;
+  std::vector<Step> pending;
+  std::set<int> pbufs;
+  auto flush = [&]() {
+    if (pending.empty()) return;
+    Step m = pending[0];
+    for (size_t i = 1; i < pending.size(); ++i)
+      for (auto& mi : pending[i].merge) m.merge.push_back(mi);
+    long long tot = 0;
+    for (auto& mi : m.merge) tot += mi.elems;
+    m.elems = tot;
+    if (pending.size() > 1) {  // one gather buffer for all
+      BufDecl d = plan.bufs[m.buf];
+      d.elems = tot * plan.world;
+      plan.bufs.push_back(d);
+      m.buf = (int)plan.bufs.size() - 1;
+    }
+    out.push_back(m);
+    pending.clear();
+    pbufs.clear();
+  };
+  for (auto& st : plan.steps) {
+    if (st.k == Step::Merge && !st.dead) {
+      pending.push_back(st);
+      for (auto& mi : st.merge) { pbufs.insert(mi.delta); pbufs.insert(mi.cell); }
+      continue;
+    }
+    if (!pending.empty() && touches(st, pbufs)) flush();
+    out.push_back(st);
+  }
+  flush();
+  // kernel indices keep their relative order (kernels never move past each other)
+  std::vector<int> oldK, newK;
+  for (size_t i = 0; i < plan.steps.size(); ++i)
+    if (plan.steps[i].k == Step::Kernel) oldK.push_back((int)i);
+  for (size_t i = 0; i < out.size(); ++i)
+    if (out[i].k == Step::Kernel) newK.push_back((int)i);
+  std::vector<int> remap(plan.steps.size(), -1);
+  for (size_t t = 0; t < oldK.size() && t < newK.size(); ++t) remap[oldK[t]] = newK[t];
+  for (auto& st : out)
+    if (st.kernelStep >= 0) st.kernelStep = remap[st.kernelStep];
+  for (auto& b : plan.bufs)
+    if (b.partialKernel >= 0) b.partialKernel = remap[b.partialKernel];
+  plan.steps = out;
 }
 
 Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>& inputs,
@@ -4732,6 +4946,8 @@ Plan lowerProgram(const ExprPtr& e, const std::vector<std::pair<Name, ValuePtr>>
   L.flushPending();
   L.plan.outputType = res->ty;
   out(res);
+  dropLocalCollectives(L.plan);
+  fuseMerges(L.plan);
   // Dead buffers (e.g. cells whose value stayed lazy and was fused away):
   // drop their zero-fills and never allocate them.
   std::vector<bool> live(L.plan.bufs.size(), false);

@@ -7,6 +7,7 @@
 // primitives of dx_device.cuh) over flat SoA buffers.
 #pragma once
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -87,9 +88,28 @@ struct Step {
   double scale = 1.0;
   // Merge: rank-ordered merge of per-rank Accum deltas into their cells (one
   // grouped NCCL all-gather into buf, then cell = ((cell + d_0) + d_1) + ...)
-  struct MergeItem { int delta, cell; long long elems; };
+  struct MergeItem {
+    int delta, cell;
+    long long elems;
+    long long rowN = 0, rowW = 0;  // Owner-only updates: rows of a rowN-ordinal range, rowW words each
+  };
   std::vector<MergeItem> merge;
   std::string note;
+  // Sharding dataflow (see dropLocalCollectives): the buffers a kernel step
+  // reads; those it reads only at its own ordinal's row (buf -> row length,
+  // base offset 0) over its shard of `total`; and, on an Allreduce of a
+  // sharded kernel's map output, the row sharding of that buffer.
+  bool rwKnown = false;
+  std::set<int> readBufs;
+  std::map<int, long long> rowReads;
+  long long rowsOf = 0;        // rowReads are the rank's rows of this many ordinals
+  std::set<int> rowBad;        // (lowering scratch) bufs read outside the own rows
+  bool rowsShifted = false;    // fixed-grid kernel of a sharded contraction (rowReads valid)
+  long long rowShardN = 0, rowShardW = 0;
+  // Sharded kernels over several flattened dims: the shard is the chunk of
+  // the first dim's ordinals times rowBlock (the product of the others), so
+  // a rank's elements are whole rows of the first dim.
+  long long rowBlock = 1;
 };
 
 struct OutLeaf {

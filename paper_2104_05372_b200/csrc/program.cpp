@@ -135,9 +135,10 @@ int Program::prepare() {
     long long lo = 0, hi = s.total;
     if (s.sharded) {
       int64_t a, b;
-      dxc_chunk_range(s.total, plan.world, plan.rank, &a, &b);
-      lo = a;
-      hi = b;
+      const long long rb = s.rowBlock > 0 ? s.rowBlock : 1;
+      dxc_chunk_range(s.total / rb, plan.world, plan.rank, &a, &b);
+      lo = a * rb;
+      hi = b * rb;
     }
     ranges[i] = {lo, hi};
     if (s.fixedGrid > 0) {

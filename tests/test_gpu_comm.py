@@ -144,3 +144,27 @@ def test_unread_index_leaf_is_range_checked_on_upload():
     prog.set_input(0, 0, keys % 4)
     prog.run()
     prog.check()
+
+
+def test_mlp_world2_shards_sum_to_the_whole():
+    """configs[4] data-parallel on one device: ranks 0 and 1 of a world-2
+    plan (tcgen05 GEMMs on each rank's batch rows, one fused merge through a
+    one-rank NCCL communicator) each return their batch shard's loss and
+    weight gradients; the two summed equal the unsharded program."""
+    import oracle
+    import paper_2104_05372_b200 as dx
+    from paper_2104_05372_b200 import programs as P
+    ctx = dx.Context(0)
+    ctx.init_comm(dx.nccl_unique_id(), 1, 0)
+    b, i, h, o = 2048, 256, 256, 128
+    x, w1, w2 = P.mlp_inputs(b, i, h, o)
+    src = P.mlp_grad(b, i, h, o)
+    whole = dx.Program(src, ctx=ctx)(x, [w1, w2])
+    parts = []
+    for rank in (0, 1):
+        prog = dx.Program(src, ctx=ctx, rank=rank, world=2, flags=dx.F_TEST_COMM_MISMATCH)
+        assert "tcgen05 gemm" in prog.plan and "allreduce" not in prog.plan.split("---")[0]
+        parts.append(prog(x, [w1, w2]))
+    for w, p0, p1 in zip(whole, parts[0], parts[1]):
+        got = np.asarray(p0, dtype=np.float64) + np.asarray(p1, dtype=np.float64)
+        assert oracle.rel_diff(got, np.asarray(w, dtype=np.float64)) <= 1e-4

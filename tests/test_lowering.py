@@ -51,12 +51,14 @@ def test_kmeans_value_and_grad_is_one_fused_kernel():
     assert "zero b" not in prog.plan.split("---")[0], prog.plan
     src = prog.source
     assert "const int dx_gl = dx_lane % 16" in src   # 16 lanes per point
-    assert "dx_grp_sum<16>(" in src                 # the per-point cost: group xor tree
+    assert "dx_grp_sum" not in src                  # per-point costs: lane partials straight into the cost register
     assert "dx_wt1[" in src                          # lane-owned words of the warp's dC table
     assert "dx_warp_tab_flush<16, 64, 20>" in src
-    assert src.count("dx_ldcs(p1 + o * 16LL") == 64  # one point stream: 16 loads x (a, b) x (first, refill)
-    assert ", true);" in src                        # fold overwrites the (never zeroed) cell
-    assert "dx_ticket_barrier(" in src and "dx_coop_fold_w<double, dx_f>" in src
+    # one point stream: 16 loads at constant offsets from one base, for a/b x first/refill x full/ragged
+    assert src.count("__ldcs(dx_b0 + ") == 128
+    assert src.count("__shfl_sync(DX_FULL, gp") == 32  # assignments: one load per chunk, shuffled to the groups
+    assert ", false, true, 1LL);" in src            # fold overwrites the (never zeroed) cell
+    assert "dx_ticket_barrier(" in src and "dx_coop_fold_b<double, dx_f>" in src
     assert "dx_block_sum(rp" in src                 # register partial for the cost
     sass = _sass(src)
     assert "STL" not in sass and "LDL" not in sass  # prefetch buffers stay in registers
@@ -203,3 +205,21 @@ def test_no_experiment_switches_in_library():
         if f.endswith((".cpp", ".inc", ".cuh", ".hpp")):
             found |= set(re.findall(r'getenv\("([A-Z_]+)"\)', open(os.path.join(here, f)).read()))
     assert found <= {"DEXLET_CACHE_DIR", "HOME", "DEXLET_NO_DISK_CACHE", "DEXLET_DUMP_DIR", "DEXLET_DEBUG_CONTRACT"}, found
+
+
+def test_mlp_world2_plan_is_data_parallel():
+    """configs[4] sharded on the batch: every contraction stays
+    on the tensor cores (forward GEMMs split by rows, weight-gradient GEMMs
+    split over K = batch), the activations and their cotangents never leave
+    the rank (no all-reduce of maps), and the Accum deltas -- dW1, dW2 and
+    the loss -- go out in one fused merge (the reference's chunk-order
+    overlay merge, eval.cpp:357-366)."""
+    b, i, h, o = 2048, 256, 256, 128
+    for rank in (0, 1):
+        plan = dx.Program(P.mlp_grad(b, i, h, o), ctx=None, rank=rank, world=2).plan.split("---")[0]
+        assert plan.count("tcgen05 gemm") == 5, plan
+        assert "gemm 1024x256x256" in plan or "gemm 1024x" in plan  # M-split: the rank's 1024 batch rows
+        assert "allreduce" not in plan, plan
+        merges = [l for l in plan.splitlines() if "merge" in l]
+        assert len(merges) == 1, plan
+        assert f"merge 3 Accum deltas ({i * h + h * o + 1} values)" in merges[0], merges
