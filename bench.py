@@ -73,7 +73,7 @@ def _config_spec(name, world):
     if name == "kmeans":
         n = N_PER_GPU * world
         pts, asg, cs = kmeans_inputs_fast(n, D, K)
-        return dict(metric=METRIC, src=P.kmeans_cost_grad(n, D, K), inputs=[[pts], [asg], [cs]],
+        return dict(metric=METRIC, src=P.kmeans_cost_grad(n, D, K), inputs=[[pts], [asg], [cs]], row_inputs=(0, 1),
                     bound="hbm", work=N_PER_GPU * D * 4 + N_PER_GPU * 4 + 2 * K * D * 4,
                     work_basis="n*d*4 (points) + n*4 (assignments) + 2*K*d*4 (centroids in, dC out)",
                     workload="kmeans cost+grad, n=1M points per GPU, d=16, K=64, fixed assignments "
@@ -82,7 +82,7 @@ def _config_spec(name, world):
     if name == "histogram":
         n, k = (1 << 28) * world, 4096
         keys = P.histogram_inputs(n, k)
-        return dict(metric="histogram evals/s (2^28 int32 keys/GPU into 4096 bins)", src=P.histogram(n, k),
+        return dict(metric="histogram evals/s (2^28 int32 keys/GPU into 4096 bins)", src=P.histogram(n, k), row_inputs=(0,),
                     inputs=[[keys]], bound="hbm", work=(1 << 28) * 4 + k * 4,
                     work_basis="n*4 (keys) + k*4 (bins)", workload="index-set histogram h!(p.i) += 1.0, "
                     "2^28 uniform keys per GPU, 4096 bins, bit-exact (BASELINE configs[3])",
@@ -99,7 +99,7 @@ def _config_spec(name, world):
         b, i, h, o = 8192 * world, 1024, 1024, 1024
         x, w1, w2 = P.mlp_inputs(b, i, h, o)
         return dict(metric="MLP fwd+grad evals/s (batch 8192/GPU, 1024^3, square activation)",
-                    src=P.mlp_grad(b, i, h, o), inputs=[[x], [w1, w2]], bound="tensor",
+                    src=P.mlp_grad(b, i, h, o), inputs=[[x], [w1, w2]], row_inputs=(0,), bound="tensor",
                     work=5 * 2 * 8192 * 1024 * 1024,
                     # every GEMM launch of the step is 8192 x 1024 x 1024 (per-launch mean time)
                     work_by_kernel={"dx_gemm_tf32x3_n128": 2 * 8192 * 1024 * 1024,
@@ -225,9 +225,18 @@ class ProgramRunner:
         # overlap (DXL_F_PIPELINE; see include/dexlet_cuda.h)
         self.prog = dx.Program(spec["src"], ctx=ctx, rank=rank, world=world, flags=dx.DXL_F_PIPELINE)
         self.inputs = spec["inputs"]
+        # sharded plans read the batch inputs only at the rank's own rows:
+        # each rank uploads its chunk (dxl_program_set_input_rows)
+        self.rows = {}
         for i, leaves in enumerate(self.inputs):
             for l, arr in enumerate(leaves):
-                self.prog.set_input(i, l, arr)
+                arr = np.asarray(arr)
+                if world > 1 and i in spec.get("row_inputs", ()):
+                    lo, hi = dx.chunk_range(arr.shape[0], world, rank)
+                    self.rows[(i, l)] = (lo, hi)
+                    self.prog.set_input_rows(i, l, arr[lo:hi], lo)
+                else:
+                    self.prog.set_input(i, l, arr)
         self.launches = self.prog.num_launches()
 
     def set_timing(self, on):
@@ -245,12 +254,13 @@ class ProgramRunner:
         self.host = []  # pinned copies of every input leaf
         for i, leaves in enumerate(self.inputs):
             for l, arr in enumerate(leaves):
-                arr = np.ascontiguousarray(arr)
+                rows = self.rows.get((i, l))
+                arr = np.ascontiguousarray(arr if rows is None else np.asarray(arr)[rows[0]:rows[1]])
                 p = ctypes.c_void_p()
                 dx.lib().dxc_host_alloc(arr.nbytes, ctypes.byref(p))
                 ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
                 dt = {np.dtype(np.float32): dx.DXC_F32, np.dtype(np.int32): dx.DXC_I32}[arr.dtype]
-                self.host.append((i, l, p.value, arr.nbytes, dt))
+                self.host.append((i, l, p.value, arr.nbytes, dt, rows))
         self.outs = []
         for leaf, (kind, count) in enumerate(self.prog.output_leaves()):
             p = ctypes.c_void_p()
@@ -261,8 +271,11 @@ class ProgramRunner:
         return sum(h[3] for h in self.host), sum(o[3] for o in self.outs)
 
     def e2e_step(self):
-        for (inp, l, ptr, nb, dt) in self.host:
-            self.prog.set_input_ptr(inp, l, ptr, dt)
+        for (inp, l, ptr, nb, dt, rows) in self.host:
+            if rows is None:
+                self.prog.set_input_ptr(inp, l, ptr, dt)
+            else:
+                self.prog.set_input_rows_ptr(inp, l, ptr, dt, rows[0], rows[1])
         self.prog.run()
         for (leaf, ptr, dt, nb) in self.outs:
             self.prog.get_output_ptr(leaf, ptr, dt)

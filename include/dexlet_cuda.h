@@ -180,6 +180,14 @@ int dxl_program_output_leaf(dxl_program* p, int leaf, int* kind, int64_t* count)
  * by dxl_program_get_output and by dxl_program_check. */
 int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host,
                           int dtype);
+/* Rank-local input shards: host holds only rows [row_lo, row_hi) of the
+ * leaf's leading table dimension (row-major, the leaf's storage type); they
+ * are uploaded into those rows of the device leaf.  A sharded plan reads an
+ * input only at its own rows when its kernels do (the plan dump marks such
+ * reads), so each rank uploads its chunk (dxc_chunk_range) instead of the
+ * whole input. */
+int dxl_program_set_input_rows(dxl_program* p, int input, int leaf, const void* host, int dtype, int64_t row_lo,
+                               int64_t row_hi);
 int dxl_program_set_input_n(dxl_program* p, int input, int leaf, const void* host,
                             int dtype, int64_t count);
 int dxl_program_bind_input_device(dxl_program* p, int input, int leaf,

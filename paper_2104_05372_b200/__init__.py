@@ -144,6 +144,8 @@ _sig("dxl_program_output_leaf", ctypes.c_int, _vp, ctypes.c_int, _ip, _i64p)
 _sig("dxl_program_set_input", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int)
 _sig("dxl_program_set_input_n", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int64)
 _sig("dxl_program_check", ctypes.c_int, _vp)
+_sig("dxl_program_set_input_rows", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int64,
+     ctypes.c_int64)
 _sig("dxl_program_bind_input_device", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _vp)
 _sig("dxl_program_input_device_ptr", ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp))
 _sig("dxl_program_run", ctypes.c_int, _vp)
@@ -181,6 +183,7 @@ ABI_SYMBOLS = [
     "dxc_buf_zero", "dxc_host_alloc", "dxc_host_free", "dxc_module_compile", "dxc_module_cubin",
     "dxc_launch", "dxc_event_record", "dxc_event_elapsed_ms", "dxc_event_destroy",
     "dxc_capture_begin", "dxc_capture_end", "dxc_graph_launch", "dxc_graph_destroy", "dxl_program_counters",
+    "dxl_program_set_input_rows",
     "dxc_nccl_unique_id", "dxc_comm_init", "dxc_allreduce_sum", "dxl_program_create",
     "dxl_program_destroy", "dxl_program_num_inputs", "dxl_program_input_num_leaves",
     "dxl_program_input_leaf", "dxl_program_output_num_leaves", "dxl_program_output_leaf",
@@ -392,6 +395,21 @@ class Program:
         if dt is None:
             raise DexError(DXC_E_ARG, f"input {i} leaf {leaf}: unsupported dtype {arr.dtype}")
         _check(_lib.dxl_program_set_input_n(self.handle, i, leaf, arr.ctypes.data_as(_vp), dt, arr.size))
+
+    def set_input_rows(self, i: int, leaf: int, rows: np.ndarray, row_lo: int):
+        """Upload a rank-local shard: `rows` are rows [row_lo, row_lo + len)
+        of the leaf's leading dimension, in the leaf's storage dtype
+        (float32 / float64 in f64 mode, int32 for index leaves)."""
+        rows = np.ascontiguousarray(rows)
+        dt = _DT_OF.get(rows.dtype)
+        if dt is None:
+            raise DexError(DXC_E_ARG, f"input {i} leaf {leaf}: unsupported dtype {rows.dtype}")
+        n = rows.shape[0] if rows.ndim else 0
+        _check(_lib.dxl_program_set_input_rows(self.handle, i, leaf, rows.ctypes.data_as(_vp), dt, row_lo,
+                                               row_lo + n))
+
+    def set_input_rows_ptr(self, i: int, leaf: int, host_ptr: int, dtype: int, row_lo: int, row_hi: int):
+        _check(_lib.dxl_program_set_input_rows(self.handle, i, leaf, _vp(host_ptr), dtype, row_lo, row_hi))
 
     def counters(self) -> dict:
         """EvalCounters of the last run (programs created with DXL_F_COUNT)."""

@@ -739,6 +739,72 @@ int dxl_program_set_input(dxl_program* p, int input, int leaf, const void* host,
   GUARD_END
 }
 
+// Leading table dimension of leaf `leaf` of a value of type t (rows), 0 when
+// the leaf is not inside a table.
+static long long leadingRows(const DTy& t, int& leaf) {
+  switch (t->k) {
+    case DType::Table:
+      return size(t->desc);
+    case DType::Pair: {
+      std::vector<LeafInfo> la;
+      leavesOf(t->a, la, 1);
+      const int na = (int)la.size();
+      if (leaf < na) return leadingRows(t->a, leaf);
+      leaf -= na;
+      return leadingRows(t->b, leaf);
+    }
+    default:
+      return 0;
+  }
+}
+
+int dxl_program_set_input_rows(dxl_program* p, int input, int leaf, const void* host, int dtype, int64_t row_lo,
+                               int64_t row_hi) {
+  GUARD_BEGIN
+  if (!p->ctx) { setError("no device context"); return DXC_E_ARG; }
+  if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
+      leaf >= (int)p->plan.inputs[input].size()) {
+    setError("bad input leaf");
+    return DXC_E_ARG;
+  }
+  const InLeaf& l = p->plan.inputs[input][leaf];
+  int lf = leaf;
+  const long long rows = leadingRows(p->plan.inputTypes[input], lf);
+  if (rows <= 0 || l.count % rows != 0 || row_lo < 0 || row_hi < row_lo || row_hi > rows) {
+    setError("set_input_rows: rows [" + std::to_string((long long)row_lo) + ", " + std::to_string((long long)row_hi) +
+             ") of a leaf with " + std::to_string(rows) + " rows");
+    return DXC_E_ARG;
+  }
+  const bool f64 = p->plan.f64;
+  const bool direct = (l.kind == SK::F && dtype == (f64 ? DXC_F64 : DXC_F32)) ||
+                      (l.kind == SK::X && dtype == DXC_I32) || (l.kind == SK::I && dtype == DXC_I64);
+  if (!direct) { setError("set_input_rows: the host dtype must be the leaf's storage type"); return DXC_E_ARG; }
+  if (p->boundInputs.count(l.buf)) { setError("input is bound to device memory"); return DXC_E_ARG; }
+  const size_t es = storageBytes(l.kind, f64);
+  const long long w = l.count / rows;
+  p->ctx->makeCurrent();
+  if (!p->prepared) {
+    int rc = p->prepare();
+    if (rc) return rc;
+  }
+  CUdeviceptr dst = p->devptr[l.buf] + (CUdeviceptr)(row_lo * w) * es;
+  const long long n = (row_hi - row_lo) * w;
+  int rc = dxrt::check(cuMemcpyHtoDAsync(dst, host, (size_t)n * es, p->ctx->stream), "input rows upload");
+  if (rc || l.kind != SK::X || n == 0) return rc;
+  int flat = 0;  // index leaves: the range check of the uploaded rows (index_set.cpp:99-106)
+  for (int i = 0; i < input; ++i) flat += (int)p->plan.inputs[i].size();
+  flat += leaf;
+  CUdeviceptr flag = p->upFlags + (CUdeviceptr)flat * 4;
+  if ((rc = dxrt::check(cuMemsetD8Async(flag, 0, 4, p->ctx->stream), "flag reset"))) return rc;
+  long long nn = n;
+  int isz = (int)(l.desc ? size(l.desc) : 0);
+  void* args[4] = {&dst, &nn, &isz, &flag};
+  return dxrt::check(cuLaunchKernel(p->checkIdxFn, (unsigned)std::min<long long>((n + 255) / 256, 1184), 1, 1, 256, 1, 1,
+                                    0, p->ctx->stream, args, nullptr),
+                     "index check");
+  GUARD_END
+}
+
 int dxl_program_set_input_n(dxl_program* p, int input, int leaf, const void* host, int dtype, int64_t count) {
   if (input < 0 || input >= (int)p->plan.inputs.size() || leaf < 0 ||
       leaf >= (int)p->plan.inputs[input].size()) {
