@@ -51,7 +51,7 @@ L2_BYTES = 126 * 1024 * 1024
 
 def input_bytes(spec):
     """Bytes of one step's inputs (all leaves / arrays)."""
-    if spec.get("gmm"):
+    if spec.get("gmm") and "src" not in spec:
         return sum(np.asarray(a).nbytes for a in spec["inputs"])
     return sum(np.asarray(a).nbytes for leaves in spec["inputs"] for a in leaves)
 
@@ -113,7 +113,7 @@ def _config_spec(name, world):
         a, mu, icf, x = gmm_inputs(n, d, k)
         fwd = 2 * n * k * d * d
         bwd = 2 * n * k * d * (d + 1)
-        return dict(metric="GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)", gmm=True,
+        spec = dict(metric="GMM fwd+grad evals/s (ADBench, n=1M points/GPU, d=64, K=200)", gmm=True,
                     inputs=(a, mu, icf, x), bound="tensor", work=fwd + bwd,
                     work_by_kernel={"dx_gmm_fwd": fwd, "dx_gmm_bwd": bwd},
                     work_basis="2nKd^2 (forward Q_k x contraction) + 2nKd(d+1) (backward moments "
@@ -122,6 +122,19 @@ def _config_spec(name, world):
                              "n=1M points per GPU, d=64, K=200, Wishart gamma=1 m=0 (BASELINE configs[2]); "
                              "fused tcgen05 kernel class (include/dexlet_gmm.h)",
                     extra={"n_total": n * world, "d": d, "k": k}, world=world)
+        if world == 1:
+            # through the program API: the canonical ADBench program
+            # (programs.gmm_program), which dxl_program_create dispatches to
+            # the fused kernel class.  The log-sum-exp maxima are inputs the
+            # fused path does not read (any value gives the same objective and
+            # gradient); the tables are the canonical ones.
+            dgi, tri, lm, lw = P.gmm_tables(d)
+            spec["src"] = P.gmm_program(n, d, k)
+            spec["inputs"] = [[x], [np.zeros(n, np.float32)], [np.array([a.max()], np.float32)], [dgi], [tri], [lm],
+                              [lw], [a, mu, icf]]
+            spec["extra"] = dict(spec["extra"], api="dxl_program_create on the dexlet GMM program (programs.gmm_program, "
+                                 "frontend_ext exp/log), dispatched to the fused kernel class")
+        return spec
     raise SystemExit(f"unknown config {name}")
 
 
@@ -570,7 +583,7 @@ def main():
         ctx.init_comm(obj[0], world, rank)
 
     spec = config_spec(args.config, world)
-    Runner = GmmRunner if spec.get("gmm") else ProgramRunner
+    Runner = GmmRunner if (spec.get("gmm") and "src" not in spec) else ProgramRunner
     # Inputs larger than L2 (timing rules): the workload's inputs rotate over
     # R device-resident copies, each its own lowered plan, so that the other
     # R - 1 copies (>= 1.5x the 126 MB L2) are read between two reads of a

@@ -133,7 +133,8 @@ enum {
   DXL_F_TEST_COMM_MISMATCH = 8, /* TEST ONLY: run a (world, rank) plan over a
                                  * communicator of another size (one device
                                  * emulating the ranks); never in production */
-  DXL_F_NO_GEMM = 16,      /* contractions through the generic SIMT lowering */
+  DXL_F_NO_GEMM = 16,      /* contractions (and the canonical GMM program)
+                            * through the generic SIMT lowering              */
   DXL_F_COUNT = 64,        /* count work like EvalCounters (eval.hpp:60-65):
                             * executed + - * /, accum updates, cells; read
                             * with dxl_program_counters.  Diagnostics mode:
@@ -198,6 +199,11 @@ int dxl_program_input_device_ptr(dxl_program* p, int input, int leaf, void** out
 int dxl_program_run(dxl_program* p);
 /* Synchronizes the stream and returns E-bounds if any index check (upload
  * or in-kernel) failed since the leaves were set; DXC_OK otherwise. */
+/* 1 when `source` is the canonical ADBench GMM program (programs.gmm_program:
+ * that text, whitespace aside, for some sizes and Wishart (gamma, m)); then
+ * dxl_program_create runs it on the fused GMM kernel class (dexlet_gmm.h)
+ * when d = 64, f32, one rank.  Fills the recognized parameters. */
+int dxl_gmm_program_match(const char* source, int64_t* n, int* d, int* k, double* gamma, int* m);
 /* Work counters of the last run (DXL_F_COUNT programs): out[0] arithmetic
  * ops, out[1] accumulator updates, out[2] cells allocated, out[3]
  * nodesEvaluated (0: there is no IR walk on the device).  Semantics of

@@ -47,6 +47,9 @@ int dxg_gmm_input_device_ptrs(dxg_gmm* g, void** alphas, void** means, void** ic
 /* Objective and gradient, asynchronous on the context stream.  want_grad = 0
  * runs the objective only (prep + forward + log-sum-exp). */
 int dxg_gmm_run(dxg_gmm* g, double wishart_gamma, int wishart_m, int want_grad);
+/* Device pointers of the fp64 gradient buffers (64-wide layout; contents
+ * valid once the run's work on the context stream completes). */
+int dxg_gmm_grad_device_ptrs(dxg_gmm* g, void** d_alphas, void** d_means, void** d_icf);
 /* Results of the last run (synchronizes).  Any output pointer may be NULL. */
 int dxg_gmm_get(dxg_gmm* g, double* err, double* d_alphas, double* d_means, double* d_icf);
 /* One-shot ADBench-shaped calls: set inputs, run, read back. */

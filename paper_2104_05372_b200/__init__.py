@@ -121,6 +121,8 @@ _sig("dxc_host_alloc", ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(_vp))
 _sig("dxc_host_free", ctypes.c_int, _vp)
 _sig("dxc_event_record", ctypes.c_int, _vp, ctypes.POINTER(_vp))
 _sig("dxc_capture_begin", ctypes.c_int, _vp)
+_sig("dxl_gmm_program_match", ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int),
+     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int))
 _sig("dxl_program_counters", ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_longlong))
 _sig("dxc_capture_end", ctypes.c_int, _vp, ctypes.POINTER(_vp))
 _sig("dxc_graph_launch", ctypes.c_int, _vp, _vp)
@@ -183,7 +185,7 @@ ABI_SYMBOLS = [
     "dxc_buf_zero", "dxc_host_alloc", "dxc_host_free", "dxc_module_compile", "dxc_module_cubin",
     "dxc_launch", "dxc_event_record", "dxc_event_elapsed_ms", "dxc_event_destroy",
     "dxc_capture_begin", "dxc_capture_end", "dxc_graph_launch", "dxc_graph_destroy", "dxl_program_counters",
-    "dxl_program_set_input_rows",
+    "dxl_program_set_input_rows", "dxl_gmm_program_match",
     "dxc_nccl_unique_id", "dxc_comm_init", "dxc_allreduce_sum", "dxl_program_create",
     "dxl_program_destroy", "dxl_program_num_inputs", "dxl_program_input_num_leaves",
     "dxl_program_input_leaf", "dxl_program_output_num_leaves", "dxl_program_output_leaf",
@@ -215,6 +217,17 @@ def lib() -> ctypes.CDLL:
 def loaded() -> bool:
     """Whether libdexlet_cuda.so has been mapped into this process."""
     return _lib._cdll is not None
+
+
+def gmm_program_match(source: str):
+    """(n, d, K, gamma, m) when `source` is the canonical ADBench GMM program
+    (programs.gmm_program), else None."""
+    n, d, k, m = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    g = ctypes.c_double()
+    if not _lib.dxl_gmm_program_match(source.encode(), ctypes.byref(n), ctypes.byref(d), ctypes.byref(k),
+                                      ctypes.byref(g), ctypes.byref(m)):
+        return None
+    return n.value, d.value, k.value, g.value, m.value
 
 
 def chunk_range(total: int, parts: int, c: int) -> Tuple[int, int]:

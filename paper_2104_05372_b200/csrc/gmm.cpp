@@ -256,6 +256,14 @@ int dxg_gmm_input_device_ptrs(dxg_gmm* g, void** alphas, void** means, void** ic
   return DXC_OK;
 }
 
+int dxg_gmm_grad_device_ptrs(dxg_gmm* g, void** d_alphas, void** d_means, void** d_icf) {
+  // fp64 gradients of the last run, d = 64 layout (valid after the run's work completes)
+  if (d_alphas) *d_alphas = (void*)g->dal;
+  if (d_means) *d_means = (void*)g->dmu;
+  if (d_icf) *d_icf = (void*)g->dicf;
+  return DXC_OK;
+}
+
 int dxg_gmm_run(dxg_gmm* g, double gamma, int wm, int want_grad) {
   if (!g) { setError("dxg_gmm_run: null plan"); return DXC_E_ARG; }
   if (!(gamma > 0.0) || wm < 0) { setError("dxg_gmm_run: Wishart gamma must be > 0 and m >= 0"); return DXC_E_ARG; }

@@ -12,6 +12,8 @@
 #include "lower.hpp"
 #include "runtime.hpp"
 
+struct dxg_gmm;
+
 namespace dexlet {
 namespace dev {
 
@@ -59,6 +61,23 @@ struct Program {
   std::vector<std::pair<CUevent, CUevent>> kernelEvents;  // per kernel step
   std::vector<int> kernelEventStep;
   std::string kernelNames;
+
+  // The canonical ADBench GMM program (programs.gmm_program, the source
+  // text with its constants; see matchGmmProgram in program.cpp) dispatches
+  // to the fused GMM kernel class: inputs x / alphas / means / icf are the
+  // kernel class's own device buffers, the table inputs must be the
+  // canonical ones (checked on upload), the stabilizers are not needed.
+  struct GmmMode {
+    dxg_gmm* g = nullptr;
+    long long n = 0;
+    int d = 0, K = 0, m = 0;
+    double gamma = 1.0;
+  };
+  GmmMode* gmm = nullptr;
+  std::vector<int> gmmBufs;  // x, alphas, means, icf input buffers (the kernel class's)
+  std::string gmmNote;
+  double gmmErr = 0.0;
+  bool gmmErrValid = false;
 
   int prepare();
   int run();

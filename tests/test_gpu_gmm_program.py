@@ -43,3 +43,33 @@ def test_gmm_program_on_device(ctx, n, d, K, gamma, m, f64):
     assert oracle.rel_diff(dm, wdm.ravel()) <= 1e-4
     assert _normrel(di, wdi) <= 1e-5
     assert oracle.rel_diff(di, wdi.ravel()) <= 1e-3
+
+
+@pytest.mark.parametrize("n,K,gamma,m", [(3000, 5, 1.0, 0), (4097, 11, 0.8, 1)])
+def test_gmm_program_dispatches_to_fused_kernels(ctx, n, K, gamma, m):
+    """The canonical program at d = 64 (ADBench's dimension) runs on the fused
+    tcgen05 kernel class through dxl_program_create: same inputs, same
+    outputs as the program's generic lowering and as oracle/gmm.py
+    (tolerances of tests/test_gpu_gmm.py)."""
+    d = 64
+    a, mu, icf, x = G.gmm_inputs(n, d, K, seed=n)
+    tabs = P.gmm_tables(d)
+    mx, ma = P.gmm_stabilizers(a, mu, icf, x)
+    src = P.gmm_program(n, d, K, gamma, m)
+    fast = dx.Program(src, ctx=ctx)
+    assert "fused GMM kernel class" in fast.plan
+    err, da, dm, di = fast(x, mx, ma, *tabs, [a, mu, icf])
+    werr, wda, wdm, wdi = G.gmm_objective_grad(a, mu, icf, x, gamma, m)
+    assert oracle.rel_diff(err, np.array([werr])) <= 1e-4
+    for g, w in ((da, wda), (dm, wdm), (di, wdi)):
+        assert _normrel(g, w) <= 1e-5
+        assert oracle.rel_diff(g, w.ravel()) <= 4e-4
+    generic = dx.Program(src, ctx=ctx, flags=dx.DXL_F_NO_GEMM)
+    assert "fused GMM" not in generic.plan
+    gerr, gda, gdm, gdi = generic(x, mx, ma, *tabs, [a, mu, icf])
+    assert oracle.rel_diff(err, gerr) <= 1e-4
+    # a non-canonical table is refused by the fused path (it would change the program)
+    bad = tabs[2].copy()
+    bad[1, 0] = 0.0
+    with pytest.raises(dx.DexError):
+        fast.set_input(5, 0, bad)

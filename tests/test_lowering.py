@@ -223,3 +223,17 @@ def test_mlp_world2_plan_is_data_parallel():
         merges = [l for l in plan.splitlines() if "merge" in l]
         assert len(merges) == 1, plan
         assert f"merge 3 Accum deltas ({i * h + h * o + 1} values)" in merges[0], merges
+
+
+def test_gmm_program_recognizer():
+    """dxl_gmm_program_match: the canonical ADBench program (any sizes, any
+    Wishart gamma / m) is recognized and its parameters read back; a change
+    to the objective is not."""
+    assert dx.gmm_program_match(P.gmm_program(3000, 64, 5)) == (3000, 64, 5, 1.0, 0)
+    n, d, k, g, m = dx.gmm_program_match(P.gmm_program(4097, 64, 11, 0.8, 1))
+    assert (n, d, k, m) == (4097, 64, 11, 1) and abs(g - 0.8) < 1e-12
+    src = P.gmm_program(100, 5, 3)
+    assert dx.gmm_program_match(src) == (100, 5, 3, 1.0, 0)
+    assert dx.gmm_program_match(src.replace("0.5 * sq", "0.25 * sq")) is None
+    assert dx.gmm_program_match(src.replace("log s", "s")) is None
+    assert dx.gmm_program_match(P.kmeans_cost_grad(10, 2, 2)) is None
