@@ -198,7 +198,7 @@ ABI_SYMBOLS = [
 #: every symbol declared in include/dexlet_gmm.h
 GMM_ABI_SYMBOLS = [
     "dxg_gmm_create", "dxg_gmm_destroy", "dxg_gmm_set_params", "dxg_gmm_set_points",
-    "dxg_gmm_input_device_ptrs", "dxg_gmm_run", "dxg_gmm_get", "dxg_gmm_objective",
+    "dxg_gmm_input_device_ptrs", "dxg_gmm_grad_device_ptrs", "dxg_gmm_run", "dxg_gmm_get", "dxg_gmm_objective",
     "dxg_gmm_objective_grad", "dxg_gmm_enable_timing", "dxg_gmm_kernel_times",
 ]
 GMM_KERNELS = ["dx_gmm_absmax", "dx_gmm_prep_q", "dx_gmm_prep_x", "dx_gmm_fwd", "dx_gmm_lse", "dx_gmm_sum", "dx_gmm_bwd",
