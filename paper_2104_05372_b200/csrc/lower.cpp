@@ -4073,14 +4073,37 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     const bool lbdErr = lbd && takeZero(plan.errFlagBuf);
     const bool coopErr = coop && takeZero(plan.errFlagBuf);
     if (!lbd && !coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
-    // epilogue: block partials
+    // epilogue: block partials.  Register cells: warp sums into scratch
+    // first; the block barrier they need is the one the next flush (or an
+    // explicit one) executes anyway; warp 0 then adds the warp sums (the
+    // dx_block_sum tree, one barrier instead of two).
+    bool regPending = false;
+    for (size_t i = 0; i < g.cells.size(); ++i)
+      if (g.cells[i].strat == CellUse::Reg) {
+        const std::string I = std::to_string(i);
+        src << "  __shared__ dx_f scr" << I << "[32];\n  { const dx_f s = dx_warp_sum(rp" << I
+            << "); if (dx_lane == 0) scr" << I << "[dx_warp] = s; }\n";
+        regPending = true;
+      }
+    auto regFinish = [&]() {
+      if (!regPending) return;
+      for (size_t i = 0; i < g.cells.size(); ++i)
+        if (g.cells[i].strat == CellUse::Reg) {
+          const std::string I = std::to_string(i);
+          src << "  if (dx_warp == 0) { dx_f r = dx_lane < (int)((blockDim.x + 31) >> 5) ? scr" << I
+              << "[dx_lane] : (dx_f)0; r = dx_warp_sum(r); if (dx_lane == 0) part" << I << "[blockIdx.x] = r; }\n";
+        }
+      regPending = false;
+    };
+    bool synced = false;  // a flush below began with a block barrier
     for (size_t i = 0; i < g.cells.size(); ++i) {
       CellUse& cu = g.cells[i];
       std::string I = std::to_string(i);
+      if (cu.strat == CellUse::Smem || cu.strat == CellUse::Count || cu.strat == CellUse::Row ||
+          (cu.strat == CellUse::TileRow && cu.warpTab))
+        synced = true;
       switch (cu.strat) {
         case CellUse::Reg:
-          src << "  { __shared__ dx_f scr" << I << "[32]; dx_f s = dx_block_sum(rp" << I << ", scr" << I
-              << "); if (threadIdx.x == 0) part" << I << "[blockIdx.x] = s; }\n";
           break;
         case CellUse::Smem:
         case CellUse::Count:
@@ -4113,6 +4136,8 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
         default: break;
       }
     }
+    if (regPending && !synced) src << "  __syncthreads();\n";
+    regFinish();
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
       src << "  dx_ticket_barrier((unsigned long long*)" << g.params[syncBuf] << ");\n";
