@@ -247,7 +247,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         while (true) {
           unsigned v;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(tickets + tile) : "memory");
-          if ((int)(v % (unsigned)S) == part) break;
+          if ((int)v == part) break;
           __nanosleep(64);
         }
       }
@@ -306,7 +306,12 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
     if (S > 1) {  // release the next part
       __threadfence();
       asm volatile("bar.sync 1, %0;" ::"n"(EW * 32) : "memory");
-      if (threadIdx.x == 0) atomicAdd(tickets + tile, 1u);
+      // the last part resets the tile's ticket: it stays in [0, S) and never
+      // wraps (S need not divide 2^32)
+      if (threadIdx.x == 0) {
+        if (part == S - 1) atomicExch(tickets + tile, 0u);
+        else atomicAdd(tickets + tile, 1u);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
