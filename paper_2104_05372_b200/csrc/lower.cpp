@@ -3497,7 +3497,11 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     for (size_t i = 0; i < g.cells.size(); ++i) {
       const CellUse& cu = g.cells[i];
       if (cu.strat == CellUse::Reg) continue;
-      if (cu.strat == CellUse::TileRow && cu.rowD == g.grpTrip && g.grpRowCell < 0 && cu.width % cu.rowD == 0) {
+      // any row-scatter cell (TileRow, or Row / Smem when the tile sort's
+      // limits ruled TileRow out) becomes the group's lane-owned table
+      if (cu.allRow && cu.rowSitesN == 1 && cu.rowD == g.grpTrip && g.grpRowCell < 0 && cu.width % cu.rowD == 0 &&
+          cells[cu.cell].lv[cu.leaf].kind == SK::F &&
+          (cu.strat == CellUse::TileRow || cu.strat == CellUse::Row || cu.strat == CellUse::Smem)) {
         g.grpRowCell = (int)i;
         continue;
       }
@@ -3512,6 +3516,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   }
   if (g.grp > 0) {
     CellUse& rc = g.cells[g.grpRowCell];
+    rc.strat = CellUse::TileRow;
     rc.warpTab = true;
     rc.vec4 = true;
     rc.aliasStage = -1;
