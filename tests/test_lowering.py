@@ -59,7 +59,7 @@ def test_kmeans_value_and_grad_is_one_fused_kernel():
     assert src.count("__shfl_sync(DX_FULL, gp") == 32  # assignments: one load per chunk, shuffled to the groups
     assert ", false, true, 1LL);" in src            # fold overwrites the (never zeroed) cell
     assert "dx_ticket_barrier(" in src and "dx_coop_fold_b<double, dx_f>" in src
-    assert "dx_block_sum(rp" in src                 # register partial for the cost
+    assert "dx_warp_sum(rp0)" in src                # register partial for the cost: warp sums share the table flush's barrier
     sass = _sass(src)
     assert "STL" not in sass and "LDL" not in sass  # prefetch buffers stay in registers
 
