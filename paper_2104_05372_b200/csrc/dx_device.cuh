@@ -607,6 +607,14 @@ __device__ __forceinline__ void dx_grid_barrier(unsigned* bar) {
 __device__ __forceinline__ void dx_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void dx_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Bulk L2 prefetch (TMA engine, no registers or shared memory): group mode
+// asks for the rows of the chunk after next while the next one is loading.
+// Needs a 16-byte aligned start (checked) and a size multiple of 16.
+__device__ __forceinline__ void dx_l2_prefetch(const void* p, unsigned bytes) {
+  if (((unsigned long long)p & 15ull) == 0ull)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Streaming (evict-first) loads for rows read once.
 __device__ __forceinline__ float dx_ldcs(const float* p) {
   float v;

@@ -52,7 +52,9 @@ def test_kmeans_value_and_grad_is_one_fused_kernel():
     src = prog.source
     assert "const int dx_gl = dx_lane % 16" in src   # 16 lanes per point
     assert "dx_grp_sum" not in src                  # per-point costs: lane partials straight into the cost register
-    assert "dx_wt1[" in src                          # lane-owned words of the warp's dC table
+    assert "*(float*)((char*)dx_wtl1 + " in src      # lane-owned words of the warp's dC table
+    assert "wtg3" in src                             # centroids: one interleaved copy per group (no bank conflicts)
+    assert src.count("dx_l2_prefetch(") >= 3         # TMA bulk L2 prefetch of the chunk after next
     assert "dx_warp_tab_flush<16, 64, 20>" in src
     # one point stream: 16 loads at constant offsets from one base, for a/b x first/refill x full/ragged
     assert src.count("__ldcs(dx_b0 + ") == 128
