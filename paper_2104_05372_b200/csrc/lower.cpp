@@ -3627,7 +3627,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
   int tickBuf = -1, syncBuf = -1;
   std::vector<int> gpartBuf(g.cells.size(), -1);
   if (coop) {
-    syncBuf = newBuf(BufDecl::Sync, SK::U32, 2);
+    syncBuf = newBuf(BufDecl::Sync, SK::U32, 2 * 16 * 8);  // DX_NCTR counters, one 128-byte line each
     param(g, syncBuf, true);
   }
   if (lbd) {
@@ -3771,6 +3771,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       if (!g.writtenBufs.count(b) && plan.bufs[b].role != BufDecl::Input && plan.bufs[b].role != BufDecl::Const)
         lateWait = false;
     if (!lateWait) src << "  dx_pdl_wait();\n";
+    if (!lateWait && coop)
+      src << "  unsigned long long dx_ep = 0;\n  if (threadIdx.x < DX_NCTR) dx_ep = dx_bar_epoch((const unsigned long long*)"
+          << g.params[syncBuf] << ");\n";
     if (g.grp > 0) {
       // group mode: chunk c of a warp = ordinals [c*CH, c*CH + CH), group gi
       // takes ordinals c*CH + u*GPW + gi (u < U); the rows it reads at its
@@ -4045,6 +4048,9 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       src << "  }\n";
       src << "  dx_pdl_trigger();\n";
       if (lateWait) src << "  dx_pdl_wait();\n";
+      if (lateWait && coop)
+        src << "  unsigned long long dx_ep = 0;\n  if (threadIdx.x < DX_NCTR) dx_ep = dx_bar_epoch((const unsigned long long*)"
+            << g.params[syncBuf] << ");\n";
     } else if (g.warpRow) {
       // one warp per ordinal (warp-uniform), the lanes split the reduction loop
       src << "  for (long long dx_base = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dx_base < dx_n; dx_base += dx_stride >> 5) {\n";
@@ -4197,7 +4203,7 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
     regFinish();
     if (coop) {
       if (coopErr) src << "  if (blockIdx.x == 0 && threadIdx.x == 0) *dx_err = 0;\n";
-      src << "  dx_ticket_barrier((unsigned long long*)" << g.params[syncBuf] << ");\n";
+      src << "  dx_spread_barrier((unsigned long long*)" << g.params[syncBuf] << ", dx_ep);\n";
       if (coopErr) src << "  if (dx_bad) atomicOr(dx_err, 1);\n";
       long long foldBase = 0;
       for (size_t i = 0; i < g.cells.size(); ++i) {

@@ -60,7 +60,7 @@ def test_kmeans_value_and_grad_is_one_fused_kernel():
     assert src.count("__ldcs(dx_b0 + ") == 128
     assert src.count("__shfl_sync(DX_FULL, gp") == 32  # assignments: one load per chunk, shuffled to the groups
     assert ", false, true, 1LL);" in src            # fold overwrites the (never zeroed) cell
-    assert "dx_ticket_barrier(" in src and "dx_coop_fold_b<double, dx_f>" in src
+    assert "dx_spread_barrier(" in src and "dx_coop_fold_b<double, dx_f>" in src
     assert "dx_warp_sum(rp0)" in src                # register partial for the cost: warp sums share the table flush's barrier
     sass = _sass(src)
     assert "STL" not in sass and "LDL" not in sass  # prefetch buffers stay in registers
