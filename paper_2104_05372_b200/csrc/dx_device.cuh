@@ -676,8 +676,11 @@ __device__ __forceinline__ unsigned long long dx_bar_epoch(const unsigned long l
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr + i * 16) : "memory");
   return v / cnt;
 }
-__device__ __forceinline__ void dx_spread_barrier(unsigned long long* ctr, unsigned long long epoch) {
+// `epoch`: a shared variable thread 0 set from dx_bar_epoch (kept out of
+// registers across the kernel's main loop)
+__device__ __forceinline__ void dx_spread_barrier(unsigned long long* ctr, const unsigned long long& epoch_s) {
   __syncthreads();
+  const unsigned long long epoch = epoch_s;
   if (threadIdx.x == 0)
     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr + (blockIdx.x % DX_NCTR) * 16) : "memory");
   if (threadIdx.x < DX_NCTR && threadIdx.x < gridDim.x) {
