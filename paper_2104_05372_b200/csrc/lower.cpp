@@ -417,6 +417,10 @@ struct CellUse {
   bool vec4 = false;     // TileRow with float4 column blocks (f32, D % 4 == 0)
   bool warpTab = false;  // TileRow realised as warp-private tables (dx_warp_tab)
   bool ownRows = true;   // Owner accesses all at row dx_o0 (the rank's own rows when sharded)
+  bool ownTop = true;    // Owner sites all unconditional at kernel level, at the ordinal's own element
+  bool overwrite = false, firstDone = false;  // first site stores (the cell's zero-fill was dropped)
+  std::string ownKey;    // the owner sites' element index (all sites must agree: ordinal o and n-1-o
+                         // from two sites would be two threads' read-modify-writes of one element)
   int aliasStage = -1;   // TMA-staged stream buffer whose stage doubles as the row tile
   long long width = 0;
   int partialBuf = -1;
@@ -1336,6 +1340,10 @@ class Lowering {
         st.buf2 = src->bufs[l];
         st.off2 = src->offs[l];
         st.elems = lv[l].count;
+        // into a whole cell right after its zero-fill: a copy (or an f32 ->
+        // f64 conversion) replaces the zero pass and the read-modify-write
+        if (st.off == 0 && st.elems == plan.bufs[st.buf].elems && takeZero(st.buf))
+          st.k = plan.bufs[st.buf].kind == plan.bufs[st.buf2].kind ? Step::CopyBuf : Step::Convert;
         addStep(st);
       }
     }
@@ -2864,9 +2872,13 @@ class Lowering {
     if (g.pass == 0 && grpTop && cu.width != 1) g.grpOK = false;
     if (g.pass == 0) {
       cu.any = true;
-      if (!ownerPath(g, ref, ref->cell)) cu.allOwner = false;
-      else if (ref->path.empty() || ref->path[0]->e != g.dim0Ord)
+      std::string key;
+      if (ownerPath(g, ref, ref->cell))
+        for (size_t i = 0; i < g.kernelVars.size(); ++i) key += ref->path[i]->e + ";";
+      if (!ownerPath(g, ref, ref->cell) || (!cu.ownKey.empty() && cu.ownKey != key)) cu.allOwner = false;
+      else if ((cu.ownKey = key), ref->path.empty() || ref->path[0]->e != g.dim0Ord)
         cu.ownRows = false;  // the row must be the dim-0 ordinal itself (not n-1-o)
+      if (!grpTop || s.inBranch || ref->path.size() != g.kernelVars.size()) cu.ownTop = false;
       if (val && val->isConst && val->ty->k == DType::Float && val->cf == std::floor(val->cf) &&
           std::fabs(val->cf) < 1e6) {
         if (!cu.haveConst) { cu.haveConst = true; cu.constVal = val->cf; }
@@ -2897,7 +2909,13 @@ class Lowering {
     switch (cu.strat) {
       case CellUse::Owner:
       case CellUse::Direct:
-        g.line(tgt + "[" + sl.off + "] += " + valE + ";");
+        if (cu.overwrite && !cu.firstDone) {
+          // every ordinal's first (unconditional) write to its own element
+          g.line(tgt + "[" + sl.off + "] = " + valE + ";");
+          cu.firstDone = true;
+        } else {
+          g.line(tgt + "[" + sl.off + "] += " + valE + ";");
+        }
         break;
       case CellUse::Reg:
         if (g.grp > 0 && grpTop && val && !val->grpPart.empty() && valE == val->e)  // lane partials
@@ -3260,6 +3278,7 @@ KV Lowering::runParts(KGen& g, const std::vector<KernelBody>& parts, bool serial
   for (int u = 0; u < (serial ? 1 : U); ++u) {
     std::string o = serial ? "0" : "dx_o" + std::to_string(u);
     g.instMemo.clear();  // each ordinal's block has its own variables
+    for (auto& cu : g.cells) cu.firstDone = false;  // each ordinal's first owner write stores
     if (!serial && U > 1) g.line(g.grp > 0 ? "if (dx_ok" + std::to_string(u) + ") {" : "if (" + o + " < dx_hi) {");
     if (!serial && U > 1) g.ind++;
     // dimension ordinals of this iteration
@@ -3581,6 +3600,13 @@ HV Lowering::emitKernel(const std::vector<KernelBody>& parts, bool serial, const
       cu.targetBuf = newBuf(BufDecl::Temp, plan.bufs[c.bufs[cu.leaf]].kind, cu.width);
       Step z; z.k = Step::Zero; z.buf = cu.targetBuf; z.elems = cu.width; addStep(z);
     }
+    // an owner-computed cell whose every element is written by its own
+    // ordinal, unconditionally, right after the cell's zero-fill: the first
+    // write stores (no zero pass over HBM, no read-modify-write)
+    cu.overwrite = cu.firstDone = false;
+    if (cu.strat == CellUse::Owner && cu.any && cu.ownTop && !serial && !g.sharded && plan.world == 1 && !opt.count &&
+        g.grp == 0 && parts.size() == 1 && total == cu.width && takeZero(cu.targetBuf))
+      cu.overwrite = true;
   }
   // pass 1: emission
   std::string body;

@@ -230,3 +230,34 @@ def test_group_mode_pipelined_runs_match(ctx):
     got = [b.get_output(0), b.get_output(1)]
     for x, y in zip(want, got):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("n", [10, 1 << 20])
+def test_revdot_grad_two_index_forms(ctx, n):
+    """grad of sum v.i * v.(reverse i) writes the cotangent at i and at n-1-i
+    from the same ordinal: two threads touch each element, so the cell must
+    not be owner-computed (was a cross-warp read-modify-write race at large
+    n).  Exact answer 2 v[n-1-i]."""
+    rng = np.random.default_rng(n)
+    v = rng.standard_normal(n).astype(np.float32)
+    g = dx.Program(P.revdot_grad(n), ctx=ctx)(v)
+    g = g[0] if isinstance(g, (tuple, list)) else g
+    want = 2.0 * v[::-1].astype(np.float64)
+    assert oracle.rel_diff(np.asarray(g, dtype=np.float64).ravel(), want) <= 1e-6
+
+
+def test_owner_cells_overwrite_after_zero(ctx):
+    """Owner-computed cells written right after their zero-fill are stored
+    (no zero pass, no read-modify-write); GEMM cell outputs likewise.  The
+    MLP plan carries no zero-fill besides the scalar loss, and the gradients
+    still match the fp64 restatement (small widths, 1e-4)."""
+    x, w1, w2 = P.mlp_inputs(512, 64, 64, 32)
+    prog = dx.Program(P.mlp_grad(512, 64, 64, 32), ctx=ctx)
+    loss, d1, d2 = prog(x, [w1, w2])
+    rl, r1, r2 = restate.mlp_grad(x, w1, w2)
+    assert oracle.rel_diff(loss, np.array([rl])) <= 1e-4
+    assert oracle.rel_diff(d1, r1.ravel()) <= 1e-4
+    assert oracle.rel_diff(d2, r2.ravel()) <= 1e-4
+    # repeated runs: the stored cells do not accumulate across runs
+    loss2, e1, e2 = prog(x, [w1, w2])
+    assert np.array_equal(d1, e1) and np.array_equal(d2, e2)
