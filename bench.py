@@ -369,10 +369,10 @@ def peaks(bound="hbm"):
 
 def traffic_per_launch(config="kmeans", kernel=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from
-    the committed ncu --set full capture (profiles/{r02b,r01f,r01e,r01d,r01c}_<config>_ncu_summary.json,
+    the committed ncu --set full capture (profiles/{r02c,r02b,r01f,r01e,r01d,r01c}_<config>_ncu_summary.json,
     newest first), per launch; None when no capture of that kernel is committed."""
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for tag in ("r02b", "r01f", "r01e", "r01d", "r01c"):
+    for tag in ("r02c", "r02b", "r01f", "r01e", "r01d", "r01c"):
         p = os.path.join(ROOT, "profiles", f"{tag}_{config}_ncu_summary.json")
         if not os.path.exists(p):
             continue
