@@ -1,20 +1,24 @@
 // dx_gemm.cuh — hand-written sm_100a tensor-core GEMM for dense contraction
 // nests (`for i k. sum (for j. A.i.j * B.j.k)` recognized by the lowering).
 //
-//   C[m][n] (+)= sum_k A[m][k] * B[n][k]        (A, B K-major fp32 in HBM)
+//   C[m][n] (+)= isa_m isb_n sum_k A'[m][k] * B'[n][k]    (A', B' K-major fp16 pairs)
 //
-// tcgen05.mma kind::tf32, cta_group::1, M = 128, N = BN, fp32 accumulators in
-// TMEM.  fp32 parity with the f64 reference (<= 1e-4) uses 3xTF32: every
-// operand arrives as an exact-tf32 pair hi + lo (dx_tf32_split, written by the
-// generated operand prologues of contract.inc) and the MMA accumulates
-// hi*hi + hi*lo + lo*hi.
+// tcgen05.mma kind::f16, cta_group::1, M = 128, N = BN, fp32 accumulators in
+// TMEM.  fp32 parity with the f64 reference (<= 1e-4) uses fp16x3: every
+// operand row r is scaled by a power of two s_r (its max |v| into [2^13,
+// 2^14)) and arrives as a pair of fp16 images hi + lo (dx_f16_split: 11 + 11
+// significand bits, the precision of a tf32 pair), written by the generated
+// operand prologues of contract.inc; the MMA accumulates hi*hi + hi*lo +
+// lo*hi and the epilogue multiplies by the exact inverse scales.  kind::f16
+// runs twice the tf32 MMA rate on half the operand bytes (measured on the
+// MLP's 8192x1024x1024 GEMMs: 121 -> 84 us).
 // Operand tiles arrive by TMA (2-D tensor maps, SWIZZLE_128B, box 32 x rows)
 // into a STAGES-deep mbarrier ring; one elected thread issues the MMAs and
 // releases stages with tcgen05.commit; four epilogue warps drain TMEM with
 // tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = tile rows) chunk by chunk.
 
 #define DX_GEMM_BM 128
-#define DX_GEMM_BK 32  // fp32 per 128-byte swizzle row
+#define DX_GEMM_BK 64  // fp16 per 128-byte swizzle row
 
 __device__ __forceinline__ unsigned long long dx_umma_desc_sw128(unsigned saddr) {
   // K-major, SWIZZLE_128B canonical layout: 8-row x 128 B atoms, SBO = 1024 B
@@ -22,17 +26,33 @@ __device__ __forceinline__ unsigned long long dx_umma_desc_sw128(unsigned saddr)
 }
 
 template <int BN>
-__device__ __forceinline__ unsigned dx_idesc_tf32() {
-  // c_format F32 (bit 4), a/b format TF32 (2 at bits 7, 10), K-major, N>>3 at 17, M>>4 at 24
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(DX_GEMM_BM >> 4) << 24);
+__device__ __forceinline__ unsigned dx_idesc_f16() {
+  // c_format F32 (bit 4), a/b format F16 (0 at bits 7, 10), K-major, N>>3 at 17, M>>4 at 24
+  return (1u << 4) | ((unsigned)(BN >> 3) << 17) | ((unsigned)(DX_GEMM_BM >> 4) << 24);
 }
 
-__device__ __forceinline__ void dx_umma_tf32(unsigned tmem, unsigned long long da, unsigned long long db,
-                                             unsigned idesc, unsigned accumulate) {
+__device__ __forceinline__ void dx_umma_f16(unsigned tmem, unsigned long long da, unsigned long long db,
+                                            unsigned idesc, unsigned accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// fp16x3 split of a scaled double (|x| < 2^14): x ~ hi + lo, hi and lo fp16
+// (11-bit significands each: the pair carries ~22 bits, as a tf32 pair does)
+__device__ __forceinline__ void dx_f16_split(double x, unsigned short& hi, unsigned short& lo) {
+  float h;
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hi) : "f"((float)x));
+  asm("cvt.f32.f16 %0, %1;" : "=f"(h) : "h"(hi));
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"((float)(x - (double)h)));
+}
+// power-of-two scale putting a row's max |v| in [2^13, 2^14) (fp16 max 65504)
+__device__ __forceinline__ double dx_f16_scale(double max_abs) {
+  if (!(max_abs > 0.0) || !(max_abs < 1e300)) return 1.0;
+  int e;
+  frexp(max_abs, &e);  // max_abs < 2^e
+  return ldexp(1.0, 14 - e);
 }
 
 __device__ __forceinline__ void dx_umma_commit(unsigned long long* bar) {
@@ -56,20 +76,6 @@ __device__ __forceinline__ void dx_mbar_wait_bounded(unsigned long long* bar, un
   __trap();
 }
 
-__device__ __forceinline__ float dx_tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-// round to the nearest tf32 (10 explicit mantissa bits): the tensor core then
-// reads the value exactly instead of truncating it
-__device__ __forceinline__ float dx_tf32_rn(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
-}
-// 3xTF32 split of a double: v ~ hi + lo with hi, lo exact tf32 values
-// (error ~2^-24 |v|, the fp32 rounding level)
-__device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
-  hi = dx_tf32_rn((float)v);
-  lo = dx_tf32_rn((float)(v - (double)hi));
-}
-
-
 #define DX_TMEM_LD32(taddr, v)                                                                                    \
   asm volatile(                                                                                                   \
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"           \
@@ -82,7 +88,7 @@ __device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
 
 // Accumulation precision.  The tensor core adds into its fp32 accumulator
 // with truncation, so a long K drifts (measured 1.5e-4 rel at K = 1024 with
-// one accumulator).  Two remedies, both free on TMEM: the large hi*hi
+// one accumulator, 3xTF32).  Two remedies, both free on TMEM: the large hi*hi
 // products and the small residual products (hi*lo + lo*hi, ~2^-11 smaller)
 // go to separate accumulators, and every DX_GEMM_CHUNK k-blocks the
 // epilogue warps promote both into fp32 registers with round-to-nearest
@@ -95,11 +101,14 @@ __device__ __forceinline__ void dx_tf32_split(double v, float& hi, float& lo) {
 // MMA issuer.  mode 0: C = acc, 1: C += acc.  MERGED: the three products
 // share one accumulator (BN = 256 fits TMEM double-buffered; the promotion
 // every 32 k keeps the truncation error at fp32 level).
+// The row scales factor out of the k-sum: C[m][n] = isa_m isb_n sum_k
+// (s_m A)(s_n B); the epilogue applies them before the store.
 template <int BN, int STAGES, class CT, bool MERGED = false>
-__device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap* tal, const dx_tmap* tb,
-                                               const dx_tmap* tbl, long long M, long long N, long long K, CT* C,
-                                               long long ldc, long long mode, long long ksplit,
-                                               unsigned* tickets) {
+__device__ __forceinline__ void dx_gemm_f16x3(const dx_tmap* ta, const dx_tmap* tal, const dx_tmap* tb,
+                                              const dx_tmap* tbl, long long M, long long N, long long K, CT* C,
+                                              long long ldc, long long mode, long long ksplit, unsigned* tickets,
+                                              const float* isa, const float* isb) {
+  constexpr int BK = DX_GEMM_BK;  // K elements per 128-byte swizzle row
   constexpr unsigned A_BYTES = DX_GEMM_BM * 128, B_BYTES = BN * 128;
   constexpr unsigned STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   constexpr int NACC = MERGED ? 1 : 2;                   // accumulators per buffer
@@ -120,7 +129,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
   const int S = (int)(ksplit > 1 ? ksplit : 1);
   const int tile = (int)(blockIdx.x / S), part = (int)(blockIdx.x % S);
   const int m0 = (int)(tile / NT) * DX_GEMM_BM, n0 = (int)(tile % NT) * BN;
-  const int KBT = (int)((K + DX_GEMM_BK - 1) / DX_GEMM_BK);
+  const int KBT = (int)((K + BK - 1) / BK);
   const int kb0 = (int)((long long)part * KBT / S);
   const int KB = (int)((long long)(part + 1) * KBT / S) - kb0;
   const int NC = (KB + DX_GEMM_CHUNK - 1) / DX_GEMM_CHUNK;
@@ -154,7 +163,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
         if (kb >= STAGES) dx_mbar_wait_bounded(&empty[s], (unsigned)(((kb / STAGES) - 1) & 1));
         unsigned char* st = smem + s * STAGE_BYTES;
         dx_mbar_expect_tx(&full[s], STAGE_BYTES);
-        const int kc = (kb0 + kb) * DX_GEMM_BK;
+        const int kc = (kb0 + kb) * BK;
         dx_tma_2d(st, ta, kc, m0, &full[s]);
         dx_tma_2d(st + A_BYTES, tal, kc, m0, &full[s]);
         dx_tma_2d(st + 2 * A_BYTES, tb, kc, n0, &full[s]);
@@ -163,7 +172,7 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
     }
   } else if (warp == MMA_W) {
     if (lane == 0) {
-      const unsigned idesc = dx_idesc_tf32<BN>();
+      const unsigned idesc = dx_idesc_f16<BN>();
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
         if (c >= 2) dx_mbar_wait_bounded(&tempty[b], (unsigned)(((c >> 1) - 1) & 1));
@@ -177,15 +186,15 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
           const unsigned st = dx_smem_addr(smem + s * STAGE_BYTES);
           const unsigned first = kb == c * DX_GEMM_CHUNK;
 #pragma unroll
-          for (int kk = 0; kk < DX_GEMM_BK / 8; ++kk) {
+          for (int kk = 0; kk < 4; ++kk) {  // 16 fp16 (32 bytes) of K per MMA
             const unsigned long long ah = dx_umma_desc_sw128(st + kk * 32);
             const unsigned long long al = dx_umma_desc_sw128(st + A_BYTES + kk * 32);
             const unsigned long long bh = dx_umma_desc_sw128(st + 2 * A_BYTES + kk * 32);
             const unsigned long long bl = dx_umma_desc_sw128(st + 2 * A_BYTES + B_BYTES + kk * 32);
             const unsigned accum = !(first && kk == 0);
-            dx_umma_tf32(tbig, ah, bh, idesc, accum);
-            dx_umma_tf32(tsmall, ah, bl, idesc, MERGED ? 1u : accum);
-            dx_umma_tf32(tsmall, al, bh, idesc, 1u);
+            dx_umma_f16(tbig, ah, bh, idesc, accum);
+            dx_umma_f16(tsmall, ah, bl, idesc, MERGED ? 1u : accum);
+            dx_umma_f16(tsmall, al, bh, idesc, 1u);
           }
           dx_umma_commit(&empty[s]);  // frees the stage once these MMAs retire
         }
@@ -255,6 +264,12 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
       if (part > 0) mode = 1;
     }
     const long long row = m0 + wq * 32 + lane;
+    if (row < M) {  // undo the operand row scales (powers of two: exact)
+      const float ra = isa[row];
+      const int nc = n0 + cb;
+#pragma unroll
+      for (int j = 0; j < CW; ++j) acc[j] *= ra * (nc + j < N ? __ldg(isb + nc + j) : 0.f);
+    }
     if (row < M) {
       const int nc = n0 + cb;  // this warp's first output column
       CT* out = C + row * ldc + nc;
@@ -324,20 +339,19 @@ __device__ __forceinline__ void dx_gemm_tf32x3(const dx_tmap* ta, const dx_tmap*
 #define DX_GEMM_SMEM(BN, STAGES) (STAGES * (2 * DX_GEMM_BM * 128 + 2 * (BN)*128) + 1024)
 
 extern "C" __global__ void __launch_bounds__(192, 1)
-    dx_gemm_tf32x3_n128(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
-                        const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
-                        long long N, long long K, float* C, long long ldc, long long mode, long long ksplit,
-                        unsigned* tickets) {
-  dx_gemm_tf32x3<128, 3, float>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
+    dx_gemm_f16x3_n128(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
+                       const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
+                       long long N, long long K, float* C, long long ldc, long long mode, long long ksplit,
+                       unsigned* tickets, const float* isa, const float* isb) {
+  dx_gemm_f16x3<128, 3, float>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets, isa, isb);
 }
 extern "C" __global__ void __launch_bounds__(192, 1)
-    dx_gemm_tf32x3_n128_d(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
-                          const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
-                          long long N, long long K, double* C, long long ldc, long long mode, long long ksplit,
-                          unsigned* tickets) {
-  dx_gemm_tf32x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets);
+    dx_gemm_f16x3_n128_d(const __grid_constant__ dx_tmap ta, const __grid_constant__ dx_tmap tal,
+                         const __grid_constant__ dx_tmap tb, const __grid_constant__ dx_tmap tbl, long long M,
+                         long long N, long long K, double* C, long long ldc, long long mode, long long ksplit,
+                         unsigned* tickets, const float* isa, const float* isb) {
+  dx_gemm_f16x3<128, 3, double>(&ta, &tal, &tb, &tbl, M, N, K, C, ldc, mode, ksplit, tickets, isa, isb);
 }
-
 // f64 parity mode (dxl_options.float64): the same contraction class in
 // binary64, as the reference evaluates it (eval.cpp:500-514).  SIMT f64 FMA,
 // 64 x 64 output tile per 256-thread block (4 x 4 per thread), K in steps of

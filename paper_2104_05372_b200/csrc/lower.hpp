@@ -62,6 +62,7 @@ struct KArg {
   long long rowLen = 0, rows = 0;
   int boxRows = 0, swizzle = 0;
   int boxCols = 0;     // box width in elements (0: the whole row)
+  int f16 = 0;         // TMap over fp16 elements (2 bytes; the buffer is declared as U32 pairs)
 };
 
 struct Step {

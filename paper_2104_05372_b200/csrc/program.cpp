@@ -261,7 +261,7 @@ int Program::buildTensorMaps() {
     for (size_t j = 0; j < st.args.size(); ++j) {
       const KArg& a = st.args[j];
       if (a.k != KArg::TMap) continue;
-      size_t es = storageBytes(plan.bufs[a.buf].kind, plan.f64);
+      size_t es = a.f16 ? 2 : storageBytes(plan.bufs[a.buf].kind, plan.f64);
       CUtensorMap m;
       cuuint64_t dims[2] = {(cuuint64_t)a.rowLen, (cuuint64_t)a.rows};
       cuuint64_t strides[1] = {(cuuint64_t)(a.rowLen * es)};
@@ -270,7 +270,7 @@ int Program::buildTensorMaps() {
       CUtensorMapSwizzle sw = a.swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                               : a.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                 : CU_TENSOR_MAP_SWIZZLE_128B;
-      int rc = dxrt::check(cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      int rc = dxrt::check(cuTensorMapEncodeTiled(&m, a.f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                                   (void*)(devptr[a.buf] + a.off * es), dims, strides, box, estr,
                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),

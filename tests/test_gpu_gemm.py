@@ -2,8 +2,10 @@
 restatement (oracle/restate.py, pinned against the reference in
 tests/test_oracle.py) and, at small sizes, the reference evaluator itself.
 
-Tolerance: rtMaxRelDiff (eval.cpp:758-763) <= 1e-4 (f32 mode; 3xTF32 products
-accumulate in fp32 in TMEM, K-ordered within a tile)."""
+Tolerance: rtMaxRelDiff (eval.cpp:758-763) <= 1e-4 (f32 mode: fp16x3 --
+every operand row scaled by a power of two and split into two fp16 values,
+the hi*hi + hi*lo + lo*hi products accumulated in fp32 in TMEM, K-ordered
+within a tile)."""
 import numpy as np
 import pytest
 
@@ -53,8 +55,8 @@ def test_gemm_repeat_deterministic(ctx):
     np.testing.assert_array_equal(a, b)
 
 
-def test_gemm_precision_beats_plain_tf32(ctx):
-    """3xTF32: error ~fp32 rounding, far below a single tf32 pass (~1e-3)."""
+def test_gemm_precision_at_fp32_level(ctx):
+    """fp16x3: error ~fp32 rounding, far below a single fp16 or tf32 pass (~1e-3)."""
     m = n = k = 512
     x, y = P.contraction_inputs(m, n, k, seed=7)
     (c,) = dx.Program(P.contraction(m, n, k), ctx=ctx)(x, y)
@@ -66,7 +68,7 @@ def test_gemm_precision_beats_plain_tf32(ctx):
 def test_matmul_fwd_uses_gemm(ctx):
     x, y = P.matmul_inputs(256)
     prog = dx.Program(P.matmul_fwd(256), ctx=ctx)
-    assert "tcgen05 gemm 256x256x256" in prog.plan
+    assert "tcgen05 gemm fp16x3 256x256x256" in prog.plan
     (z,) = prog(x, y)
     assert oracle.rel_diff(z, restate.matmul_fwd(x, y).ravel()) <= 1e-4
 
@@ -83,3 +85,34 @@ def test_split_k_plan_and_determinism(ctx):
     b = prog(x, y)[0]
     np.testing.assert_array_equal(a, b)
     assert oracle.rel_diff(a, restate.contraction(x, y).ravel()) <= 1e-4
+
+
+@pytest.mark.parametrize("xk,yk", [(True, False), (False, True)])
+def test_fp16x3_row_scales_cover_fp32_range(ctx, xk, yk):
+    """Per-row power-of-two scales: rows of both operands spanning 1e-30 ..
+    1e30 (far outside fp16's range), zero rows, and K not a multiple of 8
+    still give fp32-level results (each output is one row pair's dot product,
+    so the scales factor out exactly)."""
+    m, n, k = 160, 136, 100
+    x, y = P.contraction_inputs(m, n, k, xk, yk, seed=11)
+    x = np.array(x, dtype=np.float32)
+    y = np.array(y, dtype=np.float32)
+    xr = np.logspace(-15, 15, m).astype(np.float32)
+    yr = np.logspace(15, -15, n).astype(np.float32)
+    if xk:  # x is [m][k]
+        x *= xr[:, None]
+        x[7] = 0.0
+    else:   # x is [k][m]
+        x *= xr[None, :]
+        x[:, 7] = 0.0
+    if yk:  # y is [n][k]
+        y *= yr[:, None]
+    else:   # y is [k][n]
+        y *= yr[None, :]
+    (c,) = dx.Program(P.contraction(m, n, k, xk, yk), ctx=ctx)(x, y)
+    want = restate.contraction(x, y, xk, yk)
+    mag = restate.contraction(np.abs(x), np.abs(y), xk, yk)  # sum |x||y| per output
+    c = np.asarray(c, dtype=np.float64).reshape(m, n)
+    ok = mag > 0
+    assert np.max(np.abs(c - want)[ok] / mag[ok]) <= 1e-6
+    assert np.all(c[7] == 0.0)

@@ -115,9 +115,9 @@ def test_contraction_recognized_as_gemm():
     the generic loop kernel."""
     for xk, yk in ((True, False), (False, True), (False, False), (True, True)):
         p = dx.Program(P.contraction(200, 136, 68, xk, yk), ctx=None).plan
-        assert "tcgen05 gemm 200x136x68" in p and p.count("gemm operand") == 2, p
+        assert "tcgen05 gemm fp16x3 200x136x68" in p and p.count("gemm operand ") - p.count("gemm operand row max") == 2, p
     p = dx.Program(P.contraction(64, 64, 6), ctx=None).plan      # K padded to 8 in the operands
-    assert "tcgen05 gemm 64x64x6" in p
+    assert "tcgen05 gemm fp16x3 64x64x6" in p
     assert "tcgen05" not in dx.Program(P.contraction(64, 64, 64), ctx=None, float64=True).plan
     src = dx.Program(P.contraction(64, 64, 64), ctx=None).source
     sass = _sass(src)
@@ -131,7 +131,8 @@ def test_mlp_and_matmul_grad_on_tensor_cores():
     p = dx.Program(P.mlp_grad(8192, 1024, 1024, 1024), ctx=None).plan
     assert p.count("tcgen05 gemm") == 5, p
     assert p.count("(+=)") == 0  # cells right after their zero-fill are stored, not accumulated
-    assert "zero b" not in p.split("---")[0].split("[1]")[1]  # only the scalar loss cell is zeroed
+    zeros = [l for l in p.split("---")[0].splitlines() if " zero b" in l]
+    assert all(l.endswith("(1)") or l.endswith("(1024)") for l in zeros), zeros  # the loss cell and row-max words only
     assert p.count("copy b") == 2  # the cotangent deltas move into the zero-pending weight cells
     assert "8589934592" not in p  # no B*H*I tape
     p = dx.Program(P.matmul_grad(256), ctx=None).plan
@@ -171,14 +172,17 @@ def test_tiny_map_bodies_keep_three_vector_loads_in_flight():
 
 
 def test_transposed_gemm_operands_use_a_tiled_prologue():
-    # an operand read along its row variable (stride 1 over rows) goes through a
-    # 32x32 shared-memory transpose; a K-contiguous operand is a vector map
+    # an operand read along its row variable (stride 1 over rows) goes through
+    # 8-row blocks transposed in shared memory; a K-contiguous operand is split
+    # warp per row (both with per-row fp16 scales)
     prog = dx.Program(P.contraction(130, 260, 36, True, False), ctx=None)
-    ops = [l for l in prog.plan.split("\n") if "gemm operand" in l]
+    ops = [l for l in prog.plan.split("\n") if "gemm operand" in l and "row max" not in l]
     assert len(ops) == 2
     assert "tiled transpose" not in ops[0] and "tiled transpose" in ops[1]
-    assert "__shared__ float th[32][33]" in prog.source
-    assert "reinterpret_cast<float4*>(hi)[t]" in prog.source
+    assert "gemm operand row max" in prog.plan      # per-row max pass of the transposed operand
+    assert "unsigned short th[32][34]" in prog.source
+    assert "for (long long r = blockIdx.x * 8LL + (threadIdx.x >> 5)" in prog.source
+    assert prog.source.count("dx_f16_scale(") >= 2
 
 
 EMPTY_PROGRAMS = [
@@ -222,7 +226,7 @@ def test_mlp_world2_plan_is_data_parallel():
     for rank in (0, 1):
         plan = dx.Program(P.mlp_grad(b, i, h, o), ctx=None, rank=rank, world=2).plan.split("---")[0]
         assert plan.count("tcgen05 gemm") == 5, plan
-        assert "gemm 1024x256x256" in plan or "gemm 1024x" in plan  # M-split: the rank's 1024 batch rows
+        assert "gemm fp16x3 1024x" in plan  # M-split: the rank's 1024 batch rows
         assert "allreduce" not in plan, plan
         merges = [l for l in plan.splitlines() if "merge" in l]
         assert len(merges) == 1, plan
