@@ -4794,8 +4794,20 @@ HV Lowering::serialKernel(const HEnvP& env, const ExprPtr& e, const ValuePtr& an
 
 std::string Plan::summary() const {
   std::ostringstream o;
+  long long bytes = 0, big = 0;  // device buffers (partials are sized by the grid at prepare: excluded)
+  int bigB = -1;
+  for (size_t i = 0; i < bufs.size(); ++i) {
+    const BufDecl& b = bufs[i];
+    if (b.role == BufDecl::Partial) continue;
+    const long long by = std::max(1LL, b.elems) * (long long)storageBytesOf(b.kind, f64);
+    bytes += by;
+    if (by > big) big = by, bigB = (int)i;
+  }
+  char mb[32];
+  snprintf(mb, sizeof mb, "%.1f", bytes / 1048576.0);
   o << "plan: " << steps.size() << " steps, " << numKernels << " kernels, " << bufs.size()
-    << " buffers, " << (f64 ? "f64" : "f32") << ", world " << world << "\n";
+    << " buffers (" << mb << " MiB; largest b" << bigB << " " << big / 1048576 << " MiB), " << (f64 ? "f64" : "f32")
+    << ", world " << world << "\n";
   for (size_t i = 0; i < steps.size(); ++i) {
     const Step& s = steps[i];
     o << "  [" << i << "] ";

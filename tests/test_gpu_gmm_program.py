@@ -73,3 +73,25 @@ def test_gmm_program_dispatches_to_fused_kernels(ctx, n, K, gamma, m):
     bad[1, 0] = 0.0
     with pytest.raises(dx.DexError):
         fast.set_input(5, 0, bad)
+
+
+
+def test_gmm_program_f64_mode_at_baseline_dims(ctx):
+    """The ADBench GMM program at BASELINE configs[2]'s dimensions (d = 64,
+    K = 200) in the f64 parity mode (the generic lowering in binary64, as the
+    reference evaluates; the fused fp16x3 class is f32-only): objective and
+    every gradient entry within rtMaxRelDiff 1e-9 of the fp64 restatement.
+    n = 1000: the generic plan keeps per-(point, component) d x d tapes
+    (6.5 GB each here, 35 GB in all -- the plan header reports it), so the
+    full n = 1M runs on the fused class only (tests/test_gpu_gmm.py)."""
+    n, d, K = 1000, 64, 200
+    a, mu, icf, x = G.gmm_inputs(n, d, K, seed=5)
+    tabs = P.gmm_tables(d)
+    mx, ma = P.gmm_stabilizers(a, mu, icf, x)
+    prog = dx.Program(P.gmm_program(n, d, K), ctx=ctx, float64=True)
+    assert "fused GMM" not in prog.plan
+    err, da, dm, di = prog(x, mx, ma, *tabs, [a, mu, icf])
+    werr, wda, wdm, wdi = G.gmm_objective_grad(a, mu, icf, x)
+    assert oracle.rel_diff(err, np.array([werr])) <= 1e-9
+    for g, w in ((da, wda), (dm, wdm), (di, wdi)):
+        assert oracle.rel_diff(g, np.ravel(w)) <= 1e-9
