@@ -49,6 +49,9 @@ UNIT = "evals/s"
 L2_BYTES = 126 * 1024 * 1024
 
 
+# the tcgen05 GEMM entry points (f32 / f64 output)
+GEMM_KERNELS = ("dx_gemm_f16x3_n128", "dx_gemm_f16x3_n128_d")
+
 def input_bytes(spec):
     """Bytes of one step's inputs (all leaves / arrays)."""
     if spec.get("gmm") and "src" not in spec:
@@ -92,7 +95,7 @@ def _config_spec(name, world):
         x, y = P.matmul_inputs(n)
         return dict(metric="matmul n=256 fwd+grad evals/s", src=P.matmul_grad(n), inputs=[[x], [y]],
                     bound="tensor", work=4 * n ** 3,
-                    work_by_kernel={"dx_gemm_f16x3_n128": 2 * n ** 3, "dx_gemm_f16x3_n128_d": 2 * n ** 3}, work_basis="2n^3 (forward) + 2n^3 (dX) flops",
+                    work_by_kernel={kn: 2 * n ** 3 for kn in GEMM_KERNELS}, work_basis="2n^3 (forward) + 2n^3 (dX) flops",
                     workload="pointful matmul sum(x.y) value and gradient wrt x, n=256 (BASELINE configs[0])",
                     extra={"n": n}, out_bytes=4 + n * n * 4)
     if name == "mlp":
@@ -102,8 +105,7 @@ def _config_spec(name, world):
                     src=P.mlp_grad(b, i, h, o), inputs=[[x], [w1, w2]], row_inputs=(0,), bound="tensor",
                     work=5 * 2 * 8192 * 1024 * 1024,
                     # every GEMM launch of the step is 8192 x 1024 x 1024 (per-launch mean time)
-                    work_by_kernel={"dx_gemm_f16x3_n128": 2 * 8192 * 1024 * 1024,
-                                    "dx_gemm_f16x3_n128_d": 2 * 8192 * 1024 * 1024},
+                    work_by_kernel={kn: 2 * 8192 * 1024 * 1024 for kn in GEMM_KERNELS},
                     work_basis="fwd 2 GEMMs + bwd dW2, dH, dW1 (2*B*1024^2 flops each)",
                     workload="2-layer MLP, square activation, loss sum(y^2), grads over (W1 & W2) "
                              "(BASELINE configs[4])", extra={"batch_total": b}, out_bytes=4 + 2 * 1024 * 1024 * 4)

@@ -47,6 +47,24 @@ __device__ __forceinline__ void dx_f16_split(double x, unsigned short& hi, unsig
   asm("cvt.f32.f16 %0, %1;" : "=f"(h) : "h"(hi));
   asm("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"((float)(x - (double)h)));
 }
+// the same split of an fp32 value: x - hi is exact in fp32 (hi is x rounded
+// to 11 significand bits), so the images equal dx_f16_split's bit for bit
+__device__ __forceinline__ void dx_f16_splitf(float x, unsigned short& hi, unsigned short& lo) {
+  float h;
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hi) : "f"(x));
+  asm("cvt.f32.f16 %0, %1;" : "=f"(h) : "h"(hi));
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"(__fsub_rn(x, h)));
+}
+// the scale as fp32 when it is a normal fp32 power of two (0 otherwise)
+__device__ __forceinline__ float dx_f16_scale_f(double sc) {
+  return sc >= 0x1p-126 && sc <= 0x1p126 ? (float)sc : 0.f;
+}
+// split x * sc: fp32 when the scale fits (x * scf is the exact product rounded
+// once to fp32, as (float)((double)x * sc) is), fp64 otherwise
+__device__ __forceinline__ void dx_f16_split_sc(float x, double sc, float scf, unsigned short& hi, unsigned short& lo) {
+  if (scf != 0.f) dx_f16_splitf(__fmul_rn(x, scf), hi, lo);
+  else dx_f16_split((double)x * sc, hi, lo);
+}
 // power-of-two scale putting a row's max |v| in [2^13, 2^14) (fp16 max 65504)
 __device__ __forceinline__ double dx_f16_scale(double max_abs) {
   if (!(max_abs > 0.0) || !(max_abs < 1e300)) return 1.0;
