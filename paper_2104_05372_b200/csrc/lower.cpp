@@ -2053,7 +2053,12 @@ class Lowering {
       s.off = "0";
       s.kind = lv[l].kind;
       g.localDepth[s.base] = g.serial ? 0 : g.depth();
-      g.line(ctype(s.kind) + " " + s.base + "[" + lit(std::max(1LL, (long long)lv[l].count)) + "]" + (zero ? " = {}" : "") + ";");
+      // a scalar float accumulator starts at -0.0: -0.0 + x == x for every x
+      // (+0.0 + x is not an identity for x = -0.0), so the compiler folds the
+      // first add and contracts the next multiply-add into one FFMA
+      const bool negZero = zero && lv[l].count == 1 && (s.kind == SK::F || s.kind == SK::D);
+      g.line(ctype(s.kind) + " " + s.base + "[" + lit(std::max(1LL, (long long)lv[l].count)) + "]" +
+             (negZero ? " = {(" + ctype(s.kind) + ")-0.0}" : zero ? " = {}" : "") + ";");
       slots.push_back(s);
     }
     return slots;
