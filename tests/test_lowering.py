@@ -173,14 +173,17 @@ def test_tiny_map_bodies_keep_three_vector_loads_in_flight():
 
 def test_transposed_gemm_operands_use_a_tiled_prologue():
     # an operand read along its row variable (stride 1 over rows) goes through
-    # 8-row blocks transposed in shared memory; a K-contiguous operand is split
-    # warp per row (both with per-row fp16 scales)
+    # 32 x 64 tiles transposed in shared memory, after a column-max pass with a
+    # thread per row; a K-contiguous operand is split warp per row (16-byte
+    # loads when aligned); both with per-row fp16 scales, fp32 arithmetic
     prog = dx.Program(P.contraction(130, 260, 36, True, False), ctx=None)
     ops = [l for l in prog.plan.split("\n") if "gemm operand" in l and "row max" not in l]
     assert len(ops) == 2
     assert "tiled transpose" not in ops[0] and "tiled transpose" in ops[1]
     assert "gemm operand row max" in prog.plan      # per-row max pass of the transposed operand
-    assert "unsigned short th[32][34]" in prog.source
+    assert "unsigned short th[64 * 33 + 1]" in prog.source
+    assert "atomicMax(mx + r, __float_as_uint(mm))" in prog.source
+    assert "dx_f16_split_sc(" in prog.source
     assert "for (long long r = blockIdx.x * 8LL + (threadIdx.x >> 5)" in prog.source
     assert prog.source.count("dx_f16_scale(") >= 2
 
