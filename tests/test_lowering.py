@@ -248,3 +248,32 @@ def test_gmm_program_recognizer():
     assert dx.gmm_program_match(src.replace("0.5 * sq", "0.25 * sq")) is None
     assert dx.gmm_program_match(src.replace("log s", "s")) is None
     assert dx.gmm_program_match(P.kmeans_cost_grad(10, 2, 2)) is None
+
+
+def test_fp32_split_matches_fp64_split():
+    """The fp32 operand prologue path (dx_f16_split_sc, dx_gemm.cuh) claims
+    bit-identical fp16 hi/lo images to the fp64 form dx_f16_split((double)x * sc):
+    x * sc with sc a power of two is the exact product rounded once to fp32 in
+    both, and x - hi is exact in fp32.  Checked here with numpy's round-to-nearest
+    conversions on values spanning the fp32 range and every scale a row can get
+    (max |v| of the row into [2^13, 2^14))."""
+    import numpy as np
+    rng = np.random.default_rng(7)
+    x = (rng.standard_normal(200_000) * np.exp2(rng.integers(-60, 60, 200_000))).astype(np.float32)
+    x[:1000] = 0.0
+    x[1000:1010] = np.float32(-0.0)
+    for e in range(-60, 61, 7):
+        row = x[np.abs(x) < np.float32(2.0 ** e)]
+        if row.size == 0:
+            continue
+        sc = 2.0 ** (14 - e)                      # dx_f16_scale for a row max in [2^(e-1), 2^e)
+        # fp32 path
+        xs = row * np.float32(sc)
+        hi = xs.astype(np.float16)
+        lo = (xs - hi.astype(np.float32)).astype(np.float16)
+        # fp64 path
+        xd = row.astype(np.float64) * sc
+        hi_d = xd.astype(np.float32).astype(np.float16)
+        lo_d = (xd - hi_d.astype(np.float64)).astype(np.float32).astype(np.float16)
+        assert np.array_equal(hi.view(np.uint16), hi_d.view(np.uint16)), e
+        assert np.array_equal(lo.view(np.uint16), lo_d.view(np.uint16)), e
