@@ -210,8 +210,18 @@ __device__ __forceinline__ void dx_gemm_f16x3(const dx_tmap* ta, const dx_tmap* 
             const unsigned long long bh = dx_umma_desc_sw128(st + 2 * A_BYTES + kk * 32);
             const unsigned long long bl = dx_umma_desc_sw128(st + 2 * A_BYTES + B_BYTES + kk * 32);
             const unsigned accum = !(first && kk == 0);
-            dx_umma_f16(tbig, ah, bh, idesc, accum);
-            dx_umma_f16(tsmall, ah, bl, idesc, MERGED ? 1u : accum);
+            if (!MERGED && BN <= 128) {
+              // [B hi ; B lo] are contiguous SW128 row groups and [big | small]
+              // contiguous TMEM columns: hi*hi and hi*lo as ONE N = 2 BN MMA
+              // (same products, same accumulators, same order), so A hi is
+              // read from shared memory once per k-step instead of twice --
+              // the SS-mode MMAs are shared-memory-read bound (128 B/clk for
+              // three N = 128 products, 107 B/clk this way)
+              dx_umma_f16(tbig, ah, bh, dx_idesc_f16<2 * BN>(), accum);
+            } else {
+              dx_umma_f16(tbig, ah, bh, idesc, accum);
+              dx_umma_f16(tsmall, ah, bl, idesc, MERGED ? 1u : accum);
+            }
             dx_umma_f16(tsmall, al, bh, idesc, 1u);
           }
           dx_umma_commit(&empty[s]);  // frees the stage once these MMAs retire
